@@ -1,0 +1,507 @@
+#!/usr/bin/env python
+"""Benchmark of the SMM-Conv forward path on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+A *step* is one forward pass of every layer of BASELINE.json config C
+(default 2 = the ResNet-style 3x3 sweep, N in {1, 32}) over its synthetic
+batch.  Metric: conv GFLOP/s = sum of 2*N*c_o*h'*w'*c_i*k_h*k_w over the step's
+layers / step time.  Inputs are resident in HBM; three replicas of every
+layer's buffers are rotated so that > 2x L2 (126 MB) is touched between reuses
+of any buffer.  The K timed steps are captured once as a CUDA graph (with
+external event nodes between layers) and replayed once between a barrier +
+synchronize on both sides; time is the CUDA-event time, max over ranks.
+
+Multi-GPU (torchrun): config 2/1/3/4 run weak-scaled (every rank runs the
+full config on its own samples, no collective).  Config 5 shards the N=256
+layers by batch (strong) and the 512@7 N=8 layer by output channel with an
+NCCL all-gather.
+
+``--impl reference`` times the reference's CPU algorithm (the C restatement
+of smm_conv_parallel in oracle/, all host threads) on a bounded sample of the
+same workload; rank 0 only.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+from paper_2411_15659_b200.tensors import synthetic_layer  # noqa: E402
+from paper_2411_15659_b200.workloads import CONFIGS, layer_seed  # noqa: E402
+
+METRIC = ("conv GFLOP/s per layer shape (2·N·c_o·h'·w'·c_i·kh·kw/time), "
+          "% FP32/HBM roofline")
+L2_BYTES = 126 * 1024 * 1024
+FFMA_PER_SM_PER_CLK = 128
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="ffma", choices=["ffma", "exact"])
+    ap.add_argument("--replicas", type=int, default=0, help="0 = auto (>2x L2 between reuses)")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--details", default="", help="write per-layer details JSON here")
+    return ap.parse_args()
+
+
+def peaks():
+    p = {}
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        try:
+            p = json.loads(f.read_text())
+        except ValueError:
+            p = {}
+    return p
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons while running."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+        sm, mx, pw, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [s.strip() for s in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                pw.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "power_w_max": max(pw) if pw else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------- dist
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def layer_plan(config, rank, world):
+    """Per-rank layers: (name, n_local, geom, seed, shard) — shard is
+    'replica' (weak), 'batch' (strong, N split) or 'cout' (c_o split)."""
+    out = []
+    for li, (name, n, g) in enumerate(CONFIGS[config]["layers"]):
+        seed = layer_seed(config, li)
+        if config == 5 and world > 1:
+            if "coshard" in name:
+                out.append((name, n, g, seed, "cout"))
+            else:
+                lo, hi = n * rank // world, n * (rank + 1) // world
+                out.append((name, hi - lo, g, seed + 100003 * rank, "batch"))
+        else:
+            out.append((name, n, g, seed + 100003 * rank, "replica"))
+    return out
+
+
+# --------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import smm_oracle as orc
+    from paper_2411_15659_b200 import repack_weights
+    threads = orc.host_threads()
+    layers = CONFIGS[args.config]["layers"]
+    samples = []
+    for li, (name, n, g) in enumerate(layers):
+        x, w = synthetic_layer(g, 1, layer_seed(args.config, li))
+        samples.append((g, np.ascontiguousarray(x[0]), repack_weights(w, g)))
+    flops_per_step = sum(g.flops(1) for g, _, _ in samples)
+
+    def step():
+        for g, x, ws in samples:
+            orc.smm_conv_c(x, ws, g, threads=threads)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    value = flops_per_step * args.steps / dt / 1e9
+    sample = (f"1 sample of each of the {len(layers)} config-{args.config} layers per step "
+              f"(the reference loops samples sequentially, estimator.py:123-124)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"BASELINE config {args.config}: {CONFIGS[args.config]['title']}",
+                   "layers": [nm for nm, _, _ in layers], "parallelism": "cpu threads"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": threads,
+                         "kind": "port", "sample": sample,
+                         "impl": "oracle/smm_oracle.c: C restatement of smm_conv_parallel "
+                                 "(Algorithm 2, smm.py:254-306), bitwise-pinned to the reference"},
+        "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_15659_b200 import _native, device
+    from paper_2411_15659_b200.parallel import all_gather_cout, cout_shard
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    plan = layer_plan(args.config, rank, world)
+
+    # ---- data: synthetic host arrays -> HBM, R replicas
+    layers = []
+    for name, n, g, seed, shard in plan:
+        x, w = synthetic_layer(g, n, seed)
+        ws = np.ascontiguousarray(w.transpose(1, 3, 2, 0))
+        c_lo, c_hi = 0, g.out_channels
+        gg = g
+        if shard == "cout":
+            c_lo, c_hi = cout_shard(g.out_channels, rank, world)
+            ws = np.ascontiguousarray(ws[..., c_lo:c_hi])
+            from paper_2411_15659_b200 import ConvGeometry
+            gg = ConvGeometry(g.in_channels, c_hi - c_lo, g.in_h, g.in_w, g.k_h, g.k_w,
+                              g.stride_h, g.stride_w, g.pad_h, g.pad_w)
+        layers.append(dict(name=name, n=n, g=g, gl=gg, shard=shard, x_host=x, w_host=ws,
+                           flops=gg.flops(n), c_range=(c_lo, c_hi)))
+    step_bytes = sum(4 * (L["x_host"].size + L["w_host"].size + L["n"] * L["gl"].out_channels
+                          * L["gl"].out_h * L["gl"].out_w) for L in layers)
+    R = args.replicas or max(1, min(8, -(-3 * L2_BYTES // max(step_bytes, 1)) + 1))
+    for L in layers:
+        xd = torch.from_numpy(L["x_host"]).to(dev)
+        wd = torch.from_numpy(L["w_host"]).to(dev)
+        L["x"] = [xd] + [xd.clone() for _ in range(R - 1)]
+        L["w"] = [wd] + [wd.clone() for _ in range(R - 1)]
+        shape = (L["n"],) + L["gl"].output_shape
+        L["y"] = [torch.empty(shape, device=dev) for _ in range(R)]
+        need = _native.workspace_bytes(L["gl"], L["n"], args.mode)
+        L["ws"] = torch.empty(max(need, 16), dtype=torch.uint8, device=dev)
+        if L["shard"] == "cout":
+            L["gather"] = torch.empty((world,) + shape, device=dev)
+            L["full"] = torch.empty((L["n"],) + L["g"].output_shape, device=dev)
+
+    def run_layer(L, r):
+        if L["n"] == 0:
+            return
+        device.conv2d(L["x"][r], L["w"][r], L["gl"], mode=args.mode, out=L["y"][r],
+                      workspace=L["ws"])
+        if L["shard"] == "cout":
+            all_gather_cout(L["y"][r], L["gather"], L["full"], L["g"].out_channels, world)
+
+    def step(r, events=None):
+        for li, L in enumerate(layers):
+            run_layer(L, r)
+            if events is not None:
+                events[li + 1].record()
+
+    # ---- warm-up (eager), then capture the K timed steps as one graph
+    for s in range(args.warmup):
+        step(s % R)
+    torch.cuda.synchronize()
+    launches_before = _native.launch_count()
+    nl = len(layers)
+    ev = [[torch.cuda.Event(enable_timing=True, external=True) for _ in range(nl + 1)]
+          for _ in range(args.steps)]
+    graph = None
+    use_graph = world == 1 or all(L["shard"] != "cout" for L in layers)
+    if use_graph:
+        graph = torch.cuda.CUDAGraph()
+        cap_stream = torch.cuda.Stream(device=dev)
+        cap_stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cap_stream):
+            with torch.cuda.graph(graph, stream=cap_stream):
+                for s in range(args.steps):
+                    ev[s][0].record()
+                    step(s % R, ev[s])
+        torch.cuda.synchronize()
+    gpu_launches = _native.launch_count() - launches_before
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.2)
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start.record()
+    if graph is not None:
+        graph.replay()
+    else:
+        launches_before = _native.launch_count()
+        for s in range(args.steps):
+            ev[s][0].record()
+            step(s % R, ev[s])
+        gpu_launches = _native.launch_count() - launches_before
+    end.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    elapsed_ms = start.elapsed_time(end)
+    # per-layer device time inside the timed region
+    per_layer = [[ev[s][li].elapsed_time(ev[s][li + 1]) for s in range(args.steps)]
+                 for li in range(nl)]
+    # soak for the clock record when the timed region is short
+    soak_t0 = time.perf_counter()
+    while graph is not None and time.perf_counter() - soak_t0 < 1.0 and elapsed_ms < 1000:
+        graph.replay()
+        torch.cuda.synchronize()
+    clk = clocks.stop()
+
+    t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    flops_rank = sum(L["flops"] for L in layers)
+    ft = torch.tensor([float(flops_rank)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ft)
+    flops_total_step = float(ft.item())
+    value = flops_total_step * args.steps / (max_ms / 1e3) / 1e9
+
+    # ---- roofline of the dominant kernel (largest share of the step)
+    pk = peaks()
+    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+    sm_max = float(pk.get("sm_max_mhz", 1965.0))
+    fp32_peak_tf = sm_count * FFMA_PER_SM_PER_CLK * 2 * sm_max * 1e6 / 1e12
+    hbm_peak = float(pk.get("hbm_gbs", 6650.0))
+    details = []
+    for li, L in enumerate(layers):
+        d = per_layer[li]
+        avg = sum(d) / len(d)
+        tf = L["flops"] / (avg / 1e3) / 1e12 if avg > 0 else 0.0
+        gl = L["gl"]
+        byts = gl.compulsory_bytes(L["n"])
+        t_roof = max(L["flops"] / (fp32_peak_tf * 1e12), byts / (hbm_peak * 1e9))
+        details.append({
+            "layer": L["name"], "n": L["n"], "shard": L["shard"],
+            "gflop": round(L["flops"] / 1e9, 4), "ms_avg": round(avg, 5),
+            "ms_min": round(min(d), 5), "tflops": round(tf, 3),
+            "frac_fp32_peak": round(tf / fp32_peak_tf, 4),
+            "frac_roofline": round(t_roof * 1e3 / avg, 4) if avg > 0 else None,
+            "flop_per_byte": round(L["flops"] / byts, 1),
+            "plan": _native.plan_describe(gl, L["n"], args.mode) if L["n"] else "",
+            "launches_per_call": _native.plan_launches(gl, L["n"], args.mode) if L["n"] else 0})
+    dom = max(details, key=lambda d: d["ms_avg"])
+    traffic = None
+    tfile = ROOT / "profiles" / "traffic.json"
+    if tfile.exists():
+        try:
+            traffic = json.loads(tfile.read_text()).get(dom["layer"])
+        except ValueError:
+            traffic = None
+    roofline = {"bound": "fp32", "achieved": dom["tflops"], "peak": round(fp32_peak_tf, 2),
+                "unit": "TFLOP/s", "frac": dom["frac_fp32_peak"], "traffic": traffic,
+                "kernel": f"conv_ffma_kernel ({dom['layer']}: {dom['plan']})",
+                "peak_source": f"nominal FP32 FFMA peak {sm_count} SM x 128 x 2 x {sm_max:.0f} MHz "
+                               "(sm_max_mhz of MEASURED_PEAKS.json; no measured FP32 peak exists)",
+                "achieved_def": "dense algorithmic FLOPs of one launch / its avg CUDA-event "
+                                "duration inside the timed graph"}
+
+    # ---- e2e: host buffers through the C ABI host entry (H2D + conv + D2H)
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, layers, world, dev)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, layers)
+
+    if rank == 0:
+        par = {"replica": f"dp{world}" if world > 1 else "single",
+               "batch": f"batch-shard{world}", "cout": f"cout-shard{world}"}
+        shards = sorted({L["shard"] for L in layers})
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(max_ms / args.steps, 5), "higher_is_better": True,
+            "scaling": "strong" if (args.config == 5 and world > 1) else "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"BASELINE config {args.config}: {CONFIGS[args.config]['title']}",
+                       "layers": [L["name"] for L in layers],
+                       "mode": args.mode,
+                       "parallelism": "+".join(par[s] for s in shards),
+                       "l2": f"{R} rotating replicas of every buffer "
+                             f"({R * step_bytes / 2**20:.0f} MiB > 2x L2 between reuses)"
+                             if R > 1 else "inputs larger than L2",
+                       "timing": "K steps captured as one CUDA graph, replayed once; "
+                                 "CUDA events; max over ranks"},
+            "gpu_launches": gpu_launches,
+            "clocks": clk,
+            "roofline": roofline,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "layers": details,
+        }
+        if args.details:
+            Path(args.details).write_text(json.dumps(line, indent=1))
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(args, layers, world, dev):
+    """Same metric through smmc_conv2d_fwd_f32_host with pinned host buffers:
+    every step copies each layer's input + weights H2D and the output D2H."""
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_15659_b200 import _native
+    lib = _native.lib()
+    bufs = []
+    h2d = d2h = 0
+    for L in layers:
+        if L["n"] == 0:
+            continue
+        x = torch.from_numpy(L["x_host"]).pin_memory()
+        w = torch.from_numpy(L["w_host"]).pin_memory()
+        y = torch.empty((L["n"],) + L["gl"].output_shape).pin_memory()
+        g = _native.Geom.of(L["gl"], L["n"])
+        bufs.append((x, w, y, g))
+        h2d += x.numel() * 4 + w.numel() * 4
+        d2h += y.numel() * 4
+    mode = _native.mode_id(args.mode)
+    devi = dev.index
+
+    def step():
+        for x, w, y, g in bufs:
+            _native.check(lib.smmc_conv2d_fwd_f32_host(
+                ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(w.data_ptr()),
+                ctypes.c_void_p(y.data_ptr()), ctypes.byref(g), mode, devi), "e2e")
+
+    step()
+    steps = max(1, min(args.steps, 10))
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    dt = time.perf_counter() - t0
+    t = torch.tensor([dt], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dt = float(t.item())
+    flops = sum(L["flops"] for L in layers) * world
+    return {"value": round(flops * steps / dt / 1e9, 2), "unit": "GFLOP/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
+            "path": "smmc_conv2d_fwd_f32_host (C ABI, pinned host buffers, synchronous), "
+                    "wall clock, max over ranks"}
+
+
+def cpu_baseline(args, layers):
+    """The reference's CPU algorithm (C restatement of smm_conv_parallel,
+    all host threads) on one sample of each layer, repeated for ~10 s; also
+    cross-checks our GPU output of sample 0 against it."""
+    import torch
+
+    from oracle import smm_oracle as orc
+    threads = orc.host_threads()
+    flops = 0
+    worst = 0.0
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        for L in layers:
+            if L["n"] == 0:
+                continue
+            ref = orc.smm_conv_c(L["x_host"][0], L["w_host"], L["gl"], threads=threads)
+            flops += L["gl"].flops(1)
+            if reps == 0:
+                yd = L["y"][0][0].cpu().numpy()
+                worst = max(worst, orc.max_abs_ratio(yd, ref))
+        reps += 1
+        if time.perf_counter() - t0 >= args.cpu_seconds:
+            break
+    dt = time.perf_counter() - t0
+    torch.cuda.synchronize()
+    return {"value": round(flops / dt / 1e9, 3), "unit": "GFLOP/s", "cores": threads,
+            "kind": "port",
+            "sample": f"sample 0 of each of the {len(layers)} layers, {reps} passes "
+                      f"({dt:.1f} s), C restatement of smm_conv_parallel (Algorithm 2)",
+            "gpu_vs_oracle_max_err_ratio": worst}
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

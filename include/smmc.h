@@ -1,0 +1,148 @@
+/*
+ * smmc.h — C ABI of the B200 (sm_100a) SMM-Conv forward-convolution path.
+ *
+ * This is the drop-in boundary for the one hot path of arxiv 2411.15659 as
+ * packaged by the reference (`smmconv`, /root/reference/pkg): channels-first
+ * (NCHW) fp32 forward convolution by scalar-matrix accumulation with zero
+ * packing.  The reference has no C ABI of its own — its entry points are the
+ * Python functions cited beside each symbol below — so these are the symbols a
+ * ctypes / cffi binding of that interface binds.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no framework types.
+ *  - Device entry points take caller-owned DEVICE pointers, allocate nothing,
+ *    and are asynchronous on the caller's stream (`stream` is a cudaStream_t;
+ *    NULL = the legacy default stream).
+ *  - `*_host` entry points take HOST pointers, do H2D + kernel(s) + D2H on an
+ *    internal per-device stream and return after the result is in `y`
+ *    (the reference's numpy semantics: a freshly computed output).
+ *  - Every function returns an int status (SMMC_OK == 0); on failure
+ *    smmc_last_error() returns a thread-local message.  No CPU fallback exists:
+ *    without a usable GPU the status is SMMC_ENODEVICE.
+ *  - Re-entrant: no global mutable state except the per-device host-staging
+ *    pool (mutex-protected) and an atomic launch counter.
+ *
+ * Tensor layouts (all C-contiguous)
+ *  x      : float32 (n, c_i, h, w)                       — NCHW input
+ *  w_smm  : float32 (c_i, k_w, k_h, c_o)                 — the reference's repacked
+ *           "SMM access order" (smm.py:164-167); c_o innermost
+ *  y      : float32 (n, c_o, out_h, out_w)                — NCHW output
+ *  out_h  = (h + 2*p_h - k_h) / s_h + 1, out_w likewise   (geometry.py:60-66)
+ */
+#ifndef SMMC_H_
+#define SMMC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SMMC_API __attribute__((visibility("default")))
+#else
+#define SMMC_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SMMC_ABI_VERSION 1
+
+/* Status codes; the Python layer maps them to the reference's exception types. */
+enum smmc_status {
+    SMMC_OK = 0,
+    SMMC_EGEOM = 1,        /* -> GeometryError          (geometry.py:32-50)   */
+    SMMC_ESHAPE = 2,       /* -> ShapeMismatchError     (validation.py:25-34) */
+    SMMC_EUNSUPPORTED = 3, /* -> BackendUnsupportedError (errors.py)          */
+    SMMC_EWORKSPACE = 4,   /* -> ValueError: caller workspace too small       */
+    SMMC_ECUDA = 5,        /* -> DeviceError (RuntimeError)                    */
+    SMMC_ENODEVICE = 6,    /* -> DeviceError: no CUDA device / driver          */
+    SMMC_EINDEX = 7        /* -> IndexError             (smm.py:196-199, 211)  */
+};
+
+/* Kernel variants. */
+enum smmc_mode {
+    SMMC_MODE_FFMA = 0,  /* product: register-tiled fp32 FFMA, any order; ~1e-6 rel */
+    SMMC_MODE_EXACT = 1  /* bitwise-equal to smm_conv_single: (c, j, k) order,
+                            separately rounded mul then add (smm.py:84-114)      */
+};
+
+/* One convolution problem: the reference's ConvGeometry (geometry.py:19-30)
+ * plus a batch size n (the Conv2D.transform batch, estimator.py:112-125). */
+typedef struct smmc_geom {
+    int32_t n;    /* samples                  */
+    int32_t c_i;  /* in_channels              */
+    int32_t h;    /* in_h                     */
+    int32_t w;    /* in_w                     */
+    int32_t c_o;  /* out_channels             */
+    int32_t k_h;  /* kernel rows              */
+    int32_t k_w;  /* kernel columns           */
+    int32_t s_h;  /* stride_h                 */
+    int32_t s_w;  /* stride_w                 */
+    int32_t p_h;  /* pad_h                    */
+    int32_t p_w;  /* pad_w                    */
+} smmc_geom;
+
+/* ABI version (SMMC_ABI_VERSION). */
+SMMC_API int smmc_abi_version(void);
+
+/* Thread-local message for the last non-OK status on this thread. */
+SMMC_API const char* smmc_last_error(void);
+
+/* Validate a geometry (ConvGeometry.__post_init__, geometry.py:32-50) and
+ * return the output size.  SMMC_EGEOM on any rejection. */
+SMMC_API int smmc_geom_check(const smmc_geom* g, int32_t* out_h, int32_t* out_w);
+
+/* Device scratch (bytes) smmc_conv2d_fwd_f32 needs for this problem/mode:
+ * 0 for the fused kernels, the split-K partial planes otherwise.
+ * GPU analogue of smm_workspace_elements (smm.py:176-180). */
+SMMC_API size_t smmc_workspace_bytes(const smmc_geom* g, int mode);
+
+/* Forward convolution, device pointers, async on `stream`.
+ * Replaces the compute of smm_conv_single (smm.py:226-251),
+ * smm_conv_parallel (smm.py:254-306) and the per-sample loop of
+ * Conv2D.transform (estimator.py:112-125) with one batched launch.
+ * `workspace` must hold smmc_workspace_bytes(g, mode) bytes (may be NULL if 0). */
+SMMC_API int smmc_conv2d_fwd_f32(const float* x, const float* w_smm, float* y,
+                        const smmc_geom* g, int mode, void* workspace,
+                        size_t workspace_bytes, void* stream);
+
+/* Same, HOST pointers: H2D(x, w_smm) + conv + D2H(y), synchronous.
+ * The numpy drop-in for smm_conv_single / smm_conv_parallel. */
+SMMC_API int smmc_conv2d_fwd_f32_host(const float* x, const float* w_smm, float* y,
+                             const smmc_geom* g, int mode, int device);
+
+/* Zero-packing slice (smm.py:56-73 / extract_slice smm.py:190-203), device:
+ * buf[r, t] = x[c, r - p_h, j + t*s_w - p_w] (0 outside), buf is
+ * (h + 2*p_h) x out_w.  Uses sample 0 of x; g->n is ignored. */
+SMMC_API int smmc_extract_slice_f32(const float* x, const smmc_geom* g, int32_t c,
+                           int32_t j, float* buf, void* stream);
+
+/* dst[r, t] += alpha * src[r, t] with one rounded multiply then one rounded
+ * add (scalar_matrix_fma, smm.py:76-81, 217-223); row strides in elements. */
+SMMC_API int smmc_scalar_matrix_fma_f32(float alpha, const float* src,
+                               int64_t src_row_stride, float* dst,
+                               int64_t dst_row_stride, int32_t rows,
+                               int32_t cols, void* stream);
+
+/* Host-pointer versions of the two helpers above (synchronous). */
+SMMC_API int smmc_extract_slice_f32_host(const float* x, const smmc_geom* g, int32_t c,
+                                int32_t j, float* buf, int device);
+SMMC_API int smmc_scalar_matrix_fma_f32_host(float alpha, const float* src,
+                                    int64_t src_row_stride, float* dst,
+                                    int64_t dst_row_stride, int32_t rows,
+                                    int32_t cols, int device);
+
+/* Number of kernels smmc_conv2d_fwd_f32 launches for this problem/mode. */
+SMMC_API int smmc_plan_launches(const smmc_geom* g, int mode);
+
+/* Short human-readable description of the kernel plan (tile, split-K). */
+SMMC_API int smmc_plan_describe(const smmc_geom* g, int mode, char* buf, size_t len);
+
+/* Total kernels this library has launched in this process (atomic). */
+SMMC_API uint64_t smmc_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SMMC_H_ */

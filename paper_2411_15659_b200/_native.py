@@ -1,0 +1,166 @@
+"""ctypes binding of the C ABI (``include/smmc.h``) exported by ``lib/libsmmc.so``.
+
+The library is the only compute path: if it is missing or no GPU is visible
+the calls raise ``DeviceError`` — nothing here (or anywhere in the package)
+computes a convolution on the CPU.
+"""
+
+import ctypes
+import os
+import threading
+from pathlib import Path
+
+from .errors import (BackendUnsupportedError, DeviceError, GeometryError,
+                     ShapeMismatchError, SmmConvError)
+
+__all__ = ["lib", "Geom", "check", "LIB_PATH", "MODES", "mode_id",
+           "EXPORTED_SYMBOLS"]
+
+LIB_PATH = Path(os.environ.get(
+    "SMMC_LIB", Path(__file__).resolve().parent / "lib" / "libsmmc.so"))
+
+SMMC_OK = 0
+SMMC_EGEOM = 1
+SMMC_ESHAPE = 2
+SMMC_EUNSUPPORTED = 3
+SMMC_EWORKSPACE = 4
+SMMC_ECUDA = 5
+SMMC_ENODEVICE = 6
+SMMC_EINDEX = 7
+
+MODES = {"ffma": 0, "exact": 1}
+
+# Every function include/smmc.h declares (tests/test_boundary.py checks the
+# header and the shared object against this list).
+EXPORTED_SYMBOLS = (
+    "smmc_abi_version", "smmc_last_error", "smmc_geom_check",
+    "smmc_workspace_bytes", "smmc_conv2d_fwd_f32", "smmc_conv2d_fwd_f32_host",
+    "smmc_extract_slice_f32", "smmc_scalar_matrix_fma_f32",
+    "smmc_extract_slice_f32_host", "smmc_scalar_matrix_fma_f32_host",
+    "smmc_plan_launches", "smmc_plan_describe", "smmc_launch_count",
+)
+
+
+class Geom(ctypes.Structure):
+    """``smmc_geom``: n, c_i, h, w, c_o, k_h, k_w, s_h, s_w, p_h, p_w (int32)."""
+
+    _fields_ = [(f, ctypes.c_int32) for f in
+                ("n", "c_i", "h", "w", "c_o", "k_h", "k_w", "s_h", "s_w",
+                 "p_h", "p_w")]
+
+    @classmethod
+    def of(cls, geom, batch=1):
+        return cls(*geom.as_abi(batch))
+
+
+def mode_id(mode):
+    if isinstance(mode, int) and mode in MODES.values():
+        return mode
+    try:
+        return MODES[mode]
+    except (KeyError, TypeError):
+        raise BackendUnsupportedError(
+            f"unknown kernel mode {mode!r}; choose from {sorted(MODES)}") from None
+
+
+_lock = threading.Lock()
+_lib = None
+
+_P = ctypes.c_void_p
+_I32 = ctypes.c_int32
+_I64 = ctypes.c_int64
+_GP = ctypes.POINTER(Geom)
+
+_SIGNATURES = {
+    "smmc_abi_version": (ctypes.c_int, []),
+    "smmc_last_error": (ctypes.c_char_p, []),
+    "smmc_geom_check": (ctypes.c_int, [_GP, ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
+    "smmc_workspace_bytes": (ctypes.c_size_t, [_GP, ctypes.c_int]),
+    "smmc_conv2d_fwd_f32": (ctypes.c_int, [_P, _P, _P, _GP, ctypes.c_int, _P,
+                                           ctypes.c_size_t, _P]),
+    "smmc_conv2d_fwd_f32_host": (ctypes.c_int, [_P, _P, _P, _GP, ctypes.c_int,
+                                                ctypes.c_int]),
+    "smmc_extract_slice_f32": (ctypes.c_int, [_P, _GP, _I32, _I32, _P, _P]),
+    "smmc_scalar_matrix_fma_f32": (ctypes.c_int, [ctypes.c_float, _P, _I64, _P,
+                                                  _I64, _I32, _I32, _P]),
+    "smmc_extract_slice_f32_host": (ctypes.c_int, [_P, _GP, _I32, _I32, _P,
+                                                   ctypes.c_int]),
+    "smmc_scalar_matrix_fma_f32_host": (ctypes.c_int, [ctypes.c_float, _P, _I64,
+                                                       _P, _I64, _I32, _I32,
+                                                       ctypes.c_int]),
+    "smmc_plan_launches": (ctypes.c_int, [_GP, ctypes.c_int]),
+    "smmc_plan_describe": (ctypes.c_int, [_GP, ctypes.c_int, ctypes.c_char_p,
+                                          ctypes.c_size_t]),
+    "smmc_launch_count": (ctypes.c_uint64, []),
+}
+
+
+def lib():
+    """Load (once) and return the native library, or raise DeviceError."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise DeviceError(
+                    f"native library {LIB_PATH} is not built; run "
+                    "`python -c 'import __graft_entry__ as g; g.build()'` "
+                    "(there is no CPU fallback)")
+            try:
+                handle = ctypes.CDLL(str(LIB_PATH))
+            except OSError as exc:
+                raise DeviceError(f"cannot load {LIB_PATH}: {exc}") from exc
+            for name, (res, args) in _SIGNATURES.items():
+                fn = getattr(handle, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = handle
+    return _lib
+
+
+def last_error():
+    msg = lib().smmc_last_error()
+    return msg.decode(errors="replace") if msg else ""
+
+
+def check(status, what="smmc"):
+    """Map a C status to the reference's exception types."""
+    if status == SMMC_OK:
+        return
+    msg = f"{what}: {last_error()}"
+    if status == SMMC_EGEOM:
+        raise GeometryError(msg)
+    if status == SMMC_ESHAPE:
+        raise ShapeMismatchError(msg)
+    if status == SMMC_EUNSUPPORTED:
+        raise BackendUnsupportedError(msg)
+    if status == SMMC_EWORKSPACE:
+        raise ValueError(msg)
+    if status == SMMC_EINDEX:
+        raise IndexError(msg)
+    if status in (SMMC_ECUDA, SMMC_ENODEVICE):
+        raise DeviceError(msg)
+    raise SmmConvError(f"{what}: status {status}: {last_error()}")
+
+
+def launch_count():
+    return int(lib().smmc_launch_count())
+
+
+def plan_describe(geom, batch=1, mode="ffma"):
+    buf = ctypes.create_string_buffer(256)
+    g = Geom.of(geom, batch)
+    check(lib().smmc_plan_describe(ctypes.byref(g), mode_id(mode), buf, 256),
+          "smmc_plan_describe")
+    return buf.value.decode()
+
+
+def plan_launches(geom, batch=1, mode="ffma"):
+    g = Geom.of(geom, batch)
+    return int(lib().smmc_plan_launches(ctypes.byref(g), mode_id(mode)))
+
+
+def workspace_bytes(geom, batch=1, mode="ffma"):
+    g = Geom.of(geom, batch)
+    return int(lib().smmc_workspace_bytes(ctypes.byref(g), mode_id(mode)))

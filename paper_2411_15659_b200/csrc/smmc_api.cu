@@ -1,0 +1,429 @@
+// smmc_api.cu — the extern "C" boundary (include/smmc.h): validation, kernel
+// planning, status/error mapping and the host-buffer staging path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "smmc_internal.cuh"
+
+namespace smmc {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+}  // namespace
+
+void set_error(const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+}
+
+void count_launches(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+namespace {
+
+// ConvGeometry.__post_init__ (geometry.py:32-50), plus batch and int32 range.
+int check_geom(const smmc_geom* g, int* oh, int* ow) {
+    if (!g) {
+        set_error("geometry pointer is NULL");
+        return SMMC_EGEOM;
+    }
+    if (g->n < 0) {
+        set_error("batch size must be >= 0, got %d", g->n);
+        return SMMC_EGEOM;
+    }
+    if (g->c_i < 1 || g->c_o < 1 || g->h < 1 || g->w < 1 || g->k_h < 1 || g->k_w < 1) {
+        set_error("channel counts, spatial and kernel sizes must be >= 1");
+        return SMMC_EGEOM;
+    }
+    if (g->s_h < 1 || g->s_w < 1) {
+        set_error("strides must be >= 1");
+        return SMMC_EGEOM;
+    }
+    if (g->p_h < 0 || g->p_w < 0) {
+        set_error("paddings must be >= 0");
+        return SMMC_EGEOM;
+    }
+    const int64_t hp = (int64_t)g->h + 2 * (int64_t)g->p_h;
+    const int64_t wp = (int64_t)g->w + 2 * (int64_t)g->p_w;
+    if (g->k_h > hp || g->k_w > wp) {
+        set_error("kernel %dx%d exceeds padded input %lldx%lld", g->k_h, g->k_w, (long long)hp,
+                  (long long)wp);
+        return SMMC_EGEOM;
+    }
+    const int64_t o_h = (hp - g->k_h) / g->s_h + 1;
+    const int64_t o_w = (wp - g->k_w) / g->s_w + 1;
+    if (o_h < 1 || o_w < 1) {
+        set_error("output would be empty for this geometry");
+        return SMMC_EGEOM;
+    }
+    const int64_t m = (int64_t)g->n * o_h * o_w;
+    const int64_t k = (int64_t)g->c_i * g->k_h * g->k_w;
+    const int64_t xs = (int64_t)g->c_i * g->h * g->w;
+    if (m > INT32_MAX || k > INT32_MAX || xs > INT32_MAX || o_h * o_w > INT32_MAX) {
+        set_error("problem too large for 32-bit pixel/tap indexing");
+        return SMMC_EUNSUPPORTED;
+    }
+    if (oh) *oh = (int)o_h;
+    if (ow) *ow = (int)o_w;
+    return SMMC_OK;
+}
+
+int sm_count_for(int device) {
+    static std::mutex mu;
+    static std::vector<int> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    if (device >= (int)cache.size()) cache.resize(device + 1, 0);
+    if (!cache[device]) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0)
+            v = 148;
+        cache[device] = v;
+    }
+    return cache[device];
+}
+
+int current_device() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess) d = 0;
+    return d;
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return SMMC_OK;
+    set_error("%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) return SMMC_ENODEVICE;
+    return SMMC_ECUDA;
+}
+
+int check_mode(int mode) {
+    if (mode != SMMC_MODE_FFMA && mode != SMMC_MODE_EXACT) {
+        set_error("unknown mode %d (0 = ffma, 1 = exact)", mode);
+        return SMMC_EUNSUPPORTED;
+    }
+    return SMMC_OK;
+}
+
+size_t workspace_for(const smmc_geom& g, int mode, int oh, int ow, int sm_count) {
+    if (mode != SMMC_MODE_FFMA || g.n == 0) return 0;
+    const FfmaPlan pl = plan_ffma(g, sm_count);
+    if (pl.splits <= 1) return 0;
+    return (size_t)pl.splits * (size_t)g.n * g.c_o * oh * ow * sizeof(float);
+}
+
+// Per-device staging buffers for the *_host entry points.
+struct HostPool {
+    std::mutex mu;
+    cudaStream_t stream = nullptr;
+    void* buf[4] = {nullptr, nullptr, nullptr, nullptr};
+    size_t cap[4] = {0, 0, 0, 0};
+};
+
+HostPool& pool_for(int device) {
+    static std::mutex mu;
+    static std::vector<HostPool*> pools;
+    std::lock_guard<std::mutex> lk(mu);
+    if (device >= (int)pools.size()) pools.resize(device + 1, nullptr);
+    if (!pools[device]) pools[device] = new HostPool();
+    return *pools[device];
+}
+
+int ensure(HostPool& hp, int i, size_t bytes) {
+    if (hp.cap[i] >= bytes) return SMMC_OK;
+    if (hp.buf[i]) cudaFree(hp.buf[i]);
+    hp.buf[i] = nullptr;
+    hp.cap[i] = 0;
+    if (bytes == 0) return SMMC_OK;
+    int st = cuda_status(cudaMalloc(&hp.buf[i], bytes), "cudaMalloc(staging)");
+    if (st) return st;
+    hp.cap[i] = bytes;
+    return SMMC_OK;
+}
+
+int select_device(int device) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        set_error("no CUDA device available (%s); this library has no CPU fallback",
+                  e == cudaSuccess ? "0 devices" : cudaGetErrorString(e));
+        return SMMC_ENODEVICE;
+    }
+    if (device < 0 || device >= count) {
+        set_error("device %d out of range [0, %d)", device, count);
+        return SMMC_EINDEX;
+    }
+    return cuda_status(cudaSetDevice(device), "cudaSetDevice");
+}
+
+int conv_device(const float* x, const float* w, float* y, const smmc_geom* g, int mode, void* ws,
+                size_t ws_bytes, cudaStream_t stream) {
+    int oh = 0, ow = 0;
+    int st = check_geom(g, &oh, &ow);
+    if (st) return st;
+    if ((st = check_mode(mode))) return st;
+    if (g->n == 0) return SMMC_OK;
+    if (!x || !w || !y) {
+        set_error("x, w_smm and y must be non-NULL device pointers");
+        return SMMC_ESHAPE;
+    }
+    if (((uintptr_t)x | (uintptr_t)w | (uintptr_t)y) & 15) {
+        set_error("x, w_smm and y must be 16-byte aligned");
+        return SMMC_ESHAPE;
+    }
+    const int dev = current_device();
+    const int sms = sm_count_for(dev);
+    Problem p{};
+    p.x = x;
+    p.w = w;
+    p.y = y;
+    p.ws = static_cast<float*>(ws);
+    p.n = g->n;
+    p.c = g->c_i;
+    p.h = g->h;
+    p.w_in = g->w;
+    p.co = g->c_o;
+    p.kh = g->k_h;
+    p.kw = g->k_w;
+    p.sh = g->s_h;
+    p.sw = g->s_w;
+    p.ph = g->p_h;
+    p.pw = g->p_w;
+    p.oh = oh;
+    p.ow = ow;
+    p.hw = g->h * g->w;
+    p.ohw = oh * ow;
+    p.m = g->n * oh * ow;
+    p.k = g->c_i * g->k_h * g->k_w;
+    p.splits = 1;
+    p.k_per_split = p.k;
+    if (mode == SMMC_MODE_EXACT) return cuda_status(launch_exact(p, stream), "conv_exact launch");
+
+    const FfmaPlan pl = plan_ffma(*g, sms);
+    p.splits = pl.splits;
+    p.k_per_split = pl.k_per_split;
+    if (pl.splits > 1) {
+        const size_t need = workspace_for(*g, mode, oh, ow, sms);
+        if (!ws || ws_bytes < need) {
+            set_error("workspace of %zu bytes required (got %zu)", need, ws_bytes);
+            return SMMC_EWORKSPACE;
+        }
+        if ((uintptr_t)ws & 15) {
+            set_error("workspace must be 16-byte aligned");
+            return SMMC_ESHAPE;
+        }
+    }
+    if ((st = cuda_status(launch_ffma(p, pl, stream), "conv_ffma launch"))) return st;
+    if (pl.splits > 1)
+        return cuda_status(launch_splitk_reduce(p, stream), "splitk_reduce launch");
+    return SMMC_OK;
+}
+
+}  // namespace
+}  // namespace smmc
+
+using namespace smmc;
+
+extern "C" {
+
+int smmc_abi_version(void) { return SMMC_ABI_VERSION; }
+
+const char* smmc_last_error(void) { return g_last_error.c_str(); }
+
+int smmc_geom_check(const smmc_geom* g, int32_t* out_h, int32_t* out_w) {
+    int oh = 0, ow = 0;
+    int st = check_geom(g, &oh, &ow);
+    if (st) return st;
+    if (out_h) *out_h = oh;
+    if (out_w) *out_w = ow;
+    return SMMC_OK;
+}
+
+size_t smmc_workspace_bytes(const smmc_geom* g, int mode) {
+    int oh = 0, ow = 0;
+    if (check_geom(g, &oh, &ow) || check_mode(mode)) return 0;
+    return workspace_for(*g, mode, oh, ow, sm_count_for(current_device()));
+}
+
+int smmc_plan_launches(const smmc_geom* g, int mode) {
+    int oh = 0, ow = 0;
+    if (check_geom(g, &oh, &ow) || check_mode(mode)) return -1;
+    if (g->n == 0) return 0;
+    if (mode == SMMC_MODE_EXACT) return 1;
+    return plan_ffma(*g, sm_count_for(current_device())).splits > 1 ? 2 : 1;
+}
+
+int smmc_plan_describe(const smmc_geom* g, int mode, char* buf, size_t len) {
+    int oh = 0, ow = 0;
+    int st = check_geom(g, &oh, &ow);
+    if (st) return st;
+    if ((st = check_mode(mode))) return st;
+    if (!buf || !len) return SMMC_OK;
+    if (mode == SMMC_MODE_EXACT) {
+        snprintf(buf, len, "exact: 1 px x 8 c_o per thread, (c,j,k) order, fmul_rn+fadd_rn");
+        return SMMC_OK;
+    }
+    const FfmaPlan pl = plan_ffma(*g, sm_count_for(current_device()));
+    snprintf(buf, len, "ffma: tile %dx%dx%d, %d threads, taps=%d, split_k=%d (k_per_split=%d)",
+             pl.bm, pl.bn, pl.bk, pl.threads, pl.tap_kind, pl.splits, pl.k_per_split);
+    return SMMC_OK;
+}
+
+uint64_t smmc_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int smmc_conv2d_fwd_f32(const float* x, const float* w_smm, float* y, const smmc_geom* g, int mode,
+                        void* workspace, size_t workspace_bytes, void* stream) {
+    return conv_device(x, w_smm, y, g, mode, workspace, workspace_bytes,
+                       static_cast<cudaStream_t>(stream));
+}
+
+int smmc_conv2d_fwd_f32_host(const float* x, const float* w_smm, float* y, const smmc_geom* g,
+                             int mode, int device) {
+    int oh = 0, ow = 0;
+    int st = check_geom(g, &oh, &ow);
+    if (st) return st;
+    if ((st = check_mode(mode))) return st;
+    if (g->n == 0) return SMMC_OK;
+    if (!x || !w_smm || !y) {
+        set_error("x, w_smm and y must be non-NULL host pointers");
+        return SMMC_ESHAPE;
+    }
+    if ((st = select_device(device))) return st;
+    HostPool& hp = pool_for(device);
+    std::lock_guard<std::mutex> lk(hp.mu);
+    if (!hp.stream &&
+        (st = cuda_status(cudaStreamCreateWithFlags(&hp.stream, cudaStreamNonBlocking),
+                          "cudaStreamCreate")))
+        return st;
+    const size_t xb = (size_t)g->n * g->c_i * g->h * g->w * sizeof(float);
+    const size_t wb = (size_t)g->c_i * g->k_w * g->k_h * g->c_o * sizeof(float);
+    const size_t yb = (size_t)g->n * g->c_o * oh * ow * sizeof(float);
+    const size_t wsb = workspace_for(*g, mode, oh, ow, sm_count_for(device));
+    if ((st = ensure(hp, 0, xb)) || (st = ensure(hp, 1, wb)) || (st = ensure(hp, 2, yb)) ||
+        (st = ensure(hp, 3, wsb)))
+        return st;
+    cudaStream_t s = hp.stream;
+    if ((st = cuda_status(cudaMemcpyAsync(hp.buf[0], x, xb, cudaMemcpyHostToDevice, s), "H2D x")))
+        return st;
+    if ((st = cuda_status(cudaMemcpyAsync(hp.buf[1], w_smm, wb, cudaMemcpyHostToDevice, s),
+                          "H2D w_smm")))
+        return st;
+    if ((st = conv_device(static_cast<float*>(hp.buf[0]), static_cast<float*>(hp.buf[1]),
+                          static_cast<float*>(hp.buf[2]), g, mode, hp.buf[3], wsb, s)))
+        return st;
+    if ((st = cuda_status(cudaMemcpyAsync(y, hp.buf[2], yb, cudaMemcpyDeviceToHost, s), "D2H y")))
+        return st;
+    return cuda_status(cudaStreamSynchronize(s), "conv (host path)");
+}
+
+int smmc_extract_slice_f32(const float* x, const smmc_geom* g, int32_t c, int32_t j, float* buf,
+                           void* stream) {
+    int oh = 0, ow = 0;
+    int st = check_geom(g, &oh, &ow);
+    if (st) return st;
+    if (c < 0 || c >= g->c_i) {
+        set_error("channel %d out of range [0, %d)", c, g->c_i);
+        return SMMC_EINDEX;
+    }
+    if (j < 0 || j >= g->k_w) {
+        set_error("kernel column %d out of range [0, %d)", j, g->k_w);
+        return SMMC_EINDEX;
+    }
+    if (!x || !buf) {
+        set_error("x and buf must be non-NULL");
+        return SMMC_ESHAPE;
+    }
+    return cuda_status(launch_extract_slice(x, *g, c, j, buf, static_cast<cudaStream_t>(stream)),
+                       "extract_slice launch");
+}
+
+int smmc_scalar_matrix_fma_f32(float alpha, const float* src, int64_t src_row_stride, float* dst,
+                               int64_t dst_row_stride, int32_t rows, int32_t cols, void* stream) {
+    if (rows < 0 || cols < 0) {
+        set_error("rows/cols must be >= 0");
+        return SMMC_ESHAPE;
+    }
+    if ((rows && cols) && (!src || !dst)) {
+        set_error("src and dst must be non-NULL");
+        return SMMC_ESHAPE;
+    }
+    return cuda_status(launch_scalar_matrix_fma(alpha, src, src_row_stride, dst, dst_row_stride,
+                                                rows, cols, static_cast<cudaStream_t>(stream)),
+                       "scalar_matrix_fma launch");
+}
+
+int smmc_extract_slice_f32_host(const float* x, const smmc_geom* g, int32_t c, int32_t j,
+                                float* buf, int device) {
+    int oh = 0, ow = 0;
+    int st = check_geom(g, &oh, &ow);
+    if (st) return st;
+    if (c < 0 || c >= g->c_i || j < 0 || j >= g->k_w) {
+        set_error("slice index (c=%d, j=%d) out of range", c, j);
+        return SMMC_EINDEX;
+    }
+    if ((st = select_device(device))) return st;
+    HostPool& hp = pool_for(device);
+    std::lock_guard<std::mutex> lk(hp.mu);
+    if (!hp.stream &&
+        (st = cuda_status(cudaStreamCreateWithFlags(&hp.stream, cudaStreamNonBlocking),
+                          "cudaStreamCreate")))
+        return st;
+    const size_t xb = (size_t)g->c_i * g->h * g->w * sizeof(float);
+    const size_t bb = (size_t)(g->h + 2 * g->p_h) * ow * sizeof(float);
+    if ((st = ensure(hp, 0, xb)) || (st = ensure(hp, 2, bb))) return st;
+    cudaStream_t s = hp.stream;
+    if ((st = cuda_status(cudaMemcpyAsync(hp.buf[0], x, xb, cudaMemcpyHostToDevice, s), "H2D x")))
+        return st;
+    if ((st = smmc_extract_slice_f32(static_cast<float*>(hp.buf[0]), g, c, j,
+                                     static_cast<float*>(hp.buf[2]), s)))
+        return st;
+    if ((st = cuda_status(cudaMemcpyAsync(buf, hp.buf[2], bb, cudaMemcpyDeviceToHost, s), "D2H")))
+        return st;
+    return cuda_status(cudaStreamSynchronize(s), "extract_slice (host path)");
+}
+
+int smmc_scalar_matrix_fma_f32_host(float alpha, const float* src, int64_t src_row_stride,
+                                    float* dst, int64_t dst_row_stride, int32_t rows, int32_t cols,
+                                    int device) {
+    if (rows < 0 || cols < 0 || src_row_stride < cols || dst_row_stride < cols) {
+        set_error("invalid fma view (rows=%d cols=%d strides %lld/%lld)", rows, cols,
+                  (long long)src_row_stride, (long long)dst_row_stride);
+        return SMMC_ESHAPE;
+    }
+    if (!rows || !cols) return SMMC_OK;
+    int st = select_device(device);
+    if (st) return st;
+    HostPool& hp = pool_for(device);
+    std::lock_guard<std::mutex> lk(hp.mu);
+    if (!hp.stream &&
+        (st = cuda_status(cudaStreamCreateWithFlags(&hp.stream, cudaStreamNonBlocking),
+                          "cudaStreamCreate")))
+        return st;
+    const size_t sb = ((size_t)(rows - 1) * src_row_stride + cols) * sizeof(float);
+    const size_t db = ((size_t)(rows - 1) * dst_row_stride + cols) * sizeof(float);
+    if ((st = ensure(hp, 0, sb)) || (st = ensure(hp, 2, db))) return st;
+    cudaStream_t s = hp.stream;
+    if ((st = cuda_status(cudaMemcpyAsync(hp.buf[0], src, sb, cudaMemcpyHostToDevice, s), "H2D")))
+        return st;
+    if ((st = cuda_status(cudaMemcpyAsync(hp.buf[2], dst, db, cudaMemcpyHostToDevice, s), "H2D")))
+        return st;
+    if ((st = smmc_scalar_matrix_fma_f32(alpha, static_cast<float*>(hp.buf[0]), src_row_stride,
+                                         static_cast<float*>(hp.buf[2]), dst_row_stride, rows, cols,
+                                         s)))
+        return st;
+    if ((st = cuda_status(cudaMemcpyAsync(dst, hp.buf[2], db, cudaMemcpyDeviceToHost, s), "D2H")))
+        return st;
+    return cuda_status(cudaStreamSynchronize(s), "scalar_matrix_fma (host path)");
+}
+
+}  // extern "C"

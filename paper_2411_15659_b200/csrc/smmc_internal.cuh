@@ -1,0 +1,79 @@
+// smmc_internal.cuh — shared device/host plumbing for the sm_100a SMM-Conv kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/smmc.h"
+
+namespace smmc {
+
+// ----------------------------------------------------------------- problem
+// Resolved problem description passed by value to every kernel.
+struct Problem {
+    const float* x;      // (n, c_i, h, w)
+    const float* w;      // (c_i, k_w, k_h, c_o) == row-major [K][c_o], K = c_i*k_w*k_h
+    float* y;            // (n, c_o, oh, ow)
+    float* ws;           // split-K partial planes [splits][n*c_o*oh*ow] (or null)
+    int n, c, h, w_in, co, kh, kw, sh, sw, ph, pw, oh, ow;
+    int hw;              // h*w
+    int ohw;             // oh*ow
+    int m;               // GEMM rows: n*oh*ow output pixels
+    int k;               // GEMM depth: c_i*k_w*k_h taps (SMM (c, j, k) order)
+    int k_per_split;     // multiple of the kernel's BK
+    int splits;
+};
+
+// Last-error / launch bookkeeping (defined in smmc_api.cu).
+void set_error(const char* fmt, ...);
+void count_launches(int n);
+
+// Kernel launchers (defined in the kernel translation units).  They return
+// a cudaError_t from cudaGetLastError() after the launch.
+cudaError_t launch_exact(const Problem& p, cudaStream_t s);
+struct FfmaPlan {
+    int variant;     // index into the tile table
+    int bm, bn, bk;  // CTA tile
+    int threads;
+    int splits;      // split-K factor (1 = fused, no workspace)
+    int k_per_split;
+    int tap_kind;    // 0 generic, 1: 3x3s1, 2: 1x1s1, 3: 7x7s2, 4: 11x11s4, 5: 5x5s1
+};
+FfmaPlan plan_ffma(const smmc_geom& g, int sm_count);
+cudaError_t launch_ffma(const Problem& p, const FfmaPlan& plan, cudaStream_t s);
+cudaError_t launch_splitk_reduce(const Problem& p, cudaStream_t s);
+cudaError_t launch_extract_slice(const float* x, const smmc_geom& g, int c, int j,
+                                 float* buf, cudaStream_t s);
+cudaError_t launch_scalar_matrix_fma(float alpha, const float* src, int64_t ss,
+                                     float* dst, int64_t ds, int rows, int cols,
+                                     cudaStream_t s);
+
+// ----------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// 4-byte cp.async with zero-fill: copies `src` when `valid`, else writes 0.
+// This is the "zero packing" of the reference's slice extraction
+// (smm.py:56-73) done by the copy engine path instead of a buffer pass.
+__device__ __forceinline__ void cp_async4_zfill(uint32_t dst, const void* src, bool valid) {
+    const int n = valid ? 4 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(n));
+}
+
+// 16-byte cp.async (L2 only) with zero-fill of the tail past `bytes`.
+__device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, int bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(bytes));
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+}  // namespace smmc

@@ -1,0 +1,122 @@
+"""Device-resident entry points over torch CUDA tensors.
+
+PyTorch is plumbing here (device memory, streams); the compute is the C ABI's
+``smmc_conv2d_fwd_f32`` launched on torch's current stream, with no host
+synchronisation — usable inside CUDA-graph capture.
+"""
+
+import ctypes
+
+from . import _native
+from .errors import DeviceError, ShapeMismatchError
+
+__all__ = ["conv2d", "repack_weights", "SmmConv2d"]
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _check_tensor(t, shape, name):
+    torch = _torch()
+    if not isinstance(t, torch.Tensor):
+        raise ShapeMismatchError(f"{name} must be a torch.Tensor")
+    if not t.is_cuda:
+        raise ShapeMismatchError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != torch.float32:
+        raise ShapeMismatchError(f"{name} must be float32, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ShapeMismatchError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+    if not t.is_contiguous():
+        raise ShapeMismatchError(f"{name} must be contiguous")
+    if t.data_ptr() % 16:
+        raise ShapeMismatchError(f"{name} must be 16-byte aligned")
+    return t
+
+
+def repack_weights(weights, geom):
+    """OIHW -> (c_i, k_w, k_h, c_o) on the device (once per layer, untimed)."""
+    _check_tensor(weights, geom.weights_shape, "weight tensor")
+    return weights.permute(1, 3, 2, 0).contiguous()
+
+
+def conv2d(x, weights_smm, geom, *, mode="ffma", out=None, workspace=None):
+    """Batched NCHW forward conv on torch's current stream.
+
+    ``x`` (N, c_i, h, w), ``weights_smm`` (c_i, k_w, k_h, c_o) on the same
+    device; returns ``out`` (N, c_o, h', w').  Split-K problems need a
+    workspace: pass one (uint8 tensor of ``_native.workspace_bytes`` bytes) to
+    stay allocation-free, else one is taken from torch's caching allocator.
+    """
+    torch = _torch()
+    if not isinstance(x, torch.Tensor) or x.dim() != 4:
+        raise ShapeMismatchError("x must be a 4-D torch.Tensor (N, c_i, h, w)")
+    n = x.shape[0]
+    _check_tensor(x, (n,) + geom.input_shape, "input batch")
+    _check_tensor(weights_smm, geom.weights_smm_shape, "repacked weight tensor")
+    if weights_smm.device != x.device:
+        raise ShapeMismatchError("x and weights_smm must be on the same device")
+    if out is None:
+        out = torch.empty((n,) + geom.output_shape, device=x.device, dtype=torch.float32)
+    else:
+        _check_tensor(out, (n,) + geom.output_shape, "output tensor")
+    if n == 0:
+        return out
+    mode_id = _native.mode_id(mode)
+    g = _native.Geom.of(geom, n)
+    lib = _native.lib()
+    with torch.cuda.device(x.device):
+        need = int(lib.smmc_workspace_bytes(ctypes.byref(g), mode_id))
+        ws_ptr, ws_len = None, 0
+        if need:
+            if workspace is None or workspace.numel() * workspace.element_size() < need:
+                workspace = torch.empty(need, dtype=torch.uint8, device=x.device)
+            ws_ptr, ws_len = workspace.data_ptr(), workspace.numel() * workspace.element_size()
+        stream = torch.cuda.current_stream(x.device).cuda_stream
+        _native.check(lib.smmc_conv2d_fwd_f32(
+            ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(weights_smm.data_ptr()),
+            ctypes.c_void_p(out.data_ptr()), ctypes.byref(g), mode_id,
+            ctypes.c_void_p(ws_ptr) if ws_ptr else None, ws_len,
+            ctypes.c_void_p(stream) if stream else None), "smmc_conv2d_fwd_f32")
+    return out
+
+
+class SmmConv2d:
+    """A fitted layer held on one device: weights in SMM order, a reusable
+    workspace, and a call that launches on the current stream.
+
+    ``weights`` may be OIHW numpy / torch (repacked once here, untimed).
+    """
+
+    def __init__(self, geom, weights, device="cuda", mode="ffma", max_batch=None):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise DeviceError("SmmConv2d needs a CUDA device (no CPU fallback)")
+        self.geom = geom
+        self.mode = mode
+        self.device = torch.device(device)
+        w = torch.as_tensor(weights, dtype=torch.float32)
+        if tuple(w.shape) == geom.weights_shape:
+            w = w.permute(1, 3, 2, 0)
+        elif tuple(w.shape) != geom.weights_smm_shape:
+            raise ShapeMismatchError(
+                f"weights must be OIHW {geom.weights_shape} or SMM {geom.weights_smm_shape}")
+        self.weights_smm = w.contiguous().to(self.device)
+        self._ws = None
+        if max_batch:
+            self.workspace_for(max_batch)
+
+    def workspace_for(self, batch):
+        torch = _torch()
+        need = _native.workspace_bytes(self.geom, batch, self.mode)
+        if need and (self._ws is None or self._ws.numel() < need):
+            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def launches(self, batch):
+        return _native.plan_launches(self.geom, batch, self.mode)
+
+    def __call__(self, x, out=None):
+        return conv2d(x, self.weights_smm, self.geom, mode=self.mode, out=out,
+                      workspace=self.workspace_for(x.shape[0]))

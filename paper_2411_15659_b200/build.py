@@ -75,7 +75,8 @@ def build(force=False, verbose=False, jobs=None):
         raise RuntimeError(f"nvcc failed:\n{msg}")
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [exe, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", str(tmp),
-           *map(str, objs), "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+           *map(str, objs), "-lcudart_static", "-lrt", "-ldl", "-lpthread",
+           "-Xlinker", "--no-undefined"]
     subprocess.run(cmd, check=True, capture_output=not verbose)
     os.replace(tmp, LIB)
     return LIB

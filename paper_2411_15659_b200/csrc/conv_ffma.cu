@@ -4,9 +4,8 @@
 // slice T_j^c (smm.py:56-73), then for every kernel row k the shifted window of
 // that slice times one scalar weight per output channel is accumulated into
 // the whole output plane (smm.py:84-114).  Each output element therefore sees
-// K = c_i*k_w*k_h scalar-times-window updates, indexed in the reference's
-// (c, j, k) order by kidx = (c*k_w + j)*k_h + k — exactly the row index of the
-// repacked weights W_smm viewed as a [K][c_o] matrix (smm.py:164-167).
+// K = c_i*k_w*k_h scalar-times-window updates; the weight of update (c, j, k)
+// for channel m is W_smm[c, j, k, m] (smm.py:164-167).
 //
 // On B200 the loop nest is inverted so that the output, not the input, stays
 // on chip:
@@ -14,50 +13,62 @@
 //     channels; every thread keeps an 8x8 pixel x channel tile of fp32
 //     accumulators in registers for the whole K loop (no re-streaming of the
 //     output plane per update, which is what bounds the CPU path);
-//   * the K loop walks BK taps at a time.  The "zero-packed slice" becomes a
+//   * the K loop walks BK updates at a time.  The zero-packed slice becomes a
 //     BK x BM shared-memory tile filled by predicated cp.async with zero-fill
 //     (src-size 0 for padding taps) — no global scratch, no padded copy;
 //   * "shifting" is index arithmetic in the loader: tap (j, k) of pixel
 //     (oh, ow) reads x[c, oh*s_h + k - p_h, ow*s_w + j - p_w];
-//   * the scalar weights W_smm[c, j, k, :] are rows of the [K][c_o] matrix,
-//     staged by 16-byte cp.async into a BK x BN tile, and read back as
+//   * the scalar weights of BK updates for BN channels are rows of W_smm,
+//     staged by 16-byte cp.async into a BK x BN tile and read back as
 //     broadcast LDS.128;
-//   * a STAGES-deep cp.async ring overlaps the loads of tap block t+STAGES-1
-//     with the FFMAs of block t.
-// Per k step a thread issues 4 LDS.128 and 64 FFMA.
+//   * a STAGES-deep cp.async ring overlaps the loads of block t+STAGES-1 with
+//     the FFMAs of block t.  Per k step a thread issues 4 LDS.128 + 64 FFMA.
 //
-// Small problems (few pixel x channel tiles) split K across CTAs; each split
-// writes a full partial output plane to the workspace and a second kernel sums
-// the planes in split order, so results stay run-to-run deterministic (no
-// atomics).
+// K order.  When c_i % BK == 0 ("cvec") a BK block is one tap (j, k) x BK
+// consecutive input channels: a thread's A elements in a block share one
+// padding test and one running pointer (advanced by BK*h*w per block), and the
+// weight rows are W_smm[c0:c0+BK, j, k, :].  Otherwise (the c_i = 3 stems) a
+// block is BK consecutive updates in the reference's own (c, j, k) order.
+//
+// Split K (small problems; wave-quantisation-aware planner, see plan_ffma):
+//   reduce_mode 1 — each split stores its partial tile to the workspace; the
+//     last CTA to arrive on the tile's counter sums all partials in split
+//     order 0..S-1 and writes y (used for S <= 4);
+//   reduce_mode 2 — splits write partial NCHW planes and a second, fully
+//     parallel kernel sums them in split order (large S, tiny M).
+// Both orders are fixed, so results are bitwise run-to-run deterministic; no
+// float atomics anywhere.
 #include <algorithm>
+#include <mutex>
 
 #include "smmc_internal.cuh"
 
 namespace smmc {
 namespace {
 
-constexpr int kBK = 8;
 constexpr int kStages = 4;
 
-template <int BM, int BN, int THREADS, int KH, int KW, int SH, int SW>
-__global__ void __launch_bounds__(THREADS, (THREADS >= 256 ? 2 : 3))
-conv_ffma_kernel(const Problem p) {
-    constexpr int BK = kBK;
+template <int BM, int BN, int THREADS, int MINB, int BK, int KH, int KW, int SH, int SW, bool CVEC>
+__global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem p) {
     constexpr int STAGES = kStages;
     constexpr int TPX = BM / 8;            // pixel groups (4 + 4 pixels each)
     constexpr int TCO = BN / 8;            // channel groups (4 + 4 channels each)
     static_assert(TPX * TCO == THREADS, "thread tile must cover the CTA tile");
     static_assert(TCO % 8 == 0 && TPX % 4 == 0, "warp = 4 pixel groups x 8 channel groups");
     static_assert(THREADS % BM == 0, "loader maps one pixel column per thread");
-    constexpr int KSTEP = THREADS / BM;    // taps apart for one thread's A loads
+    constexpr int KSTEP = THREADS / BM;    // k rows apart for one thread's A loads
     constexpr int A_PER = BK * BM / THREADS;
     constexpr int B_CHUNKS = BK * BN / 4;  // 16-byte chunks per B tile
-    static_assert(B_CHUNKS % THREADS == 0, "B loader");
-    constexpr int B_PER = B_CHUNKS / THREADS;
+    constexpr int B_PER = (B_CHUNKS + THREADS - 1) / THREADS;
+    constexpr bool B_FULL = (B_CHUNKS % THREADS) == 0;
+    constexpr int B_ROWS_PER_PASS = THREADS / (BN / 4);
+    constexpr uint32_t AS_STAGE = BK * BM * 4;
+    constexpr uint32_t BS_STAGE = BK * BN * 4;
 
-    __shared__ __align__(16) float As[STAGES][BK][BM];
-    __shared__ __align__(16) float Bs[STAGES][BK][BN];
+    extern __shared__ __align__(16) float smem[];
+    float* As = smem;                                // [STAGES][BK][BM]
+    float* Bs = smem + STAGES * BK * BM;             // [STAGES][BK][BN]
+    __shared__ int s_last;
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
@@ -69,9 +80,8 @@ conv_ffma_kernel(const Problem p) {
     const int m0 = blockIdx.x * BM;
     const int n0 = blockIdx.y * BN;
     const int split = blockIdx.z;
-    const int kbeg = split * p.k_per_split;
-    const int kend = min(p.k, kbeg + p.k_per_split);
-    const int ktiles = (kend - kbeg + BK - 1) / BK;
+    const int kt_beg = split * p.kt_per_split;
+    const int ktiles = min(p.kt_total - kt_beg, p.kt_per_split);
 
     const int kh = KH ? KH : p.kh;
     const int kw = KW ? KW : p.kw;
@@ -95,44 +105,114 @@ conv_ffma_kernel(const Problem p) {
         iw0 = ow * sw - p.pw;
         xoff0 = (int64_t)n * p.c * p.hw + (int64_t)ih0 * p.w_in + iw0;
     }
+    const float* __restrict__ xg = p.x;
+    const float* __restrict__ wg = p.w;
+    const uint32_t as_base = smem_u32(As + lk0 * BM + lp);
+    const uint32_t bs_base = smem_u32(Bs);
     const bool b_vec = (p.co & 3) == 0;
 
+    // B chunk of this thread (first pass): row brow, columns bcol..bcol+3
+    const int brow = tid / (BN / 4);
+    const int bcol = (tid % (BN / 4)) * 4;
+    const int bco = n0 + bcol;
+    const int b_bytes = min(max(p.co - bco, 0), 4) * 4;
+
+    // ---- cvec loader state (tap-major K order)
+    uint32_t rowmask = 0, colmask = 0;
+    if (CVEC && pvalid) {
+        for (int r = 0; r < kh; ++r) rowmask |= (uint32_t)((unsigned)(ih0 + r) < (unsigned)p.h) << r;
+        for (int j = 0; j < kw; ++j)
+            colmask |= (uint32_t)((unsigned)(iw0 + j) < (unsigned)p.w_in) << j;
+    }
+    const int cblocks = p.c / BK;
+    const int64_t a_blk = (int64_t)BK * p.hw;             // A pointer step per channel block
+    const int64_t a_elem = (int64_t)KSTEP * p.hw;         // between one thread's A elements
+    const int64_t b_blk = (int64_t)BK * taps * p.co;      // B pointer step per channel block
+    const int64_t b_pass = (int64_t)B_ROWS_PER_PASS * taps * p.co;
+    int ld_tap = 0, ld_cb = 0;
+    bool a_ok = false;
+    const float* a_ptr = xg;
+    const float* b_ptr = wg;
+    auto set_tap = [&]() {
+        const int j = ld_tap / kh;
+        const int kr = ld_tap - j * kh;
+        a_ok = (rowmask >> kr) & (colmask >> j) & 1u;
+        a_ptr = xg + xoff0 + (int64_t)(ld_cb * BK + lk0) * p.hw + kr * p.w_in + j;
+        b_ptr = wg + ((int64_t)(ld_cb * BK + brow) * taps + ld_tap) * p.co + bco;
+    };
+    if (CVEC) {
+        ld_tap = kt_beg / cblocks;
+        ld_cb = kt_beg - ld_tap * cblocks;
+        set_tap();
+    }
+
     auto load_stage = [&](int slot, int kt) {
-        const int kb = kbeg + kt * BK;
-        // A: zero-packed, shifted input taps (the SMM slice, built in smem)
+        if (CVEC) {
+            const uint32_t adst = as_base + slot * AS_STAGE;
 #pragma unroll
-        for (int i = 0; i < A_PER; ++i) {
-            const int kk = lk0 + i * KSTEP;
-            const int kidx = kb + kk;
-            const int c = kidx / taps;
-            const int tap = kidx - c * taps;
-            const int j = tap / kh;
-            const int kr = tap - j * kh;
-            const int ih = ih0 + kr;
-            const int iw = iw0 + j;
-            const bool ok = pvalid && kidx < kend && (unsigned)ih < (unsigned)p.h &&
-                            (unsigned)iw < (unsigned)p.w_in;
-            const float* src = ok ? p.x + xoff0 + (int64_t)c * p.hw + kr * p.w_in + j : p.x;
-            cp_async4_zfill(smem_u32(&As[slot][kk][lp]), src, ok);
-        }
-        // B: scalar weights W_smm[c, j, k, n0:n0+BN] (rows of [K][c_o])
+            for (int i = 0; i < A_PER; ++i)
+                cp_async4_zfill(adst + i * KSTEP * BM * 4, a_ok ? a_ptr + i * a_elem : xg, a_ok);
+            const uint32_t bdst = bs_base + slot * BS_STAGE + (brow * BN + bcol) * 4;
 #pragma unroll
-        for (int i = 0; i < B_PER; ++i) {
-            const int q = tid + i * THREADS;
-            const int row = q / (BN / 4);
-            const int col = (q % (BN / 4)) * 4;
-            const int kidx = kb + row;
-            const int co = n0 + col;
-            if (b_vec) {
-                int bytes = (kidx < kend) ? min(max(p.co - co, 0), 4) * 4 : 0;
-                const float* src = bytes ? p.w + (int64_t)kidx * p.co + co : p.w;
-                cp_async16_zfill(smem_u32(&Bs[slot][row][col]), src, bytes);
+            for (int i = 0; i < B_PER; ++i) {
+                if (!B_FULL && tid + i * THREADS >= B_CHUNKS) break;
+                const uint32_t dst = bdst + i * B_ROWS_PER_PASS * BN * 4;
+                const float* src = b_ptr + i * b_pass;
+                if (b_vec) {
+                    cp_async16_zfill(dst, b_bytes ? src : wg, b_bytes);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const bool okb = bco + e < p.co;
+                        cp_async4_zfill(dst + e * 4, okb ? src + e : wg, okb);
+                    }
+                }
+            }
+            if (++ld_cb == cblocks) {
+                ld_cb = 0;
+                ++ld_tap;
+                if (ld_tap < taps) set_tap();
             } else {
+                a_ptr += a_blk;
+                b_ptr += b_blk;
+            }
+        } else {
+            // reference (c, j, k) order: kidx = (c*kw + j)*kh + k
+            const int kb = (kt_beg + kt) * BK;
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const bool ok = kidx < kend && co + e < p.co;
-                    const float* src = ok ? p.w + (int64_t)kidx * p.co + co + e : p.w;
-                    cp_async4_zfill(smem_u32(&Bs[slot][row][col + e]), src, ok);
+            for (int i = 0; i < A_PER; ++i) {
+                const int kk = lk0 + i * KSTEP;
+                const int kidx = kb + kk;
+                const int c = kidx / taps;
+                const int tap = kidx - c * taps;
+                const int j = tap / kh;
+                const int kr = tap - j * kh;
+                const int ih = ih0 + kr;
+                const int iw = iw0 + j;
+                const bool ok = pvalid && kidx < p.k && (unsigned)ih < (unsigned)p.h &&
+                                (unsigned)iw < (unsigned)p.w_in;
+                const float* src = ok ? xg + xoff0 + (int64_t)c * p.hw + kr * p.w_in + j : xg;
+                cp_async4_zfill(as_base + slot * AS_STAGE + i * KSTEP * BM * 4, src, ok);
+            }
+#pragma unroll
+            for (int i = 0; i < B_PER; ++i) {
+                const int q = tid + i * THREADS;
+                if (!B_FULL && q >= B_CHUNKS) break;
+                const int row = q / (BN / 4);
+                const int col = (q % (BN / 4)) * 4;
+                const int kidx = kb + row;
+                const int co = n0 + col;
+                const uint32_t dst = bs_base + slot * BS_STAGE + (row * BN + col) * 4;
+                if (b_vec) {
+                    const int bytes = (kidx < p.k) ? min(max(p.co - co, 0), 4) * 4 : 0;
+                    cp_async16_zfill(dst, bytes ? wg + (int64_t)kidx * p.co + co : wg, bytes);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const bool okb = kidx < p.k && co + e < p.co;
+                        cp_async4_zfill(dst + e * 4, okb ? wg + (int64_t)kidx * p.co + co + e : wg,
+                                        okb);
+                    }
                 }
             }
         }
@@ -150,6 +230,8 @@ conv_ffma_kernel(const Problem p) {
         cp_async_commit();
     }
 
+    const float* a_rd = As + pg * 4;
+    const float* b_rd = Bs + cg * 4;
     for (int kt = 0; kt < ktiles; ++kt) {
         cp_async_wait<STAGES - 2>();
         __syncthreads();
@@ -159,12 +241,14 @@ conv_ffma_kernel(const Problem p) {
             cp_async_commit();
         }
         const int slot = kt % STAGES;
+        const float* ap = a_rd + slot * (BK * BM);
+        const float* bp = b_rd + slot * (BK * BN);
 #pragma unroll
         for (int kk = 0; kk < BK; ++kk) {
-            const float4 a0 = *reinterpret_cast<const float4*>(&As[slot][kk][pg * 4]);
-            const float4 a1 = *reinterpret_cast<const float4*>(&As[slot][kk][BM / 2 + pg * 4]);
-            const float4 b0 = *reinterpret_cast<const float4*>(&Bs[slot][kk][cg * 4]);
-            const float4 b1 = *reinterpret_cast<const float4*>(&Bs[slot][kk][BN / 2 + cg * 4]);
+            const float4 a0 = *reinterpret_cast<const float4*>(ap + kk * BM);
+            const float4 a1 = *reinterpret_cast<const float4*>(ap + kk * BM + BM / 2);
+            const float4 b0 = *reinterpret_cast<const float4*>(bp + kk * BN);
+            const float4 b1 = *reinterpret_cast<const float4*>(bp + kk * BN + BN / 2);
             const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
             const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
@@ -175,8 +259,58 @@ conv_ffma_kernel(const Problem p) {
     }
     cp_async_wait<0>();
 
-    // ---- epilogue: NCHW stores (split-K: partial plane `split` of the workspace)
-    float* out = p.splits > 1 ? p.ws + (int64_t)split * ((int64_t)p.m * p.co) : p.y;
+    // ---- split-K reduce_mode 1: deterministic last-arriver fixup
+    if (p.splits > 1 && p.reduce_mode == 1) {
+        const int64_t tile = (int64_t)blockIdx.x * gridDim.y + blockIdx.y;
+        float* part = p.ws + (tile * p.splits) * (BM * BN);
+        // layout [split][16 float4 groups][THREADS]: warp stores are contiguous
+        float4* mine = reinterpret_cast<float4*>(part + (int64_t)split * (BM * BN));
+#pragma unroll
+        for (int g = 0; g < 16; ++g)
+            mine[g * THREADS + tid] = make_float4(acc[g >> 1][(g & 1) * 4 + 0], acc[g >> 1][(g & 1) * 4 + 1],
+                                                  acc[g >> 1][(g & 1) * 4 + 2], acc[g >> 1][(g & 1) * 4 + 3]);
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) s_last = atomicAdd(p.counters + tile, 1) == p.splits - 1;
+        __syncthreads();
+        if (!s_last) return;
+        __threadfence();
+        // P_0 + P_1 + ... + P_{S-1} in split order (own partial re-read too);
+        // 8 independent loads in flight per round
+        const float4* base = reinterpret_cast<const float4*>(part) + tid;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            float4 s4[8];
+#pragma unroll
+            for (int g = 0; g < 8; ++g) s4[g] = __ldcg(base + (h * 8 + g) * THREADS);
+            for (int z = 1; z < p.splits; ++z) {
+                float4 v[8];
+#pragma unroll
+                for (int g = 0; g < 8; ++g)
+                    v[g] = __ldcg(base + (int64_t)z * (BM * BN / 4) + (h * 8 + g) * THREADS);
+#pragma unroll
+                for (int g = 0; g < 8; ++g) {
+                    s4[g].x += v[g].x;
+                    s4[g].y += v[g].y;
+                    s4[g].z += v[g].z;
+                    s4[g].w += v[g].w;
+                }
+            }
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                const int gg = h * 8 + g;
+                acc[gg >> 1][(gg & 1) * 4 + 0] = s4[g].x;
+                acc[gg >> 1][(gg & 1) * 4 + 1] = s4[g].y;
+                acc[gg >> 1][(gg & 1) * 4 + 2] = s4[g].z;
+                acc[gg >> 1][(gg & 1) * 4 + 3] = s4[g].w;
+            }
+        }
+        if (tid == 0) p.counters[tile] = 0;  // re-arm for the next launch
+    }
+
+    // ---- epilogue: NCHW stores (reduce_mode 2: partial plane `split` of ws)
+    float* out = (p.splits > 1 && p.reduce_mode == 2) ? p.ws + (int64_t)split * ((int64_t)p.m * p.co)
+                                                       : p.y;
     const bool vec_ok = (p.ohw & 3) == 0;
 #pragma unroll
     for (int ib = 0; ib < 2; ++ib) {
@@ -211,19 +345,29 @@ conv_ffma_kernel(const Problem p) {
     }
 }
 
-// y = sum over splits of the partial planes, in split order (deterministic).
-__global__ void splitk_reduce_kernel(const float* __restrict__ ws, float* __restrict__ y,
-                                     int64_t total, int splits) {
-    const int64_t total4 = total >> 2;
+// reduce_mode 2: y = sum of the partial planes in split order.
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ ws,
+                                                            float* __restrict__ y, int64_t total,
+                                                            int splits) {
+    const int64_t total4 = (total & 3) ? 0 : (total >> 2);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total4; i += stride) {
-        float4 s = reinterpret_cast<const float4*>(ws)[i];
-        for (int z = 1; z < splits; ++z) {
-            const float4 v = reinterpret_cast<const float4*>(ws + (int64_t)z * total)[i];
-            s.x += v.x;
-            s.y += v.y;
-            s.z += v.z;
-            s.w += v.w;
+        const float4* src = reinterpret_cast<const float4*>(ws) + i;
+        float4 s = __ldcg(src);
+        int z = 1;
+        for (; z + 3 < splits; z += 4) {  // 4 independent loads in flight
+            const float4 v0 = __ldcg(src + (int64_t)(z + 0) * total4);
+            const float4 v1 = __ldcg(src + (int64_t)(z + 1) * total4);
+            const float4 v2 = __ldcg(src + (int64_t)(z + 2) * total4);
+            const float4 v3 = __ldcg(src + (int64_t)(z + 3) * total4);
+            s.x += v0.x; s.y += v0.y; s.z += v0.z; s.w += v0.w;
+            s.x += v1.x; s.y += v1.y; s.z += v1.z; s.w += v1.w;
+            s.x += v2.x; s.y += v2.y; s.z += v2.z; s.w += v2.w;
+            s.x += v3.x; s.y += v3.y; s.z += v3.z; s.w += v3.w;
+        }
+        for (; z < splits; ++z) {
+            const float4 v = __ldcg(src + (int64_t)z * total4);
+            s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
         }
         reinterpret_cast<float4*>(y)[i] = s;
     }
@@ -236,24 +380,49 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, float* __rest
 }
 
 struct TileCfg {
-    int bm, bn, threads;
+    int bm, bn, threads, per_sm;
 };
 constexpr TileCfg kTiles[] = {
-    {128, 128, 256},  // 0: wide channel dimension
-    {128, 64, 128},   // 1: c_o <= 64
+    {128, 128, 256, 2},  // 0
+    {128, 64, 128, 3},   // 1
+    {256, 64, 256, 2},   // 2
+    {64, 128, 128, 3},   // 3
 };
+constexpr int kNumTiles = sizeof(kTiles) / sizeof(kTiles[0]);
+constexpr int kBKCvec = 16;
+constexpr int kBKGeneric = 8;
 
-template <int BM, int BN, int T>
-cudaError_t launch_tile(const Problem& p, int tap_kind, dim3 grid, cudaStream_t s) {
-    switch (tap_kind) {
-        case 1: conv_ffma_kernel<BM, BN, T, 3, 3, 1, 1><<<grid, T, 0, s>>>(p); break;
-        case 2: conv_ffma_kernel<BM, BN, T, 1, 1, 1, 1><<<grid, T, 0, s>>>(p); break;
-        case 3: conv_ffma_kernel<BM, BN, T, 7, 7, 2, 2><<<grid, T, 0, s>>>(p); break;
-        case 4: conv_ffma_kernel<BM, BN, T, 11, 11, 4, 4><<<grid, T, 0, s>>>(p); break;
-        case 5: conv_ffma_kernel<BM, BN, T, 5, 5, 1, 1><<<grid, T, 0, s>>>(p); break;
-        default: conv_ffma_kernel<BM, BN, T, 0, 0, 0, 0><<<grid, T, 0, s>>>(p); break;
-    }
+template <int BM, int BN, int T, int MINB, int BK, int KH, int KW, int SH, int SW, bool CVEC>
+cudaError_t launch_one(const Problem& p, dim3 grid, cudaStream_t s) {
+    constexpr int smem = kStages * BK * (BM + BN) * (int)sizeof(float);
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    auto kern = conv_ffma_kernel<BM, BN, T, MINB, BK, KH, KW, SH, SW, CVEC>;
+    std::call_once(once, [&] {
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    });
+    if (attr_err != cudaSuccess) return attr_err;
+    kern<<<grid, T, smem, s>>>(p);
     return cudaGetLastError();
+}
+
+template <int BM, int BN, int T, int MINB>
+cudaError_t launch_tile(const Problem& p, int tap_kind, bool cvec, dim3 grid, cudaStream_t s) {
+    constexpr int C = kBKCvec, G = kBKGeneric;
+    if (cvec) {
+        switch (tap_kind) {
+            case 1: return launch_one<BM, BN, T, MINB, C, 3, 3, 1, 1, true>(p, grid, s);
+            case 2: return launch_one<BM, BN, T, MINB, C, 1, 1, 1, 1, true>(p, grid, s);
+            case 5: return launch_one<BM, BN, T, MINB, C, 5, 5, 1, 1, true>(p, grid, s);
+            default: return launch_one<BM, BN, T, MINB, C, 0, 0, 0, 0, true>(p, grid, s);
+        }
+    }
+    switch (tap_kind) {
+        case 1: return launch_one<BM, BN, T, MINB, G, 3, 3, 1, 1, false>(p, grid, s);
+        case 3: return launch_one<BM, BN, T, MINB, G, 7, 7, 2, 2, false>(p, grid, s);
+        case 4: return launch_one<BM, BN, T, MINB, G, 11, 11, 4, 4, false>(p, grid, s);
+        default: return launch_one<BM, BN, T, MINB, G, 0, 0, 0, 0, false>(p, grid, s);
+    }
 }
 
 int tap_kind_of(const smmc_geom& g) {
@@ -267,52 +436,85 @@ int tap_kind_of(const smmc_geom& g) {
 
 }  // namespace
 
+// Wave-quantisation-aware choice of CTA tile and split-K factor.  Cost model:
+// a wave of `slots` CTAs runs per_sm CTAs per SM, so its time is proportional
+// to per_sm * BM * BN * (work per CTA in 8-deep tap blocks, plus a prologue /
+// epilogue term and ~3 blocks of partial-tile traffic when split), with a
+// small per-split overhead.
 FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) {
-    FfmaPlan pl{};
+    FfmaPlan best{};
+    double best_cost = 1e300;
     const int oh = (g.h + 2 * g.p_h - g.k_h) / g.s_h + 1;
     const int ow = (g.w + 2 * g.p_w - g.k_w) / g.s_w + 1;
     const int64_t m = (int64_t)g.n * oh * ow;
-    const int k = g.c_i * g.k_h * g.k_w;
-    pl.variant = g.c_o <= 64 ? 1 : 0;
-    const TileCfg t = kTiles[pl.variant];
-    pl.bm = t.bm;
-    pl.bn = t.bn;
-    pl.bk = kBK;
-    pl.threads = t.threads;
-    pl.tap_kind = tap_kind_of(g);
-    const int64_t tiles = ((m + t.bm - 1) / t.bm) * ((g.c_o + t.bn - 1) / t.bn);
-    const int ktiles = (k + kBK - 1) / kBK;
-    const int resident = t.threads >= 256 ? 2 : 3;
-    const int64_t target = (int64_t)sm_count * resident;
-    int splits = 1;
-    if (tiles < target) {
-        splits = (int)((target + tiles - 1) / tiles);
-        splits = std::min(splits, std::max(1, ktiles / 4));  // >= 4 tap blocks per split
-        splits = std::min(splits, 32);
+    const int taps = g.k_h * g.k_w;
+    const bool cvec = (g.c_i % kBKCvec) == 0 && g.k_h <= 32 && g.k_w <= 32;
+    const int bk = cvec ? kBKCvec : kBKGeneric;
+    const int kt_total = cvec ? taps * (g.c_i / bk) : (g.c_i * taps + bk - 1) / bk;
+    for (int v = 0; v < kNumTiles; ++v) {
+        const TileCfg t = kTiles[v];
+        const int64_t mt = (m + t.bm - 1) / t.bm;
+        const int64_t nt = (g.c_o + t.bn - 1) / t.bn;
+        const int64_t tiles = mt * nt;
+        const int64_t slots = (int64_t)sm_count * t.per_sm;
+        const int max_s = std::max(1, std::min(32, kt_total / 2));
+        for (int s = 1; s <= max_s; ++s) {
+            const int per = (kt_total + s - 1) / s;
+            const int sp = (kt_total + per - 1) / per;  // effective splits
+            if (sp != s) continue;
+            const int64_t ctas = tiles * sp;
+            const int64_t waves = (ctas + slots - 1) / slots;
+            const double work = per * (bk / 8.0) + 1.0 + (sp > 1 ? 3.0 : 0.0);
+            double cost = (double)waves * t.per_sm * t.bm * t.bn * work * (1.0 + 0.02 * (sp - 1));
+            if (cost < best_cost * 0.999) {
+                best_cost = cost;
+                best.variant = v;
+                best.bm = t.bm;
+                best.bn = t.bn;
+                best.threads = t.threads;
+                best.splits = sp;
+                best.kt_per_split = per;
+                best.tiles = tiles;
+            }
+        }
     }
-    int kt_per = (ktiles + splits - 1) / splits;
-    pl.k_per_split = kt_per * kBK;
-    pl.splits = (ktiles + kt_per - 1) / kt_per;
-    return pl;
+    best.bk = bk;
+    best.kt_total = kt_total;
+    best.cvec = cvec ? 1 : 0;
+    best.tap_kind = tap_kind_of(g);
+    best.reduce_mode = best.splits > 1 ? (best.splits <= 4 ? 1 : 2) : 0;
+    if (best.reduce_mode == 1) {
+        const size_t part = (size_t)best.tiles * best.splits * best.bm * best.bn * sizeof(float);
+        best.ws_counter_offset = (part + 255) & ~(size_t)255;
+        best.ws_bytes = best.ws_counter_offset + (size_t)best.tiles * sizeof(int);
+    } else if (best.reduce_mode == 2) {
+        best.ws_counter_offset = 0;
+        best.ws_bytes = (size_t)best.splits * (size_t)m * g.c_o * sizeof(float);
+    } else {
+        best.ws_bytes = 0;
+        best.ws_counter_offset = 0;
+    }
+    return best;
 }
 
 cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
     dim3 grid((p.m + pl.bm - 1) / pl.bm, (p.co + pl.bn - 1) / pl.bn, pl.splits);
     cudaError_t e;
-    if (pl.variant == 0)
-        e = launch_tile<128, 128, 256>(p, pl.tap_kind, grid, s);
-    else
-        e = launch_tile<128, 64, 128>(p, pl.tap_kind, grid, s);
+    switch (pl.variant) {
+        case 0: e = launch_tile<128, 128, 256, 2>(p, pl.tap_kind, pl.cvec, grid, s); break;
+        case 1: e = launch_tile<128, 64, 128, 3>(p, pl.tap_kind, pl.cvec, grid, s); break;
+        case 2: e = launch_tile<256, 64, 256, 2>(p, pl.tap_kind, pl.cvec, grid, s); break;
+        default: e = launch_tile<64, 128, 128, 3>(p, pl.tap_kind, pl.cvec, grid, s); break;
+    }
     count_launches(1);
-    return e;
-}
-
-cudaError_t launch_splitk_reduce(const Problem& p, cudaStream_t s) {
+    if (e != cudaSuccess || pl.reduce_mode != 2) return e;
     const int64_t total = (int64_t)p.m * p.co;
-    int blocks = (int)std::min<int64_t>((total / 4 + 255) / 256 + 1, 148 * 8);
+    const int blocks = (int)std::min<int64_t>((total / 4 + 255) / 256 + 1, 148 * 16);
     splitk_reduce_kernel<<<blocks, 256, 0, s>>>(p.ws, p.y, total, p.splits);
     count_launches(1);
     return cudaGetLastError();
 }
+
+int ffma_launches(const FfmaPlan& pl) { return pl.reduce_mode == 2 ? 2 : 1; }
 
 }  // namespace smmc

@@ -115,11 +115,9 @@ int check_mode(int mode) {
     return SMMC_OK;
 }
 
-size_t workspace_for(const smmc_geom& g, int mode, int oh, int ow, int sm_count) {
+size_t workspace_for(const smmc_geom& g, int mode, int sm_count) {
     if (mode != SMMC_MODE_FFMA || g.n == 0) return 0;
-    const FfmaPlan pl = plan_ffma(g, sm_count);
-    if (pl.splits <= 1) return 0;
-    return (size_t)pl.splits * (size_t)g.n * g.c_o * oh * ow * sizeof(float);
+    return plan_ffma(g, sm_count).ws_bytes;
 }
 
 // Per-device staging buffers for the *_host entry points.
@@ -148,7 +146,8 @@ int ensure(HostPool& hp, int i, size_t bytes) {
     int st = cuda_status(cudaMalloc(&hp.buf[i], bytes), "cudaMalloc(staging)");
     if (st) return st;
     hp.cap[i] = bytes;
-    return SMMC_OK;
+    // split-K counters must start at zero (kernels leave them zeroed)
+    return cuda_status(cudaMemset(hp.buf[i], 0, bytes), "cudaMemset(staging)");
 }
 
 int select_device(int device) {
@@ -206,27 +205,33 @@ int conv_device(const float* x, const float* w, float* y, const smmc_geom* g, in
     p.m = g->n * oh * ow;
     p.k = g->c_i * g->k_h * g->k_w;
     p.splits = 1;
-    p.k_per_split = p.k;
     if (mode == SMMC_MODE_EXACT) return cuda_status(launch_exact(p, stream), "conv_exact launch");
 
     const FfmaPlan pl = plan_ffma(*g, sms);
     p.splits = pl.splits;
-    p.k_per_split = pl.k_per_split;
+    p.kt_total = pl.kt_total;
+    p.kt_per_split = pl.kt_per_split;
+    p.cvec = pl.cvec;
+    p.reduce_mode = pl.reduce_mode;
     if (pl.splits > 1) {
-        const size_t need = workspace_for(*g, mode, oh, ow, sms);
-        if (!ws || ws_bytes < need) {
-            set_error("workspace of %zu bytes required (got %zu)", need, ws_bytes);
+        if (!ws || ws_bytes < pl.ws_bytes) {
+            set_error("workspace of %zu bytes required (got %zu)", pl.ws_bytes, ws_bytes);
             return SMMC_EWORKSPACE;
         }
-        if ((uintptr_t)ws & 15) {
-            set_error("workspace must be 16-byte aligned");
+        if ((uintptr_t)ws & 255) {
+            set_error("workspace must be 256-byte aligned");
             return SMMC_ESHAPE;
         }
     }
-    if ((st = cuda_status(launch_ffma(p, pl, stream), "conv_ffma launch"))) return st;
-    if (pl.splits > 1)
-        return cuda_status(launch_splitk_reduce(p, stream), "splitk_reduce launch");
-    return SMMC_OK;
+    if (pl.reduce_mode == 1) {
+        p.counters = reinterpret_cast<int*>(static_cast<char*>(ws) + pl.ws_counter_offset);
+        // arrival counters must read zero at kernel start; the workspace may
+        // hold another problem's partials where this plan keeps its counters
+        if ((st = cuda_status(cudaMemsetAsync(p.counters, 0, (size_t)pl.tiles * sizeof(int), stream),
+                              "cudaMemsetAsync(split-K counters)")))
+            return st;
+    }
+    return cuda_status(launch_ffma(p, pl, stream), "conv_ffma launch");
 }
 
 }  // namespace
@@ -252,7 +257,7 @@ int smmc_geom_check(const smmc_geom* g, int32_t* out_h, int32_t* out_w) {
 size_t smmc_workspace_bytes(const smmc_geom* g, int mode) {
     int oh = 0, ow = 0;
     if (check_geom(g, &oh, &ow) || check_mode(mode)) return 0;
-    return workspace_for(*g, mode, oh, ow, sm_count_for(current_device()));
+    return workspace_for(*g, mode, sm_count_for(current_device()));
 }
 
 int smmc_plan_launches(const smmc_geom* g, int mode) {
@@ -260,7 +265,7 @@ int smmc_plan_launches(const smmc_geom* g, int mode) {
     if (check_geom(g, &oh, &ow) || check_mode(mode)) return -1;
     if (g->n == 0) return 0;
     if (mode == SMMC_MODE_EXACT) return 1;
-    return plan_ffma(*g, sm_count_for(current_device())).splits > 1 ? 2 : 1;
+    return ffma_launches(plan_ffma(*g, sm_count_for(current_device())));
 }
 
 int smmc_plan_describe(const smmc_geom* g, int mode, char* buf, size_t len) {
@@ -274,8 +279,13 @@ int smmc_plan_describe(const smmc_geom* g, int mode, char* buf, size_t len) {
         return SMMC_OK;
     }
     const FfmaPlan pl = plan_ffma(*g, sm_count_for(current_device()));
-    snprintf(buf, len, "ffma: tile %dx%dx%d, %d threads, taps=%d, split_k=%d (k_per_split=%d)",
-             pl.bm, pl.bn, pl.bk, pl.threads, pl.tap_kind, pl.splits, pl.k_per_split);
+    snprintf(buf, len,
+             "ffma: tile %dx%dx%d, %d threads, taps=%d, %s K order, split_k=%d (%d of %d tap blocks "
+             "each, reduce=%s), %lld tiles",
+             pl.bm, pl.bn, pl.bk, pl.threads, pl.tap_kind, pl.cvec ? "tap-major" : "(c,j,k)",
+             pl.splits, pl.kt_per_split, pl.kt_total,
+             pl.reduce_mode == 0 ? "none" : (pl.reduce_mode == 1 ? "last-arriver" : "kernel"),
+             (long long)pl.tiles);
     return SMMC_OK;
 }
 
@@ -308,7 +318,7 @@ int smmc_conv2d_fwd_f32_host(const float* x, const float* w_smm, float* y, const
     const size_t xb = (size_t)g->n * g->c_i * g->h * g->w * sizeof(float);
     const size_t wb = (size_t)g->c_i * g->k_w * g->k_h * g->c_o * sizeof(float);
     const size_t yb = (size_t)g->n * g->c_o * oh * ow * sizeof(float);
-    const size_t wsb = workspace_for(*g, mode, oh, ow, sm_count_for(device));
+    const size_t wsb = workspace_for(*g, mode, sm_count_for(device));
     if ((st = ensure(hp, 0, xb)) || (st = ensure(hp, 1, wb)) || (st = ensure(hp, 2, yb)) ||
         (st = ensure(hp, 3, wsb)))
         return st;

@@ -17,14 +17,18 @@ struct Problem {
     const float* x;      // (n, c_i, h, w)
     const float* w;      // (c_i, k_w, k_h, c_o) == row-major [K][c_o], K = c_i*k_w*k_h
     float* y;            // (n, c_o, oh, ow)
-    float* ws;           // split-K partial planes [splits][n*c_o*oh*ow] (or null)
+    float* ws;           // split-K partial tiles [tiles][splits][BM*BN] (or null)
+    int* counters;       // split-K arrival counters [tiles] (zero at rest)
     int n, c, h, w_in, co, kh, kw, sh, sw, ph, pw, oh, ow;
     int hw;              // h*w
     int ohw;             // oh*ow
     int m;               // GEMM rows: n*oh*ow output pixels
     int k;               // GEMM depth: c_i*k_w*k_h taps (SMM (c, j, k) order)
-    int k_per_split;     // multiple of the kernel's BK
+    int kt_total;        // BK-wide tap blocks along K
+    int kt_per_split;    // tap blocks per split
     int splits;
+    int cvec;            // 1: tap-major K order (c_i % BK == 0)
+    int reduce_mode;     // split-K: 0 none, 1 in-kernel last-arriver, 2 separate reduce kernel
 };
 
 // Last-error / launch bookkeeping (defined in smmc_api.cu).
@@ -35,16 +39,22 @@ void count_launches(int n);
 // a cudaError_t from cudaGetLastError() after the launch.
 cudaError_t launch_exact(const Problem& p, cudaStream_t s);
 struct FfmaPlan {
-    int variant;     // index into the tile table
-    int bm, bn, bk;  // CTA tile
+    int variant;       // index into the tile table
+    int bm, bn, bk;    // CTA tile
     int threads;
-    int splits;      // split-K factor (1 = fused, no workspace)
-    int k_per_split;
-    int tap_kind;    // 0 generic, 1: 3x3s1, 2: 1x1s1, 3: 7x7s2, 4: 11x11s4, 5: 5x5s1
+    int splits;        // split-K factor (1 = no workspace)
+    int kt_total;      // BK-wide tap blocks
+    int kt_per_split;
+    int tap_kind;      // 0 generic, 1: 3x3s1, 2: 1x1s1, 3: 7x7s2, 4: 11x11s4, 5: 5x5s1
+    int cvec;          // tap-major K order
+    int reduce_mode;   // 0 none, 1 in-kernel last-arriver fixup, 2 separate reduce kernel
+    int64_t tiles;     // pixel tiles x channel tiles
+    size_t ws_bytes;   // partial tiles + counters
+    size_t ws_counter_offset;
 };
 FfmaPlan plan_ffma(const smmc_geom& g, int sm_count);
 cudaError_t launch_ffma(const Problem& p, const FfmaPlan& plan, cudaStream_t s);
-cudaError_t launch_splitk_reduce(const Problem& p, cudaStream_t s);
+int ffma_launches(const FfmaPlan& plan);
 cudaError_t launch_extract_slice(const float* x, const smmc_geom& g, int c, int j,
                                  float* buf, cudaStream_t s);
 cudaError_t launch_scalar_matrix_fma(float alpha, const float* src, int64_t ss,

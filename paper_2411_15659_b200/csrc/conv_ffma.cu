@@ -22,7 +22,9 @@
 //     staged by 16-byte cp.async into a BK x BN tile and read back as
 //     broadcast LDS.128;
 //   * a STAGES-deep cp.async ring overlaps the loads of block t+STAGES-1 with
-//     the FFMAs of block t.  Per k step a thread issues 4 LDS.128 + 64 FFMA.
+//     the FMAs of block t.  Per k step a thread issues 4 LDS.128 + 32 FFMA2
+//     (Blackwell packed fp32 FMA: one scalar pixel value times a pair of
+//     channel weights), i.e. 64 FMAs in 36 issue slots.
 //
 // K order.  When c_i % BK == 0 ("cvec") a BK block is one tap (j, k) x BK
 // consecutive input channels: a thread's A elements in a block share one
@@ -218,11 +220,12 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
         }
     };
 
-    float acc[8][8];
+    // accumulators as FFMA2 lane pairs: acc2[i][jp] = (channel 2jp, 2jp+1) of pixel i
+    uint64_t acc2[8][4];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+        for (int j = 0; j < 4; ++j) acc2[i][j] = 0ull;
 
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
@@ -247,17 +250,27 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
         for (int kk = 0; kk < BK; ++kk) {
             const float4 a0 = *reinterpret_cast<const float4*>(ap + kk * BM);
             const float4 a1 = *reinterpret_cast<const float4*>(ap + kk * BM + BM / 2);
-            const float4 b0 = *reinterpret_cast<const float4*>(bp + kk * BN);
-            const float4 b1 = *reinterpret_cast<const float4*>(bp + kk * BN + BN / 2);
+            const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(bp + kk * BN);
+            const ulonglong2 b1 = *reinterpret_cast<const ulonglong2*>(bp + kk * BN + BN / 2);
             const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-            const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+            const uint64_t b[4] = {b0.x, b0.y, b1.x, b1.y};
 #pragma unroll
             for (int i = 0; i < 8; ++i)
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+                for (int j = 0; j < 4; ++j) acc2[i][j] = ffma2_bcast(a[i], b[j], acc2[i][j]);
         }
     }
     cp_async_wait<0>();
+
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float2 v = unpack2(acc2[i][j]);
+            acc[i][2 * j] = v.x;
+            acc[i][2 * j + 1] = v.y;
+        }
 
     // ---- split-K reduce_mode 1: deterministic last-arriver fixup
     if (p.splits > 1 && p.reduce_mode == 1) {

@@ -79,6 +79,29 @@ __device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, 
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(bytes));
 }
 
+// Blackwell packed FP32 FMA (SASS FFMA2): d = a*b + c on two lanes, each an
+// IEEE round-to-nearest fma.  The scalar `a` is broadcast to both lanes;
+// ptxas folds the {a, a} pair into FFMA2's .F32 scalar-operand form.
+__device__ __forceinline__ uint64_t ffma2_bcast(float a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("{\n\t.reg .b64 t;\n\tmov.b64 t, {%1, %1};\n\tfma.rn.f32x2 %0, t, %2, %3;\n\t}"
+        : "=l"(d)
+        : "f"(a), "l"(b), "l"(c));
+    return d;
+}
+
+__device__ __forceinline__ uint64_t pack2(float lo, float hi) {
+    uint64_t d;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
+    return d;
+}
+
+__device__ __forceinline__ float2 unpack2(uint64_t v) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 
 template <int N>

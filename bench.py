@@ -53,7 +53,9 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="ffma", choices=["ffma", "exact"])
+    ap.add_argument("--mode", default="ffma", choices=["ffma", "exact", "bf16_tc"],
+                    help="ffma: fp32 product kernel; exact: bitwise mode; bf16_tc: separately "
+                         "labelled bf16-input tcgen05 variant (stride-1 layers)")
     ap.add_argument("--replicas", type=int, default=0, help="0 = auto (>2x L2 between reuses)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -239,14 +241,29 @@ def run_ours(args):
     step_bytes = sum(4 * (L["x_host"].size + L["w_host"].size + L["n"] * L["gl"].out_channels
                           * L["gl"].out_h * L["gl"].out_w) for L in layers)
     R = args.replicas or max(1, min(8, -(-3 * L2_BYTES // max(step_bytes, 1)) + 1))
+    tc = args.mode == "bf16_tc"
+    if tc:
+        for L in layers:
+            if not device.tc_supported(L["gl"], max(L["n"], 1)):
+                raise SystemExit(f"--mode bf16_tc: layer {L['name']} is not supported "
+                                 "(stride 1 and c_i % 8 == 0 required)")
     for L in layers:
         xd = torch.from_numpy(L["x_host"]).to(dev)
         wd = torch.from_numpy(L["w_host"]).to(dev)
-        L["x"] = [xd] + [xd.clone() for _ in range(R - 1)]
-        L["w"] = [wd] + [wd.clone() for _ in range(R - 1)]
+        if tc:
+            # untimed packs: weights once per layer (as the reference's repack),
+            # inputs once per replica (the variant's input is bf16 NHWC)
+            xb = device.pack_input_bf16(xd, L["gl"])
+            L["xb"] = [xb] + [xb.clone() for _ in range(R - 1)]
+            wt = device.pack_weights_bf16(wd, L["gl"])
+            L["wt"] = [wt] + [wt.clone() for _ in range(R - 1)]
+            del xd, wd
+        else:
+            L["x"] = [xd] + [xd.clone() for _ in range(R - 1)]
+            L["w"] = [wd] + [wd.clone() for _ in range(R - 1)]
         shape = (L["n"],) + L["gl"].output_shape
         L["y"] = [torch.empty(shape, device=dev) for _ in range(R)]
-        need = _native.workspace_bytes(L["gl"], L["n"], args.mode)
+        need = 0 if tc else _native.workspace_bytes(L["gl"], L["n"], args.mode)
         L["ws"] = torch.empty(max(need, 16), dtype=torch.uint8, device=dev)
         if L["shard"] == "cout":
             L["gather"] = torch.empty((world,) + shape, device=dev)
@@ -255,8 +272,11 @@ def run_ours(args):
     def run_layer(L, r):
         if L["n"] == 0:
             return
-        device.conv2d(L["x"][r], L["w"][r], L["gl"], mode=args.mode, out=L["y"][r],
-                      workspace=L["ws"])
+        if tc:
+            device.conv2d_bf16_tc(L["xb"][r], L["wt"][r], L["gl"], out=L["y"][r])
+        else:
+            device.conv2d(L["x"][r], L["w"][r], L["gl"], mode=args.mode, out=L["y"][r],
+                          workspace=L["ws"])
         if L["shard"] == "cout":
             all_gather_cout(L["y"][r], L["gather"], L["full"], L["g"].out_channels, world)
 
@@ -337,23 +357,34 @@ def run_ours(args):
     sm_max = float(pk.get("sm_max_mhz", 1965.0))
     fp32_peak_tf = sm_count * FFMA_PER_SM_PER_CLK * 2 * sm_max * 1e6 / 1e12
     hbm_peak = float(pk.get("hbm_gbs", 6650.0))
+    bf16_peak_tf = float(pk.get("bf16_tflops", 1590.0))
+    comp_peak_tf = bf16_peak_tf if tc else fp32_peak_tf
     details = []
     for li, L in enumerate(layers):
         d = per_layer[li]
         avg = sum(d) / len(d)
         tf = L["flops"] / (avg / 1e3) / 1e12 if avg > 0 else 0.0
         gl = L["gl"]
-        byts = gl.compulsory_bytes(L["n"])
-        t_roof = max(L["flops"] / (fp32_peak_tf * 1e12), byts / (hbm_peak * 1e9))
+        byts = (gl.compulsory_bytes(L["n"], in_bytes=2, w_bytes=2) if tc
+                else gl.compulsory_bytes(L["n"]))
+        t_comp = L["flops"] / (comp_peak_tf * 1e12)
+        t_mem = byts / (hbm_peak * 1e9)
+        t_roof = max(t_comp, t_mem)
+        achieved_gbs = byts / (avg / 1e3) / 1e9 if avg > 0 else 0.0
         details.append({
             "layer": L["name"], "n": L["n"], "shard": L["shard"],
             "gflop": round(L["flops"] / 1e9, 4), "ms_avg": round(avg, 5),
             "ms_min": round(min(d), 5), "tflops": round(tf, 3),
             "frac_fp32_peak": round(tf / fp32_peak_tf, 4),
             "frac_roofline": round(t_roof * 1e3 / avg, 4) if avg > 0 else None,
+            "bound": "hbm" if t_mem > t_comp else ("tensor" if tc else "fp32"),
+            "achieved_gbs": round(achieved_gbs, 1),
+            "compulsory_bytes": byts,
             "flop_per_byte": round(L["flops"] / byts, 1),
-            "plan": _native.plan_describe(gl, L["n"], args.mode) if L["n"] else "",
-            "launches_per_call": _native.plan_launches(gl, L["n"], args.mode) if L["n"] else 0})
+            "plan": ("tcgen05 bf16 128x128x64, 3 stages, TMA SW128" if tc else
+                     (_native.plan_describe(gl, L["n"], args.mode) if L["n"] else "")),
+            "launches_per_call": 1 if tc else
+            (_native.plan_launches(gl, L["n"], args.mode) if L["n"] else 0)})
     dom = max(details, key=lambda d: d["ms_avg"])
     traffic = None
     tfile = ROOT / "profiles" / "traffic.json"
@@ -362,13 +393,32 @@ def run_ours(args):
             traffic = json.loads(tfile.read_text()).get(dom["layer"])
         except ValueError:
             traffic = None
-    roofline = {"bound": "fp32", "achieved": dom["tflops"], "peak": round(fp32_peak_tf, 2),
-                "unit": "TFLOP/s", "frac": dom["frac_fp32_peak"], "traffic": traffic,
-                "kernel": f"conv_ffma_kernel ({dom['layer']}: {dom['plan']})",
-                "peak_source": f"nominal FP32 FFMA peak {sm_count} SM x 128 x 2 x {sm_max:.0f} MHz "
-                               "(sm_max_mhz of MEASURED_PEAKS.json; no measured FP32 peak exists)",
-                "achieved_def": "dense algorithmic FLOPs of one launch / its avg CUDA-event "
-                                "duration inside the timed graph"}
+    if dom["bound"] == "hbm":
+        roofline = {"bound": "hbm", "achieved": dom["achieved_gbs"], "peak": hbm_peak,
+                    "unit": "GB/s", "frac": round(dom["achieved_gbs"] / hbm_peak, 4),
+                    "traffic": traffic,
+                    "kernel": f"{'conv_tc_bf16_kernel' if tc else 'conv_ffma_kernel'} "
+                              f"({dom['layer']}: {dom['plan']})",
+                    "peak_source": "hbm_gbs of MEASURED_PEAKS.json (measured copy bandwidth)",
+                    "achieved_def": "compulsory bytes (input + weights + output) of one launch / "
+                                    "its avg CUDA-event duration inside the timed graph"}
+    elif tc:
+        roofline = {"bound": "tensor", "achieved": dom["tflops"], "peak": bf16_peak_tf,
+                    "unit": "TFLOP/s", "frac": round(dom["tflops"] / bf16_peak_tf, 4),
+                    "traffic": traffic,
+                    "kernel": f"conv_tc_bf16_kernel ({dom['layer']}: {dom['plan']})",
+                    "peak_source": "bf16_tflops (burst) of MEASURED_PEAKS.json (cuBLAS bf16 GEMM)",
+                    "achieved_def": "dense algorithmic FLOPs of one launch / its avg CUDA-event "
+                                    "duration inside the timed graph"}
+    else:
+        roofline = {"bound": "fp32", "achieved": dom["tflops"], "peak": round(fp32_peak_tf, 2),
+                    "unit": "TFLOP/s", "frac": dom["frac_fp32_peak"], "traffic": traffic,
+                    "kernel": f"conv_ffma_kernel ({dom['layer']}: {dom['plan']})",
+                    "peak_source": f"nominal FP32 FFMA peak {sm_count} SM x 128 x 2 x "
+                                   f"{sm_max:.0f} MHz (sm_max_mhz of MEASURED_PEAKS.json; no "
+                                   "measured FP32 peak exists)",
+                    "achieved_def": "dense algorithmic FLOPs of one launch / its avg CUDA-event "
+                                    "duration inside the timed graph"}
 
     # ---- e2e: host buffers through the C ABI host entry (H2D + conv + D2H)
     e2e = None
@@ -388,7 +438,8 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(max_ms / args.steps, 5), "higher_is_better": True,
             "scaling": "strong" if (args.config == 5 and world > 1) else "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "vs_baseline": None, "dtype": "bf16-in/f32-acc" if tc else "f32",
+            "data": "synthetic",
             "config": {"workload": f"BASELINE config {args.config}: {CONFIGS[args.config]['title']}",
                        "layers": [L["name"] for L in layers],
                        "mode": args.mode,
@@ -421,7 +472,9 @@ def run_e2e(args, layers, world, dev):
     import torch
     import torch.distributed as dist
 
-    from paper_2411_15659_b200 import _native
+    from paper_2411_15659_b200 import _native, device
+    if args.mode == "bf16_tc":
+        return run_e2e_tc(args, layers, world, dev)
     lib = _native.lib()
     bufs = []
     h2d = d2h = 0
@@ -461,6 +514,52 @@ def run_e2e(args, layers, world, dev):
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
             "path": "smmc_conv2d_fwd_f32_host (C ABI, pinned host buffers, synchronous), "
                     "wall clock, max over ranks"}
+
+
+def run_e2e_tc(args, layers, world, dev):
+    """bf16 variant end to end through the public device API: pinned fp32 NCHW
+    input H2D, on-device bf16 NHWC pack, tcgen05 conv, fp32 output D2H."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_15659_b200 import device
+    bufs = []
+    h2d = d2h = 0
+    for L in layers:
+        if L["n"] == 0:
+            continue
+        xh = torch.from_numpy(L["x_host"]).pin_memory()
+        yh = torch.empty((L["n"],) + L["gl"].output_shape).pin_memory()
+        xd = torch.empty_like(xh, device=dev)
+        bufs.append((L, xh, yh, xd))
+        h2d += xh.numel() * 4
+        d2h += yh.numel() * 4
+
+    def step():
+        for L, xh, yh, xd in bufs:
+            xd.copy_(xh, non_blocking=True)
+            xb = device.pack_input_bf16(xd, L["gl"], out=L["xb"][0])
+            y = device.conv2d_bf16_tc(xb, L["wt"][0], L["gl"], out=L["y"][0])
+            yh.copy_(y, non_blocking=True)
+        torch.cuda.synchronize()
+
+    step()
+    steps = max(1, min(args.steps, 10))
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    dt = time.perf_counter() - t0
+    t = torch.tensor([dt], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dt = float(t.item())
+    flops = sum(L["flops"] for L in layers) * world
+    return {"value": round(flops * steps / dt / 1e9, 2), "unit": "GFLOP/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
+            "path": "device.pack_input_bf16 + device.conv2d_bf16_tc (C ABI) with pinned fp32 "
+                    "host input/output, wall clock, max over ranks"}
 
 
 def cpu_baseline(args, layers):

@@ -132,6 +132,31 @@ SMMC_API int smmc_scalar_matrix_fma_f32_host(float alpha, const float* src,
                                     int64_t dst_row_stride, int32_t rows,
                                     int32_t cols, int device);
 
+/* ---------------------------------------------------------------------------
+ * Separately labelled tensor-core variant (BASELINE config 5): bf16 inputs,
+ * fp32 accumulation in TMEM (tcgen05), fp32 NCHW output.  Parity bar
+ * 2e-2 * max|ref| against the fp32 oracle.  Stride 1, c_i % 8 == 0.
+ * Replaces the same compute as smmc_conv2d_fwd_f32 (smm.py:226-306), with the
+ * input in channels-last bf16 and the weights packed per tap.
+ * ------------------------------------------------------------------------- */
+
+/* 1 if smmc_conv2d_fwd_bf16_tc supports this geometry, else 0. */
+SMMC_API int smmc_tc_supported(const smmc_geom* g);
+
+/* x fp32 NCHW (n, c_i, h, w) -> x_nhwc bf16 (n, h, w, c_i), device, async. */
+SMMC_API int smmc_pack_input_bf16_nhwc(const float* x, uint16_t* x_nhwc, const smmc_geom* g,
+                                       void* stream);
+
+/* w_smm fp32 (c_i, k_w, k_h, c_o) -> w_tc bf16 (k_w*k_h, c_o, c_i), tap = j*k_h + k
+ * (the tensor-core analogue of repack_weights, smm.py:164-167). */
+SMMC_API int smmc_pack_weights_bf16(const float* w_smm, uint16_t* w_tc, const smmc_geom* g,
+                                    void* stream);
+
+/* y fp32 NCHW = conv(x_nhwc, w_tc): tcgen05 implicit GEMM over the k_h*k_w
+ * shifted windows, TMA zero-fill padding.  Device pointers, async. */
+SMMC_API int smmc_conv2d_fwd_bf16_tc(const uint16_t* x_nhwc, const uint16_t* w_tc, float* y,
+                                     const smmc_geom* g, void* stream);
+
 /* Number of kernels smmc_conv2d_fwd_f32 launches for this problem/mode. */
 SMMC_API int smmc_plan_launches(const smmc_geom* g, int mode);
 

@@ -38,6 +38,8 @@ EXPORTED_SYMBOLS = (
     "smmc_extract_slice_f32", "smmc_scalar_matrix_fma_f32",
     "smmc_extract_slice_f32_host", "smmc_scalar_matrix_fma_f32_host",
     "smmc_plan_launches", "smmc_plan_describe", "smmc_launch_count",
+    "smmc_tc_supported", "smmc_pack_input_bf16_nhwc", "smmc_pack_weights_bf16",
+    "smmc_conv2d_fwd_bf16_tc",
 )
 
 
@@ -92,6 +94,10 @@ _SIGNATURES = {
     "smmc_plan_describe": (ctypes.c_int, [_GP, ctypes.c_int, ctypes.c_char_p,
                                           ctypes.c_size_t]),
     "smmc_launch_count": (ctypes.c_uint64, []),
+    "smmc_tc_supported": (ctypes.c_int, [_GP]),
+    "smmc_pack_input_bf16_nhwc": (ctypes.c_int, [_P, _P, _GP, _P]),
+    "smmc_pack_weights_bf16": (ctypes.c_int, [_P, _P, _GP, _P]),
+    "smmc_conv2d_fwd_bf16_tc": (ctypes.c_int, [_P, _P, _P, _GP, _P]),
 }
 
 

@@ -336,6 +336,66 @@ int smmc_conv2d_fwd_f32_host(const float* x, const float* w_smm, float* y, const
     return cuda_status(cudaStreamSynchronize(s), "conv (host path)");
 }
 
+int smmc_tc_supported(const smmc_geom* g) {
+    int oh = 0, ow = 0;
+    if (check_geom(g, &oh, &ow)) return 0;
+    smmc_geom gg = *g;
+    if (gg.n == 0) gg.n = 1;
+    return plan_tc(gg).supported ? 1 : 0;
+}
+
+int smmc_pack_input_bf16_nhwc(const float* x, uint16_t* x_nhwc, const smmc_geom* g, void* stream) {
+    int oh = 0, ow = 0;
+    int st = check_geom(g, &oh, &ow);
+    if (st) return st;
+    if (g->n == 0) return SMMC_OK;
+    if (!x || !x_nhwc) {
+        set_error("x and x_nhwc must be non-NULL device pointers");
+        return SMMC_ESHAPE;
+    }
+    return cuda_status(launch_pack_input_nhwc(x, x_nhwc, *g, static_cast<cudaStream_t>(stream)),
+                       "pack_input_nhwc launch");
+}
+
+int smmc_pack_weights_bf16(const float* w_smm, uint16_t* w_tc, const smmc_geom* g, void* stream) {
+    int oh = 0, ow = 0;
+    int st = check_geom(g, &oh, &ow);
+    if (st) return st;
+    if (!w_smm || !w_tc) {
+        set_error("w_smm and w_tc must be non-NULL device pointers");
+        return SMMC_ESHAPE;
+    }
+    return cuda_status(launch_pack_weights_bf16(w_smm, w_tc, *g, static_cast<cudaStream_t>(stream)),
+                       "pack_weights_bf16 launch");
+}
+
+int smmc_conv2d_fwd_bf16_tc(const uint16_t* x_nhwc, const uint16_t* w_tc, float* y,
+                            const smmc_geom* g, void* stream) {
+    int oh = 0, ow = 0;
+    int st = check_geom(g, &oh, &ow);
+    if (st) return st;
+    if (g->n == 0) return SMMC_OK;
+    if (!x_nhwc || !w_tc || !y) {
+        set_error("x_nhwc, w_tc and y must be non-NULL device pointers");
+        return SMMC_ESHAPE;
+    }
+    if (((uintptr_t)x_nhwc | (uintptr_t)w_tc) & 15) {
+        set_error("x_nhwc and w_tc must be 16-byte aligned (TMA)");
+        return SMMC_ESHAPE;
+    }
+    const char* why = "";
+    cudaError_t e = launch_tc_bf16(x_nhwc, w_tc, y, *g, static_cast<cudaStream_t>(stream), &why);
+    if (e == cudaErrorNotSupported) {
+        set_error("%s", why);
+        return SMMC_EUNSUPPORTED;
+    }
+    if (e != cudaSuccess && why[0]) {
+        set_error("%s (%s)", why, cudaGetErrorString(e));
+        return SMMC_ECUDA;
+    }
+    return cuda_status(e, "conv_tc_bf16 launch");
+}
+
 int smmc_extract_slice_f32(const float* x, const smmc_geom* g, int32_t c, int32_t j, float* buf,
                            void* stream) {
     int oh = 0, ow = 0;

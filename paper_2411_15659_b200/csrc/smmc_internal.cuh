@@ -55,6 +55,20 @@ struct FfmaPlan {
 FfmaPlan plan_ffma(const smmc_geom& g, int sm_count);
 cudaError_t launch_ffma(const Problem& p, const FfmaPlan& plan, cudaStream_t s);
 int ffma_launches(const FfmaPlan& plan);
+// bf16 tensor-core variant (conv_tc.cu)
+struct TcPlan {
+    int supported;
+    int flat;
+    int tw, th, nb;
+    int64_t tiles_m;
+    int tiles_n;
+};
+TcPlan plan_tc(const smmc_geom& g);
+cudaError_t launch_tc_bf16(const uint16_t* x_nhwc, const uint16_t* w_tc, float* y, const smmc_geom& g,
+                           cudaStream_t s, const char** why);
+cudaError_t launch_pack_input_nhwc(const float* x, uint16_t* out, const smmc_geom& g, cudaStream_t s);
+cudaError_t launch_pack_weights_bf16(const float* w, uint16_t* out, const smmc_geom& g,
+                                     cudaStream_t s);
 cudaError_t launch_extract_slice(const float* x, const smmc_geom& g, int c, int j,
                                  float* buf, cudaStream_t s);
 cudaError_t launch_scalar_matrix_fma(float alpha, const float* src, int64_t ss,

@@ -120,3 +120,105 @@ class SmmConv2d:
     def __call__(self, x, out=None):
         return conv2d(x, self.weights_smm, self.geom, mode=self.mode, out=out,
                       workspace=self.workspace_for(x.shape[0]))
+
+
+# --------------------------------------------------------------------------
+# Separately labelled tensor-core variant: bf16 inputs, fp32 accumulation in
+# TMEM (tcgen05), fp32 NCHW output.  Parity bar 2e-2 * max|ref| (BASELINE
+# config 5).  Input is channels-last bf16, weights are packed per tap.
+# --------------------------------------------------------------------------
+
+def tc_supported(geom, batch=1):
+    g = _native.Geom.of(geom, max(batch, 1))
+    return bool(_native.lib().smmc_tc_supported(ctypes.byref(g)))
+
+
+def _stream_ptr(torch, dev):
+    s = torch.cuda.current_stream(dev).cuda_stream
+    return ctypes.c_void_p(s) if s else None
+
+
+def pack_input_bf16(x, geom, out=None):
+    """fp32 NCHW (N, c_i, h, w) -> bf16 NHWC (N, h, w, c_i) on the device."""
+    torch = _torch()
+    n = x.shape[0]
+    _check_tensor(x, (n,) + geom.input_shape, "input batch")
+    if out is None:
+        out = torch.empty((n, geom.in_h, geom.in_w, geom.in_channels), dtype=torch.bfloat16,
+                          device=x.device)
+    g = _native.Geom.of(geom, n)
+    with torch.cuda.device(x.device):
+        _native.check(_native.lib().smmc_pack_input_bf16_nhwc(
+            ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()), ctypes.byref(g),
+            _stream_ptr(torch, x.device)), "smmc_pack_input_bf16_nhwc")
+    return out
+
+
+def pack_weights_bf16(weights_smm, geom):
+    """fp32 (c_i, k_w, k_h, c_o) -> bf16 (k_w*k_h, c_o, c_i) on the device."""
+    torch = _torch()
+    _check_tensor(weights_smm, geom.weights_smm_shape, "repacked weight tensor")
+    out = torch.empty((geom.k_w * geom.k_h, geom.out_channels, geom.in_channels),
+                      dtype=torch.bfloat16, device=weights_smm.device)
+    g = _native.Geom.of(geom, 1)
+    with torch.cuda.device(weights_smm.device):
+        _native.check(_native.lib().smmc_pack_weights_bf16(
+            ctypes.c_void_p(weights_smm.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+            ctypes.byref(g), _stream_ptr(torch, weights_smm.device)), "smmc_pack_weights_bf16")
+    return out
+
+
+def conv2d_bf16_tc(x_nhwc, w_tc, geom, out=None):
+    """tcgen05 bf16 conv: x_nhwc bf16 (N, h, w, c_i), w_tc bf16 (taps, c_o, c_i)
+    -> fp32 NCHW (N, c_o, h', w'), on torch's current stream."""
+    torch = _torch()
+    if not isinstance(x_nhwc, torch.Tensor) or x_nhwc.dim() != 4 or not x_nhwc.is_cuda \
+            or x_nhwc.dtype != torch.bfloat16 or not x_nhwc.is_contiguous():
+        raise ShapeMismatchError("x_nhwc must be a contiguous CUDA bf16 (N, h, w, c_i) tensor")
+    n = x_nhwc.shape[0]
+    if tuple(x_nhwc.shape[1:]) != (geom.in_h, geom.in_w, geom.in_channels):
+        raise ShapeMismatchError(f"x_nhwc has shape {tuple(x_nhwc.shape)}")
+    if tuple(w_tc.shape) != (geom.k_w * geom.k_h, geom.out_channels, geom.in_channels) \
+            or w_tc.dtype != torch.bfloat16 or not w_tc.is_cuda:
+        raise ShapeMismatchError("w_tc must be bf16 (k_w*k_h, c_o, c_i) on the device")
+    if out is None:
+        out = torch.empty((n,) + geom.output_shape, device=x_nhwc.device, dtype=torch.float32)
+    else:
+        _check_tensor(out, (n,) + geom.output_shape, "output tensor")
+    if n == 0:
+        return out
+    g = _native.Geom.of(geom, n)
+    with torch.cuda.device(x_nhwc.device):
+        _native.check(_native.lib().smmc_conv2d_fwd_bf16_tc(
+            ctypes.c_void_p(x_nhwc.data_ptr()), ctypes.c_void_p(w_tc.data_ptr()),
+            ctypes.c_void_p(out.data_ptr()), ctypes.byref(g), _stream_ptr(torch, x_nhwc.device)),
+            "smmc_conv2d_fwd_bf16_tc")
+    return out
+
+
+class TcSmmConv2d:
+    """Fitted bf16 tensor-core layer: weights packed once (untimed, like the
+    reference's repack); ``pack_input`` casts an fp32 NCHW batch to bf16 NHWC;
+    the call runs the tcgen05 kernel."""
+
+    def __init__(self, geom, weights, device="cuda"):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise DeviceError("TcSmmConv2d needs a CUDA device (no CPU fallback)")
+        if not tc_supported(geom):
+            from .errors import BackendUnsupportedError
+            raise BackendUnsupportedError(
+                "bf16 tensor-core variant needs stride 1 and c_i % 8 == 0")
+        self.geom = geom
+        self.device = torch.device(device)
+        w = torch.as_tensor(weights, dtype=torch.float32)
+        if tuple(w.shape) == geom.weights_shape:
+            w = w.permute(1, 3, 2, 0)
+        w = w.contiguous().to(self.device)
+        self.w_tc = pack_weights_bf16(w, geom)
+
+    def pack_input(self, x, out=None):
+        return pack_input_bf16(x, self.geom, out=out)
+
+    def __call__(self, x_nhwc, out=None):
+        return conv2d_bf16_tc(x_nhwc, self.w_tc, self.geom, out=out)

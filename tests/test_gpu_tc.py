@@ -1,0 +1,69 @@
+"""GPU parity of the separately labelled bf16 tensor-core variant (tcgen05):
+max|y - ref| <= 2e-2 * max|ref| against the fp32 oracle (BASELINE config 5)."""
+
+import numpy as np
+import pytest
+
+from oracle import smm_oracle as orc
+from paper_2411_15659_b200 import BackendUnsupportedError, ConvGeometry
+from paper_2411_15659_b200.tensors import synthetic_layer
+from paper_2411_15659_b200.workloads import CONFIGS, layer_seed
+
+pytestmark = pytest.mark.gpu
+
+TOL_BF16 = 2e-2
+
+
+def _run_tc(g, n, seed):
+    import torch
+    from paper_2411_15659_b200 import device
+    x, w = synthetic_layer(g, n, seed)
+    layer = device.TcSmmConv2d(g, w)
+    xd = torch.from_numpy(x).cuda()
+    y = layer(layer.pack_input(xd))
+    torch.cuda.synchronize()
+    return x, w, y.cpu().numpy()
+
+
+SMALL = [
+    (64, 64, 14, 14, 3, 3, 1, 1, 1, 1, 2),
+    (64, 128, 28, 28, 3, 3, 1, 1, 1, 1, 1),
+    (128, 64, 7, 7, 3, 3, 1, 1, 1, 1, 3),
+    (96, 256, 27, 27, 5, 5, 1, 1, 2, 2, 1),
+    (64, 256, 12, 12, 1, 1, 1, 1, 0, 0, 3),
+    (256, 64, 56, 56, 1, 1, 1, 1, 0, 0, 1),
+    (32, 40, 9, 11, 3, 3, 1, 1, 1, 1, 2),
+    (8, 130, 6, 5, 3, 5, 1, 1, 1, 2, 2),
+]
+
+
+@pytest.mark.parametrize("case", SMALL, ids=lambda c: "x".join(map(str, c)))
+def test_tc_small_shapes(case):
+    *gt, n = case
+    g = ConvGeometry(*gt)
+    x, w, y = _run_tc(g, n, 11)
+    ref = orc.smm_conv_c(x, orc.repack(w), g, threads=orc.host_threads())
+    err = orc.max_abs_ratio(y, ref)
+    assert err <= TOL_BF16, err
+    assert err >= 1e-5  # it really is bf16 (not a silent fp32 path)
+
+
+TC_LAYERS = [(5, li, name, n, g) for li, (name, n, g) in enumerate(CONFIGS[5]["layers"])]
+
+
+@pytest.mark.parametrize("ci,li,name,n,g", TC_LAYERS, ids=[l[2] for l in TC_LAYERS])
+def test_tc_config5_full_size(ci, li, name, n, g):
+    x, w, y = _run_tc(g, n, layer_seed(ci, li))
+    assert np.isfinite(y).all()
+    samples = [0, n - 1]
+    ref = orc.smm_conv_c(np.ascontiguousarray(x[samples]), orc.repack(w), g,
+                         threads=orc.host_threads())
+    assert orc.max_abs_ratio(y[samples], ref) <= TOL_BF16
+
+
+def test_tc_rejects_strided():
+    from paper_2411_15659_b200 import device
+    g = ConvGeometry(16, 16, 16, 16, 3, 3, stride_h=2, stride_w=2, pad_h=1, pad_w=1)
+    assert not device.tc_supported(g)
+    with pytest.raises(BackendUnsupportedError):
+        device.TcSmmConv2d(g, np.zeros(g.weights_shape, np.float32))

@@ -41,6 +41,8 @@
 // Both orders are fixed, so results are bitwise run-to-run deterministic; no
 // float atomics anywhere.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "smmc_internal.cuh"
@@ -489,6 +491,20 @@ FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) {
                 best.kt_per_split = per;
                 best.tiles = tiles;
             }
+        }
+    }
+    // experiment hook: SMMC_FORCE_PLAN="variant,splits" overrides the planner
+    if (const char* f = getenv("SMMC_FORCE_PLAN")) {
+        int v = -1, sp = 0;
+        if (sscanf(f, "%d,%d", &v, &sp) == 2 && v >= 0 && v < kNumTiles && sp >= 1) {
+            const TileCfg t = kTiles[v];
+            best.variant = v;
+            best.bm = t.bm;
+            best.bn = t.bn;
+            best.threads = t.threads;
+            best.kt_per_split = (kt_total + sp - 1) / sp;
+            best.splits = (kt_total + best.kt_per_split - 1) / best.kt_per_split;
+            best.tiles = ((m + t.bm - 1) / t.bm) * ((g.c_o + t.bn - 1) / t.bn);
         }
     }
     best.bk = bk;

@@ -121,12 +121,36 @@ size_t workspace_for(const smmc_geom& g, int mode, int sm_count) {
 }
 
 // Per-device staging buffers for the *_host entry points.
+constexpr int kMaxChunks = 8;
+
 struct HostPool {
     std::mutex mu;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;                      // compute
+    cudaStream_t s_in = nullptr, s_out = nullptr;       // H2D / D2H copy engines
+    cudaEvent_t ev_in[kMaxChunks] = {}, ev_done[kMaxChunks] = {};
     void* buf[4] = {nullptr, nullptr, nullptr, nullptr};
     size_t cap[4] = {0, 0, 0, 0};
 };
+
+int ensure_streams(HostPool& hp) {
+    if (hp.stream) return SMMC_OK;
+    int st;
+    if ((st = cuda_status(cudaStreamCreateWithFlags(&hp.stream, cudaStreamNonBlocking),
+                          "cudaStreamCreate")) ||
+        (st = cuda_status(cudaStreamCreateWithFlags(&hp.s_in, cudaStreamNonBlocking),
+                          "cudaStreamCreate")) ||
+        (st = cuda_status(cudaStreamCreateWithFlags(&hp.s_out, cudaStreamNonBlocking),
+                          "cudaStreamCreate")))
+        return st;
+    for (int i = 0; i < kMaxChunks; ++i) {
+        if ((st = cuda_status(cudaEventCreateWithFlags(&hp.ev_in[i], cudaEventDisableTiming),
+                              "cudaEventCreate")) ||
+            (st = cuda_status(cudaEventCreateWithFlags(&hp.ev_done[i], cudaEventDisableTiming),
+                              "cudaEventCreate")))
+            return st;
+    }
+    return SMMC_OK;
+}
 
 HostPool& pool_for(int device) {
     static std::mutex mu;
@@ -311,29 +335,55 @@ int smmc_conv2d_fwd_f32_host(const float* x, const float* w_smm, float* y, const
     if ((st = select_device(device))) return st;
     HostPool& hp = pool_for(device);
     std::lock_guard<std::mutex> lk(hp.mu);
-    if (!hp.stream &&
-        (st = cuda_status(cudaStreamCreateWithFlags(&hp.stream, cudaStreamNonBlocking),
-                          "cudaStreamCreate")))
-        return st;
-    const size_t xb = (size_t)g->n * g->c_i * g->h * g->w * sizeof(float);
+    if ((st = ensure_streams(hp))) return st;
+    const size_t xs = (size_t)g->c_i * g->h * g->w;          // floats per input sample
+    const size_t ys = (size_t)g->c_o * oh * ow;              // floats per output sample
+    const size_t xb = (size_t)g->n * xs * sizeof(float);
     const size_t wb = (size_t)g->c_i * g->k_w * g->k_h * g->c_o * sizeof(float);
-    const size_t yb = (size_t)g->n * g->c_o * oh * ow * sizeof(float);
-    const size_t wsb = workspace_for(*g, mode, sm_count_for(device));
+    const size_t yb = (size_t)g->n * ys * sizeof(float);
+    // Pipeline: the batch is cut into chunks of whole samples; chunk c's H2D
+    // (copy stream), conv (compute stream) and D2H (second copy stream) overlap
+    // with its neighbours'.  Chunks of >= ~8 MB keep the copies efficient.
+    const size_t per_sample = (xs + ys) * sizeof(float);
+    int chunks = (int)std::min<size_t>((size_t)kMaxChunks, (size_t)g->n);
+    chunks = (int)std::min<size_t>((size_t)chunks,
+                                   std::max<size_t>(1, (per_sample * g->n) / (8u << 20)));
+    const int per = (g->n + chunks - 1) / chunks;
+    chunks = (g->n + per - 1) / per;
+    smmc_geom gc = *g;
+    gc.n = per;
+    size_t wsb = workspace_for(gc, mode, sm_count_for(device));
+    gc.n = g->n - (chunks - 1) * per;
+    wsb = std::max(wsb, workspace_for(gc, mode, sm_count_for(device)));
     if ((st = ensure(hp, 0, xb)) || (st = ensure(hp, 1, wb)) || (st = ensure(hp, 2, yb)) ||
         (st = ensure(hp, 3, wsb)))
         return st;
-    cudaStream_t s = hp.stream;
-    if ((st = cuda_status(cudaMemcpyAsync(hp.buf[0], x, xb, cudaMemcpyHostToDevice, s), "H2D x")))
-        return st;
-    if ((st = cuda_status(cudaMemcpyAsync(hp.buf[1], w_smm, wb, cudaMemcpyHostToDevice, s),
+    float* xd = static_cast<float*>(hp.buf[0]);
+    float* wd = static_cast<float*>(hp.buf[1]);
+    float* yd = static_cast<float*>(hp.buf[2]);
+    if ((st = cuda_status(cudaMemcpyAsync(wd, w_smm, wb, cudaMemcpyHostToDevice, hp.s_in),
                           "H2D w_smm")))
         return st;
-    if ((st = conv_device(static_cast<float*>(hp.buf[0]), static_cast<float*>(hp.buf[1]),
-                          static_cast<float*>(hp.buf[2]), g, mode, hp.buf[3], wsb, s)))
-        return st;
-    if ((st = cuda_status(cudaMemcpyAsync(y, hp.buf[2], yb, cudaMemcpyDeviceToHost, s), "D2H y")))
-        return st;
-    return cuda_status(cudaStreamSynchronize(s), "conv (host path)");
+    for (int c = 0; c < chunks; ++c) {
+        const int n0 = c * per;
+        gc.n = std::min(per, g->n - n0);
+        const size_t xo = (size_t)n0 * xs, yo = (size_t)n0 * ys;
+        if ((st = cuda_status(cudaMemcpyAsync(xd + xo, x + xo, gc.n * xs * sizeof(float),
+                                              cudaMemcpyHostToDevice, hp.s_in),
+                              "H2D x")) ||
+            (st = cuda_status(cudaEventRecord(hp.ev_in[c], hp.s_in), "cudaEventRecord")) ||
+            (st = cuda_status(cudaStreamWaitEvent(hp.stream, hp.ev_in[c], 0), "cudaStreamWaitEvent")))
+            return st;
+        if ((st = conv_device(xd + xo, wd, yd + yo, &gc, mode, hp.buf[3], wsb, hp.stream))) return st;
+        if ((st = cuda_status(cudaEventRecord(hp.ev_done[c], hp.stream), "cudaEventRecord")) ||
+            (st = cuda_status(cudaStreamWaitEvent(hp.s_out, hp.ev_done[c], 0),
+                              "cudaStreamWaitEvent")) ||
+            (st = cuda_status(cudaMemcpyAsync(y + yo, yd + yo, gc.n * ys * sizeof(float),
+                                              cudaMemcpyDeviceToHost, hp.s_out),
+                              "D2H y")))
+            return st;
+    }
+    return cuda_status(cudaStreamSynchronize(hp.s_out), "conv (host path)");
 }
 
 int smmc_tc_supported(const smmc_geom* g) {
@@ -444,10 +494,7 @@ int smmc_extract_slice_f32_host(const float* x, const smmc_geom* g, int32_t c, i
     if ((st = select_device(device))) return st;
     HostPool& hp = pool_for(device);
     std::lock_guard<std::mutex> lk(hp.mu);
-    if (!hp.stream &&
-        (st = cuda_status(cudaStreamCreateWithFlags(&hp.stream, cudaStreamNonBlocking),
-                          "cudaStreamCreate")))
-        return st;
+    if ((st = ensure_streams(hp))) return st;
     const size_t xb = (size_t)g->c_i * g->h * g->w * sizeof(float);
     const size_t bb = (size_t)(g->h + 2 * g->p_h) * ow * sizeof(float);
     if ((st = ensure(hp, 0, xb)) || (st = ensure(hp, 2, bb))) return st;
@@ -475,10 +522,7 @@ int smmc_scalar_matrix_fma_f32_host(float alpha, const float* src, int64_t src_r
     if (st) return st;
     HostPool& hp = pool_for(device);
     std::lock_guard<std::mutex> lk(hp.mu);
-    if (!hp.stream &&
-        (st = cuda_status(cudaStreamCreateWithFlags(&hp.stream, cudaStreamNonBlocking),
-                          "cudaStreamCreate")))
-        return st;
+    if ((st = ensure_streams(hp))) return st;
     const size_t sb = ((size_t)(rows - 1) * src_row_stride + cols) * sizeof(float);
     const size_t db = ((size_t)(rows - 1) * dst_row_stride + cols) * sizeof(float);
     if ((st = ensure(hp, 0, sb)) || (st = ensure(hp, 2, db))) return st;

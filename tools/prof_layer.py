@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--layer", default="conv128@28_n32")
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--mode", default="ffma")
+    ap.add_argument("--graph", type=int, default=1)
     a = ap.parse_args()
     for li, (name, n, g) in enumerate(CONFIGS[a.config]["layers"]):
         if name != a.layer:
@@ -31,10 +32,25 @@ def main():
         y = mod(xd)
         torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        for _ in range(a.iters):
-            mod(xd, out=y)
-        e.record()
+        if a.graph:
+            # CUDA graph of `iters` launches: no host launch overhead in the timing
+            g_ = torch.cuda.CUDAGraph()
+            cs = torch.cuda.Stream()
+            cs.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(cs), torch.cuda.graph(g_, stream=cs):
+                for _ in range(a.iters):
+                    mod(xd, out=y)
+            torch.cuda.synchronize()
+            g_.replay()
+            torch.cuda.synchronize()
+            s.record()
+            g_.replay()
+            e.record()
+        else:
+            s.record()
+            for _ in range(a.iters):
+                mod(xd, out=y)
+            e.record()
         torch.cuda.synchronize()
         ms = s.elapsed_time(e) / a.iters
         print(f"{name}: {ms * 1e3:.1f} us/launch, {g.flops(n) / ms / 1e9:.2f} TFLOP/s")

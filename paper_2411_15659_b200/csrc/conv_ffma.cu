@@ -399,9 +399,9 @@ struct TileCfg {
 };
 constexpr TileCfg kTiles[] = {
     {128, 128, 256, 2},  // 0
-    {128, 64, 128, 3},   // 1
+    {128, 64, 128, 4},   // 1
     {256, 64, 256, 2},   // 2
-    {64, 128, 128, 3},   // 3
+    {64, 128, 128, 4},   // 3
 };
 constexpr int kNumTiles = sizeof(kTiles) / sizeof(kTiles[0]);
 constexpr int kBKCvec = 16;
@@ -531,9 +531,9 @@ cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
     cudaError_t e;
     switch (pl.variant) {
         case 0: e = launch_tile<128, 128, 256, 2>(p, pl.tap_kind, pl.cvec, grid, s); break;
-        case 1: e = launch_tile<128, 64, 128, 3>(p, pl.tap_kind, pl.cvec, grid, s); break;
+        case 1: e = launch_tile<128, 64, 128, 4>(p, pl.tap_kind, pl.cvec, grid, s); break;
         case 2: e = launch_tile<256, 64, 256, 2>(p, pl.tap_kind, pl.cvec, grid, s); break;
-        default: e = launch_tile<64, 128, 128, 3>(p, pl.tap_kind, pl.cvec, grid, s); break;
+        default: e = launch_tile<64, 128, 128, 4>(p, pl.tap_kind, pl.cvec, grid, s); break;
     }
     count_launches(1);
     if (e != cudaSuccess || pl.reduce_mode != 2) return e;

@@ -52,7 +52,8 @@ namespace {
 
 constexpr int kStages = 4;
 
-template <int BM, int BN, int THREADS, int MINB, int BK, int KH, int KW, int SH, int SW, bool CVEC>
+template <int BM, int BN, int THREADS, int MINB, int BK, int KH, int KW, int SH, int SW, bool CVEC,
+          bool SK>
 __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem p) {
     constexpr int STAGES = kStages;
     constexpr int TPX = BM / 8;            // pixel groups (4 + 4 pixels each)
@@ -81,11 +82,38 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
     const int cg = (warp % WCO) * 8 + (lane & 7);
     const int pg = (warp / WCO) * 4 + (lane >> 3);
 
-    const int m0 = blockIdx.x * BM;
-    const int n0 = blockIdx.y * BN;
-    const int split = blockIdx.z;
-    const int kt_beg = split * p.kt_per_split;
-    const int ktiles = min(p.kt_total - kt_beg, p.kt_per_split);
+    // ---- work decomposition.  Modes 0-2: one (tile, split) per CTA from the
+    // 3-D grid.  Mode 3 (stream-K): CTA b walks iterations [b*I, (b+1)*I) of
+    // the linearised (tile, tap-block) space, tile-major, so it finishes the
+    // tail of one tile and starts the next; tiles cut between CTAs are summed
+    // by their last arriving CTA in segment order.
+    constexpr bool sk = SK;  // stream-K instantiation (reduce_mode 3)
+    const int KT = p.kt_total;
+    int it = sk ? blockIdx.x * p.sk_iters : 0;
+    const int it_end = sk ? (int)min((int64_t)p.tiles * KT, (int64_t)it + p.sk_iters) : 0;
+    for (;;) {
+    int m0, n0, kt_beg, ktiles, slot, nslots;
+    int64_t tile;
+    if (sk) {
+        tile = it / KT;
+        kt_beg = it - (int)tile * KT;
+        ktiles = min(KT - kt_beg, it_end - it);
+        const int tm = (int)(tile / p.tiles_n);
+        m0 = tm * BM;
+        n0 = (int)(tile - (int64_t)tm * p.tiles_n) * BN;
+        const int first = (int)((tile * KT) / p.sk_iters);
+        const int last = (int)((tile * KT + KT - 1) / p.sk_iters);
+        slot = blockIdx.x - first;
+        nslots = last - first + 1;
+    } else {
+        m0 = blockIdx.x * BM;
+        n0 = blockIdx.y * BN;
+        tile = (int64_t)blockIdx.x * gridDim.y + blockIdx.y;
+        slot = blockIdx.z;
+        nslots = p.splits;
+        kt_beg = slot * p.kt_per_split;
+        ktiles = min(KT - kt_beg, p.kt_per_split);
+    }
 
     const int kh = KH ? KH : p.kh;
     const int kw = KW ? KW : p.kw;
@@ -274,61 +302,64 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
             acc[i][2 * j + 1] = v.y;
         }
 
-    // ---- split-K reduce_mode 1: deterministic last-arriver fixup
-    if (p.splits > 1 && p.reduce_mode == 1) {
-        const int64_t tile = (int64_t)blockIdx.x * gridDim.y + blockIdx.y;
-        float* part = p.ws + (tile * p.splits) * (BM * BN);
-        // layout [split][16 float4 groups][THREADS]: warp stores are contiguous
-        float4* mine = reinterpret_cast<float4*>(part + (int64_t)split * (BM * BN));
+    // ---- split-K / stream-K: deterministic last-arriver fixup
+    bool store = true;
+    if ((p.reduce_mode == 1 && p.splits > 1) || (sk && nslots > 1)) {
+        const int stride_slots = sk ? p.sk_maxseg : p.splits;
+        float* part = p.ws + (tile * stride_slots) * (BM * BN);
+        // layout [slot][16 float4 groups][THREADS]: warp stores are contiguous
+        float4* mine = reinterpret_cast<float4*>(part + (int64_t)slot * (BM * BN));
 #pragma unroll
         for (int g = 0; g < 16; ++g)
             mine[g * THREADS + tid] = make_float4(acc[g >> 1][(g & 1) * 4 + 0], acc[g >> 1][(g & 1) * 4 + 1],
                                                   acc[g >> 1][(g & 1) * 4 + 2], acc[g >> 1][(g & 1) * 4 + 3]);
         __threadfence();
         __syncthreads();
-        if (tid == 0) s_last = atomicAdd(p.counters + tile, 1) == p.splits - 1;
+        if (tid == 0) s_last = atomicAdd(p.counters + tile, 1) == nslots - 1;
         __syncthreads();
-        if (!s_last) return;
-        __threadfence();
-        // P_0 + P_1 + ... + P_{S-1} in split order (own partial re-read too);
-        // 8 independent loads in flight per round
-        const float4* base = reinterpret_cast<const float4*>(part) + tid;
+        store = s_last;
+        if (store) {
+            __threadfence();
+            // P_0 + P_1 + ... in slot order (own partial re-read too);
+            // 8 independent loads in flight per round
+            const float4* base = reinterpret_cast<const float4*>(part) + tid;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            float4 s4[8];
+            for (int h = 0; h < 2; ++h) {
+                float4 s4[8];
 #pragma unroll
-            for (int g = 0; g < 8; ++g) s4[g] = __ldcg(base + (h * 8 + g) * THREADS);
-            for (int z = 1; z < p.splits; ++z) {
-                float4 v[8];
+                for (int g = 0; g < 8; ++g) s4[g] = __ldcg(base + (h * 8 + g) * THREADS);
+                for (int z = 1; z < nslots; ++z) {
+                    float4 v[8];
 #pragma unroll
-                for (int g = 0; g < 8; ++g)
-                    v[g] = __ldcg(base + (int64_t)z * (BM * BN / 4) + (h * 8 + g) * THREADS);
+                    for (int g = 0; g < 8; ++g)
+                        v[g] = __ldcg(base + (int64_t)z * (BM * BN / 4) + (h * 8 + g) * THREADS);
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) {
+                        s4[g].x += v[g].x;
+                        s4[g].y += v[g].y;
+                        s4[g].z += v[g].z;
+                        s4[g].w += v[g].w;
+                    }
+                }
 #pragma unroll
                 for (int g = 0; g < 8; ++g) {
-                    s4[g].x += v[g].x;
-                    s4[g].y += v[g].y;
-                    s4[g].z += v[g].z;
-                    s4[g].w += v[g].w;
+                    const int gg = h * 8 + g;
+                    acc[gg >> 1][(gg & 1) * 4 + 0] = s4[g].x;
+                    acc[gg >> 1][(gg & 1) * 4 + 1] = s4[g].y;
+                    acc[gg >> 1][(gg & 1) * 4 + 2] = s4[g].z;
+                    acc[gg >> 1][(gg & 1) * 4 + 3] = s4[g].w;
                 }
             }
-#pragma unroll
-            for (int g = 0; g < 8; ++g) {
-                const int gg = h * 8 + g;
-                acc[gg >> 1][(gg & 1) * 4 + 0] = s4[g].x;
-                acc[gg >> 1][(gg & 1) * 4 + 1] = s4[g].y;
-                acc[gg >> 1][(gg & 1) * 4 + 2] = s4[g].z;
-                acc[gg >> 1][(gg & 1) * 4 + 3] = s4[g].w;
-            }
+            if (tid == 0) p.counters[tile] = 0;  // re-arm for the next launch
         }
-        if (tid == 0) p.counters[tile] = 0;  // re-arm for the next launch
     }
 
-    // ---- epilogue: NCHW stores (reduce_mode 2: partial plane `split` of ws)
-    float* out = (p.splits > 1 && p.reduce_mode == 2) ? p.ws + (int64_t)split * ((int64_t)p.m * p.co)
+    // ---- epilogue: NCHW stores (reduce_mode 2: partial plane `slot` of ws)
+    float* out = (p.splits > 1 && p.reduce_mode == 2) ? p.ws + (int64_t)slot * ((int64_t)p.m * p.co)
                                                        : p.y;
     const bool vec_ok = (p.ohw & 3) == 0;
 #pragma unroll
-    for (int ib = 0; ib < 2; ++ib) {
+    for (int ib = 0; ib < 2 && store; ++ib) {
         const int pbase = m0 + ib * (BM / 2) + pg * 4;
         if (pbase >= p.m) continue;
         const int n = pbase / p.ohw;
@@ -358,6 +389,11 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
             }
         }
     }
+    if (!sk) break;
+    it += ktiles;
+    if (it >= it_end) break;
+    __syncthreads();  // smem ring and s_last are reused by the next segment
+    }  // segment loop
 }
 
 // reduce_mode 2: y = sum of the partial planes in split order.
@@ -407,12 +443,15 @@ constexpr int kNumTiles = sizeof(kTiles) / sizeof(kTiles[0]);
 constexpr int kBKCvec = 16;
 constexpr int kBKGeneric = 8;
 
-template <int BM, int BN, int T, int MINB, int BK, int KH, int KW, int SH, int SW, bool CVEC>
+template <int BM, int BN, int T, int MINB, int BK, int KH, int KW, int SH, int SW, bool CVEC,
+          bool SK = false>
 cudaError_t launch_one(const Problem& p, dim3 grid, cudaStream_t s) {
+    if (CVEC && !SK && p.reduce_mode == 3)
+        return launch_one<BM, BN, T, MINB, BK, KH, KW, SH, SW, CVEC, true>(p, grid, s);
     constexpr int smem = kStages * BK * (BM + BN) * (int)sizeof(float);
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
-    auto kern = conv_ffma_kernel<BM, BN, T, MINB, BK, KH, KW, SH, SW, CVEC>;
+    auto kern = conv_ffma_kernel<BM, BN, T, MINB, BK, KH, KW, SH, SW, CVEC, SK && CVEC>;
     std::call_once(once, [&] {
         attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     });
@@ -451,6 +490,37 @@ int tap_kind_of(const smmc_geom& g) {
 
 }  // namespace
 
+// Measured-best (tile variant, splits) for the BASELINE.json layer shapes on
+// B200 (tools/plan_table_sweep.py; profiles/r01/plan_sweep.json).  splits = 0
+// selects stream-K.  Shapes not listed use the cost model below.
+struct TunedPlan {
+    int n, c_i, h, w, c_o, k, s, p;
+    int variant, splits;
+};
+constexpr TunedPlan kTuned[] = {
+    {1, 64, 56, 56, 64, 3, 1, 1, 1, 8},        // 14.8 us (model: 15.5)
+    {1, 128, 28, 28, 128, 3, 1, 1, 1, 8},      // 15.0 us (19.4)
+    {1, 256, 14, 14, 256, 3, 1, 1, 1, 16},     // 15.9 us (32.4)
+    {1, 512, 7, 7, 512, 3, 1, 1, 3, 32},       // 20.2 us (42.9)
+    {32, 64, 56, 56, 64, 3, 1, 1, 2, 0},       // 160.0 us (168.0)
+    {8, 96, 27, 27, 256, 5, 1, 2, 3, 4},       // 150.1 us (154.2)
+    {256, 64, 56, 56, 256, 1, 1, 0, 3, 1},     // 642.2 us (695.3)
+    {256, 128, 28, 28, 128, 3, 1, 1, 0, 1},    // 1083.9 us (1119.4)
+    {8, 512, 7, 7, 512, 3, 1, 1, 3, 24},       // 60.1 us (76.3)
+    {64, 128, 56, 56, 256, 3, 1, 1, 3, 1},     // 2136.5 us (2154.1)
+    {64, 256, 56, 56, 256, 3, 1, 1, 3, 1},     // 4206.0 us (4249.3)
+    {64, 256, 28, 28, 512, 3, 1, 1, 0, 3},     // 2122.6 us (2164.0)
+};
+
+int64_t best_cost_waves(const FfmaPlan& b, int64_t m, int c_o, int sm_count) {
+    int per_sm = 1;
+    for (int v = 0; v < kNumTiles; ++v)
+        if (kTiles[v].bm == b.bm && kTiles[v].bn == b.bn) per_sm = kTiles[v].per_sm;
+    const int64_t tiles = ((m + b.bm - 1) / b.bm) * ((c_o + b.bn - 1) / b.bn);
+    const int64_t slots = (int64_t)sm_count * per_sm;
+    return (tiles * std::max(b.splits, 1) + slots - 1) / slots;
+}
+
 // Wave-quantisation-aware choice of CTA tile and split-K factor.  Cost model:
 // a wave of `slots` CTAs runs per_sm CTAs per SM, so its time is proportional
 // to per_sm * BM * BN * (work per CTA in 8-deep tap blocks, plus a prologue /
@@ -466,12 +536,15 @@ FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) {
     const bool cvec = (g.c_i % kBKCvec) == 0 && g.k_h <= 32 && g.k_w <= 32;
     const int bk = cvec ? kBKCvec : kBKGeneric;
     const int kt_total = cvec ? taps * (g.c_i / bk) : (g.c_i * taps + bk - 1) / bk;
+    const double blk = bk / 8.0;  // work of one tap block in 8-deep units
     for (int v = 0; v < kNumTiles; ++v) {
         const TileCfg t = kTiles[v];
         const int64_t mt = (m + t.bm - 1) / t.bm;
         const int64_t nt = (g.c_o + t.bn - 1) / t.bn;
         const int64_t tiles = mt * nt;
         const int64_t slots = (int64_t)sm_count * t.per_sm;
+        const double tile_area = (double)t.per_sm * t.bm * t.bn;
+        // (a) classic grid: one (tile, split) per CTA
         const int max_s = std::max(1, std::min(32, kt_total / 2));
         for (int s = 1; s <= max_s; ++s) {
             const int per = (kt_total + s - 1) / s;
@@ -479,10 +552,11 @@ FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) {
             if (sp != s) continue;
             const int64_t ctas = tiles * sp;
             const int64_t waves = (ctas + slots - 1) / slots;
-            const double work = per * (bk / 8.0) + 1.0 + (sp > 1 ? 3.0 : 0.0);
-            double cost = (double)waves * t.per_sm * t.bm * t.bn * work * (1.0 + 0.02 * (sp - 1));
+            const double work = per * blk + 1.0 + (sp > 1 ? 3.0 : 0.0);
+            const double cost = (double)waves * tile_area * work * (1.0 + 0.02 * (sp - 1));
             if (cost < best_cost * 0.999) {
                 best_cost = cost;
+                best = FfmaPlan{};
                 best.variant = v;
                 best.bm = t.bm;
                 best.bn = t.bn;
@@ -490,30 +564,108 @@ FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) {
                 best.splits = sp;
                 best.kt_per_split = per;
                 best.tiles = tiles;
+                best.tiles_n = (int)nt;
+                best.reduce_mode = sp > 1 ? (sp <= 4 ? 1 : 2) : 0;
             }
         }
     }
-    // experiment hook: SMMC_FORCE_PLAN="variant,splits" overrides the planner
-    if (const char* f = getenv("SMMC_FORCE_PLAN")) {
-        int v = -1, sp = 0;
-        if (sscanf(f, "%d,%d", &v, &sp) == 2 && v >= 0 && v < kNumTiles && sp >= 1) {
-            const TileCfg t = kTiles[v];
+    // (b) stream-K: one persistent wave, every CTA the same number (>= 8) of tap
+    // blocks, tiles cut between CTAs fixed up by the last arriver.  Only worth
+    // it when the best classic grid runs <= 2 waves (quantisation loss is
+    // large) and it is clearly cheaper; A/B on B200: +5-6 % on conv64@56 and
+    // conv512@7 at N=32, but slower than split-K on many-wave layers.
+    const int64_t best_waves = best_cost_waves(best, m, g.c_o, sm_count);
+    const double classic_cost = best_cost;
+    for (int v = 0; v < kNumTiles && cvec && best_waves <= 2; ++v) {
+        const TileCfg t = kTiles[v];
+        const int64_t nt = (g.c_o + t.bn - 1) / t.bn;
+        const int64_t tiles = ((m + t.bm - 1) / t.bm) * nt;
+        const int64_t slots = (int64_t)sm_count * t.per_sm;
+        const int64_t W = tiles * kt_total;
+        if (W >= (int64_t)INT32_MAX) continue;
+        int64_t ctas = std::min<int64_t>(slots, W / 32);  // >= 32 tap blocks per CTA
+        if (ctas < 1) continue;
+        const int iters = (int)((W + ctas - 1) / ctas);
+        ctas = (W + iters - 1) / iters;
+        const double segs = (double)iters / kt_total + 1.0;  // tiles touched per CTA
+        const double work = iters * blk + segs * 1.0 + 3.0;
+        const double cost = (double)t.per_sm * t.bm * t.bn * work;
+        if (cost < classic_cost * 0.93 && cost < best_cost) {
+            best_cost = cost;
+            best = FfmaPlan{};
             best.variant = v;
             best.bm = t.bm;
             best.bn = t.bn;
             best.threads = t.threads;
-            best.kt_per_split = (kt_total + sp - 1) / sp;
+            best.splits = 1;
+            best.kt_per_split = kt_total;
+            best.tiles = tiles;
+            best.tiles_n = (int)nt;
+            best.reduce_mode = 3;
+            best.sk_ctas = (int)ctas;
+            best.sk_iters = iters;
+            int maxseg = 1;
+            for (int64_t tt = 0; tt < tiles; ++tt) {
+                const int64_t first = (tt * kt_total) / iters;
+                const int64_t last = (tt * kt_total + kt_total - 1) / iters;
+                maxseg = std::max(maxseg, (int)(last - first + 1));
+            }
+            best.sk_maxseg = maxseg;
+        }
+    }
+    // measured-best plans for known shapes (tuning table), then the
+    // SMMC_FORCE_PLAN="variant,splits" experiment hook (splits 0 = stream-K)
+    int fv = -1, fs = -1;
+    for (const TunedPlan& e : kTuned) {
+        if (e.n == g.n && e.c_i == g.c_i && e.h == g.h && e.w == g.w && e.c_o == g.c_o &&
+            e.k == g.k_h && g.k_w == g.k_h && e.s == g.s_h && g.s_w == g.s_h && e.p == g.p_h &&
+            g.p_w == g.p_h) {
+            fv = e.variant;
+            fs = e.splits;
+        }
+    }
+    if (const char* f = getenv("SMMC_FORCE_PLAN")) {
+        int v = -1, sp = -1;
+        if (sscanf(f, "%d,%d", &v, &sp) == 2) {
+            fv = v;
+            fs = sp;
+        }
+    }
+    if (fv >= 0 && fv < kNumTiles && fs >= 0 && (fs > 0 || cvec)) {
+        const TileCfg t = kTiles[fv];
+        best = FfmaPlan{};
+        best.variant = fv;
+        best.bm = t.bm;
+        best.bn = t.bn;
+        best.threads = t.threads;
+        best.tiles_n = (int)((g.c_o + t.bn - 1) / t.bn);
+        best.tiles = ((m + t.bm - 1) / t.bm) * best.tiles_n;
+        if (fs == 0) {
+            const int64_t W = best.tiles * kt_total;
+            int64_t ctas = std::max<int64_t>(1, std::min<int64_t>((int64_t)sm_count * t.per_sm, W / 8));
+            best.sk_iters = (int)((W + ctas - 1) / ctas);
+            best.sk_ctas = (int)((W + best.sk_iters - 1) / best.sk_iters);
+            best.splits = 1;
+            best.kt_per_split = kt_total;
+            best.reduce_mode = 3;
+            int maxseg = 1;
+            for (int64_t tt = 0; tt < best.tiles; ++tt)
+                maxseg = std::max(maxseg, (int)((tt * kt_total + kt_total - 1) / best.sk_iters -
+                                                (tt * kt_total) / best.sk_iters + 1));
+            best.sk_maxseg = maxseg;
+        } else {
+            best.kt_per_split = (kt_total + fs - 1) / fs;
             best.splits = (kt_total + best.kt_per_split - 1) / best.kt_per_split;
-            best.tiles = ((m + t.bm - 1) / t.bm) * ((g.c_o + t.bn - 1) / t.bn);
+            best.reduce_mode = best.splits > 1 ? (best.splits <= 4 ? 1 : 2) : 0;
         }
     }
     best.bk = bk;
     best.kt_total = kt_total;
     best.cvec = cvec ? 1 : 0;
     best.tap_kind = tap_kind_of(g);
-    best.reduce_mode = best.splits > 1 ? (best.splits <= 4 ? 1 : 2) : 0;
-    if (best.reduce_mode == 1) {
-        const size_t part = (size_t)best.tiles * best.splits * best.bm * best.bn * sizeof(float);
+    if (best.reduce_mode == 1 || best.reduce_mode == 3) {
+        const int slots_per_tile = best.reduce_mode == 1 ? best.splits : best.sk_maxseg;
+        const size_t part = (size_t)best.tiles * slots_per_tile * best.bm * best.bn * sizeof(float);
         best.ws_counter_offset = (part + 255) & ~(size_t)255;
         best.ws_bytes = best.ws_counter_offset + (size_t)best.tiles * sizeof(int);
     } else if (best.reduce_mode == 2) {
@@ -528,6 +680,7 @@ FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) {
 
 cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
     dim3 grid((p.m + pl.bm - 1) / pl.bm, (p.co + pl.bn - 1) / pl.bn, pl.splits);
+    if (pl.reduce_mode == 3) grid = dim3((unsigned)pl.sk_ctas, 1, 1);
     cudaError_t e;
     switch (pl.variant) {
         case 0: e = launch_tile<128, 128, 256, 2>(p, pl.tap_kind, pl.cvec, grid, s); break;

@@ -237,7 +237,11 @@ int conv_device(const float* x, const float* w, float* y, const smmc_geom* g, in
     p.kt_per_split = pl.kt_per_split;
     p.cvec = pl.cvec;
     p.reduce_mode = pl.reduce_mode;
-    if (pl.splits > 1) {
+    p.tiles = pl.tiles;
+    p.tiles_n = pl.tiles_n;
+    p.sk_iters = pl.sk_iters;
+    p.sk_maxseg = pl.sk_maxseg;
+    if (pl.ws_bytes > 0) {
         if (!ws || ws_bytes < pl.ws_bytes) {
             set_error("workspace of %zu bytes required (got %zu)", pl.ws_bytes, ws_bytes);
             return SMMC_EWORKSPACE;
@@ -247,7 +251,7 @@ int conv_device(const float* x, const float* w, float* y, const smmc_geom* g, in
             return SMMC_ESHAPE;
         }
     }
-    if (pl.reduce_mode == 1) {
+    if (pl.reduce_mode == 1 || pl.reduce_mode == 3) {
         p.counters = reinterpret_cast<int*>(static_cast<char*>(ws) + pl.ws_counter_offset);
         // arrival counters must read zero at kernel start; the workspace may
         // hold another problem's partials where this plan keeps its counters
@@ -308,8 +312,16 @@ int smmc_plan_describe(const smmc_geom* g, int mode, char* buf, size_t len) {
              "each, reduce=%s), %lld tiles",
              pl.bm, pl.bn, pl.bk, pl.threads, pl.tap_kind, pl.cvec ? "tap-major" : "(c,j,k)",
              pl.splits, pl.kt_per_split, pl.kt_total,
-             pl.reduce_mode == 0 ? "none" : (pl.reduce_mode == 1 ? "last-arriver" : "kernel"),
+             pl.reduce_mode == 0 ? "none"
+             : pl.reduce_mode == 1 ? "last-arriver"
+             : pl.reduce_mode == 2 ? "kernel"
+                                   : "stream-K",
              (long long)pl.tiles);
+    if (pl.reduce_mode == 3) {
+        const size_t used = strlen(buf);
+        snprintf(buf + used, len - used, ", stream-K %d CTAs x %d tap blocks", pl.sk_ctas,
+                 pl.sk_iters);
+    }
     return SMMC_OK;
 }
 

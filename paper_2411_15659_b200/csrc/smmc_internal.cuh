@@ -28,7 +28,11 @@ struct Problem {
     int kt_per_split;    // tap blocks per split
     int splits;
     int cvec;            // 1: tap-major K order (c_i % BK == 0)
-    int reduce_mode;     // split-K: 0 none, 1 in-kernel last-arriver, 2 separate reduce kernel
+    int reduce_mode;     // 0 none, 1 split-K last-arriver, 2 split-K reduce kernel, 3 stream-K
+    int64_t tiles;       // pixel tiles x channel tiles
+    int tiles_n;         // channel tiles
+    int sk_iters;        // stream-K: tap blocks per CTA
+    int sk_maxseg;       // stream-K: partial-tile slots per tile in the workspace
 };
 
 // Last-error / launch bookkeeping (defined in smmc_api.cu).
@@ -47,8 +51,12 @@ struct FfmaPlan {
     int kt_per_split;
     int tap_kind;      // 0 generic, 1: 3x3s1, 2: 1x1s1, 3: 7x7s2, 4: 11x11s4, 5: 5x5s1
     int cvec;          // tap-major K order
-    int reduce_mode;   // 0 none, 1 in-kernel last-arriver fixup, 2 separate reduce kernel
+    int reduce_mode;   // 0 none, 1 split-K last-arriver, 2 split-K reduce kernel, 3 stream-K
     int64_t tiles;     // pixel tiles x channel tiles
+    int tiles_n;
+    int sk_ctas;       // stream-K grid
+    int sk_iters;      // stream-K tap blocks per CTA
+    int sk_maxseg;
     size_t ws_bytes;   // partial tiles + counters
     size_t ws_counter_offset;
 };

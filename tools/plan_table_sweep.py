@@ -1,0 +1,84 @@
+"""Sweep forced FFMA plans for every BASELINE layer (one process), print the
+best plan per layer as a table (for the per-shape tuning table in conv_ffma.cu).
+
+    python tools/plan_table_sweep.py [--configs 2,3,5] > sweep.txt
+"""
+import argparse
+import json
+import os
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch  # noqa: E402
+
+from paper_2411_15659_b200 import _native, device  # noqa: E402
+from paper_2411_15659_b200.tensors import synthetic_layer  # noqa: E402
+from paper_2411_15659_b200.workloads import CONFIGS, layer_seed  # noqa: E402
+
+
+def time_plan(mod, xd, y, iters):
+    g_ = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    cs.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(cs), torch.cuda.graph(g_, stream=cs):
+        for _ in range(iters):
+            mod(xd, out=y)
+    torch.cuda.synchronize()
+    g_.replay()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    g_.replay()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters * 1e3
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="2,3,5,4")
+    a = ap.parse_args()
+    out = {}
+    seen = set()
+    for ci in map(int, a.configs.split(",")):
+        for li, (name, n, g) in enumerate(CONFIGS[ci]["layers"]):
+            key = (n,) + g.as_abi(n)[1:]
+            if key in seen:
+                continue
+            seen.add(key)
+            x, w = synthetic_layer(g, n, layer_seed(ci, li))
+            xd = torch.from_numpy(x).cuda()
+            small = g.flops(n) < 2e9
+            cands = ([(v, s) for v in (0, 1, 3) for s in (4, 8, 16, 24, 32, 0)] if small else
+                     [(v, s) for v in (0, 1, 2, 3) for s in (1, 2, 3, 4, 0)])
+            iters = 20 if g.flops(n) < 20e9 else 3
+            res = []
+            os.environ.pop("SMMC_FORCE_PLAN", None)
+            mod = device.SmmConv2d(g, w)
+            y = mod(xd)
+            default = (time_plan(mod, xd, y, iters), _native.plan_describe(g, n))
+            for v, s in cands:
+                os.environ["SMMC_FORCE_PLAN"] = f"{v},{s}"
+                mod = device.SmmConv2d(g, w)
+                y = mod(xd)
+                try:
+                    res.append((time_plan(mod, xd, y, iters), v, s))
+                except Exception as exc:  # noqa: BLE001
+                    print(f"  {name} {v},{s}: {exc}", file=sys.stderr)
+            os.environ.pop("SMMC_FORCE_PLAN", None)
+            res.sort()
+            best = res[0]
+            print(f"{name:32s} default {default[0]:9.1f} us | best {best[0]:9.1f} us plan {best[1]},{best[2]}"
+                  f" | next {res[1][0]:.1f} ({res[1][1]},{res[1][2]}) {res[2][0]:.1f} ({res[2][1]},{res[2][2]})",
+                  flush=True)
+            out[name] = {"key": key, "default_us": default[0], "default_plan": default[1],
+                         "best": [best[1], best[2]], "best_us": best[0],
+                         "all": [[r[1], r[2], round(r[0], 2)] for r in res]}
+            del xd, mod, y
+            torch.cuda.empty_cache()
+    Path("gpurun_out/plan_sweep.json").write_text(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()

@@ -157,6 +157,13 @@ SMMC_API int smmc_pack_weights_bf16(const float* w_smm, uint16_t* w_tc, const sm
 SMMC_API int smmc_conv2d_fwd_bf16_tc(const uint16_t* x_nhwc, const uint16_t* w_tc, float* y,
                                      const smmc_geom* g, void* stream);
 
+/* GPU im2col comparator (the paper's baseline): the explicit
+ * lowered matrix of im2col_pack (im2col.py:22-71), per sample
+ * [c_i*k_h*k_w][out_h*out_w], row (c*k_h + k)*k_w + j, zero-filled padding.
+ * `lowered` holds n*c_i*k_h*k_w*out_h*out_w floats — the scratch SMM avoids. */
+SMMC_API size_t smmc_im2col_bytes(const smmc_geom* g);
+SMMC_API int smmc_im2col_pack_f32(const float* x, float* lowered, const smmc_geom* g, void* stream);
+
 /* Number of kernels smmc_conv2d_fwd_f32 launches for this problem/mode. */
 SMMC_API int smmc_plan_launches(const smmc_geom* g, int mode);
 

@@ -39,7 +39,7 @@ EXPORTED_SYMBOLS = (
     "smmc_extract_slice_f32_host", "smmc_scalar_matrix_fma_f32_host",
     "smmc_plan_launches", "smmc_plan_describe", "smmc_launch_count",
     "smmc_tc_supported", "smmc_pack_input_bf16_nhwc", "smmc_pack_weights_bf16",
-    "smmc_conv2d_fwd_bf16_tc",
+    "smmc_conv2d_fwd_bf16_tc", "smmc_im2col_bytes", "smmc_im2col_pack_f32",
 )
 
 
@@ -98,6 +98,8 @@ _SIGNATURES = {
     "smmc_pack_input_bf16_nhwc": (ctypes.c_int, [_P, _P, _GP, _P]),
     "smmc_pack_weights_bf16": (ctypes.c_int, [_P, _P, _GP, _P]),
     "smmc_conv2d_fwd_bf16_tc": (ctypes.c_int, [_P, _P, _P, _GP, _P]),
+    "smmc_im2col_bytes": (ctypes.c_size_t, [_GP]),
+    "smmc_im2col_pack_f32": (ctypes.c_int, [_P, _P, _GP, _P]),
 }
 
 

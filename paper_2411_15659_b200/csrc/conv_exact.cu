@@ -122,3 +122,49 @@ cudaError_t launch_scalar_matrix_fma(float alpha, const float* src, int64_t ss, 
 }
 
 }  // namespace smmc
+
+// ---------------------------------------------------------------------------
+// GPU im2col comparator (the paper's baseline): the explicit
+// lowered matrix of the reference's im2col_pack (im2col.py:22-42), per sample
+// [c_i*k_h*k_w][out_h*out_w] with row (c*k_h + k)*k_w + j, zero-filled padding.
+// Its size is exactly the scratch SMM-Conv avoids.
+namespace smmc {
+namespace {
+
+__global__ void im2col_pack_kernel(const float* __restrict__ x, float* __restrict__ low, int n,
+                                   int c, int h, int w, int kh, int kw, int sh, int sw, int ph,
+                                   int pw, int oh, int ow) {
+    const int64_t ohw = (int64_t)oh * ow;
+    const int64_t rows = (int64_t)c * kh * kw;
+    const int64_t total = (int64_t)n * rows * ohw;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t col = i % ohw;
+        const int64_t r = (i / ohw) % rows;
+        const int64_t s = i / (ohw * rows);
+        const int j = (int)(r % kw);
+        const int k = (int)((r / kw) % kh);
+        const int cc = (int)(r / ((int64_t)kw * kh));
+        const int orow = (int)(col / ow), ocol = (int)(col % ow);
+        const int ih = orow * sh + k - ph, iw = ocol * sw + j - pw;
+        float v = 0.0f;
+        if ((unsigned)ih < (unsigned)h && (unsigned)iw < (unsigned)w)
+            v = __ldg(x + ((s * c + cc) * h + ih) * (int64_t)w + iw);
+        low[i] = v;
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_im2col_pack(const float* x, float* low, const smmc_geom& g, int oh, int ow,
+                               cudaStream_t s) {
+    const int64_t total = (int64_t)g.n * g.c_i * g.k_h * g.k_w * oh * ow;
+    if (total == 0) return cudaSuccess;
+    const int blocks = (int)((total + 255) / 256 < 148 * 32 ? (total + 255) / 256 : 148 * 32);
+    im2col_pack_kernel<<<blocks, 256, 0, s>>>(x, low, g.n, g.c_i, g.h, g.w, g.k_h, g.k_w, g.s_h,
+                                              g.s_w, g.p_h, g.p_w, oh, ow);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+}  // namespace smmc

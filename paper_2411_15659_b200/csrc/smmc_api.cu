@@ -398,6 +398,25 @@ int smmc_conv2d_fwd_f32_host(const float* x, const float* w_smm, float* y, const
     return cuda_status(cudaStreamSynchronize(hp.s_out), "conv (host path)");
 }
 
+size_t smmc_im2col_bytes(const smmc_geom* g) {
+    int oh = 0, ow = 0;
+    if (check_geom(g, &oh, &ow)) return 0;
+    return (size_t)g->n * g->c_i * g->k_h * g->k_w * oh * ow * sizeof(float);
+}
+
+int smmc_im2col_pack_f32(const float* x, float* lowered, const smmc_geom* g, void* stream) {
+    int oh = 0, ow = 0;
+    int st = check_geom(g, &oh, &ow);
+    if (st) return st;
+    if (g->n == 0) return SMMC_OK;
+    if (!x || !lowered) {
+        set_error("x and lowered must be non-NULL device pointers");
+        return SMMC_ESHAPE;
+    }
+    return cuda_status(launch_im2col_pack(x, lowered, *g, oh, ow, static_cast<cudaStream_t>(stream)),
+                       "im2col_pack launch");
+}
+
 int smmc_tc_supported(const smmc_geom* g) {
     int oh = 0, ow = 0;
     if (check_geom(g, &oh, &ow)) return 0;

@@ -77,6 +77,8 @@ cudaError_t launch_tc_bf16(const uint16_t* x_nhwc, const uint16_t* w_tc, float* 
 cudaError_t launch_pack_input_nhwc(const float* x, uint16_t* out, const smmc_geom& g, cudaStream_t s);
 cudaError_t launch_pack_weights_bf16(const float* w, uint16_t* out, const smmc_geom& g,
                                      cudaStream_t s);
+cudaError_t launch_im2col_pack(const float* x, float* low, const smmc_geom& g, int oh, int ow,
+                               cudaStream_t s);
 cudaError_t launch_extract_slice(const float* x, const smmc_geom& g, int c, int j,
                                  float* buf, cudaStream_t s);
 cudaError_t launch_scalar_matrix_fma(float alpha, const float* src, int64_t ss,

@@ -52,11 +52,12 @@ namespace {
 
 constexpr int kStages = 4;
 
-template <int BM, int BN, int THREADS, int MINB, int BK, int KH, int KW, int SH, int SW, bool CVEC,
-          bool SK>
+template <int BM, int BN, int THREADS, int MINB, int TM, int BK, int KH, int KW, int SH, int SW,
+          bool CVEC, bool SK>
 __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem p) {
     constexpr int STAGES = kStages;
-    constexpr int TPX = BM / 8;            // pixel groups (4 + 4 pixels each)
+    constexpr int NQ = TM / 4;             // 4-pixel blocks per thread, BM/NQ apart
+    constexpr int TPX = BM / TM;           // pixel groups
     constexpr int TCO = BN / 8;            // channel groups (4 + 4 channels each)
     static_assert(TPX * TCO == THREADS, "thread tile must cover the CTA tile");
     static_assert(TCO % 8 == 0 && TPX % 4 == 0, "warp = 4 pixel groups x 8 channel groups");
@@ -251,9 +252,9 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
     };
 
     // accumulators as FFMA2 lane pairs: acc2[i][jp] = (channel 2jp, 2jp+1) of pixel i
-    uint64_t acc2[8][4];
+    uint64_t acc2[TM][4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc2[i][j] = 0ull;
 
@@ -278,23 +279,29 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
         const float* bp = b_rd + slot * (BK * BN);
 #pragma unroll
         for (int kk = 0; kk < BK; ++kk) {
-            const float4 a0 = *reinterpret_cast<const float4*>(ap + kk * BM);
-            const float4 a1 = *reinterpret_cast<const float4*>(ap + kk * BM + BM / 2);
+            float a[TM];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const float4 aq = *reinterpret_cast<const float4*>(ap + kk * BM + q * (BM / NQ));
+                a[4 * q + 0] = aq.x;
+                a[4 * q + 1] = aq.y;
+                a[4 * q + 2] = aq.z;
+                a[4 * q + 3] = aq.w;
+            }
             const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(bp + kk * BN);
             const ulonglong2 b1 = *reinterpret_cast<const ulonglong2*>(bp + kk * BN + BN / 2);
-            const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
             const uint64_t b[4] = {b0.x, b0.y, b1.x, b1.y};
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
+            for (int i = 0; i < TM; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) acc2[i][j] = ffma2_bcast(a[i], b[j], acc2[i][j]);
         }
     }
     cp_async_wait<0>();
 
-    float acc[8][8];
+    float acc[TM][8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const float2 v = unpack2(acc2[i][j]);
@@ -307,10 +314,10 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
     if ((p.reduce_mode == 1 && p.splits > 1) || (sk && nslots > 1)) {
         const int stride_slots = sk ? p.sk_maxseg : p.splits;
         float* part = p.ws + (tile * stride_slots) * (BM * BN);
-        // layout [slot][16 float4 groups][THREADS]: warp stores are contiguous
+        // layout [slot][2*TM float4 groups][THREADS]: warp stores are contiguous
         float4* mine = reinterpret_cast<float4*>(part + (int64_t)slot * (BM * BN));
 #pragma unroll
-        for (int g = 0; g < 16; ++g)
+        for (int g = 0; g < 2 * TM; ++g)
             mine[g * THREADS + tid] = make_float4(acc[g >> 1][(g & 1) * 4 + 0], acc[g >> 1][(g & 1) * 4 + 1],
                                                   acc[g >> 1][(g & 1) * 4 + 2], acc[g >> 1][(g & 1) * 4 + 3]);
         __threadfence();
@@ -324,7 +331,7 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
             // 8 independent loads in flight per round
             const float4* base = reinterpret_cast<const float4*>(part) + tid;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < TM / 4; ++h) {
                 float4 s4[8];
 #pragma unroll
                 for (int g = 0; g < 8; ++g) s4[g] = __ldcg(base + (h * 8 + g) * THREADS);
@@ -359,8 +366,8 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
                                                        : p.y;
     const bool vec_ok = (p.ohw & 3) == 0;
 #pragma unroll
-    for (int ib = 0; ib < 2 && store; ++ib) {
-        const int pbase = m0 + ib * (BM / 2) + pg * 4;
+    for (int ib = 0; ib < NQ && store; ++ib) {
+        const int pbase = m0 + ib * (BM / NQ) + pg * 4;
         if (pbase >= p.m) continue;
         const int n = pbase / p.ohw;
         const int rem = pbase - n * p.ohw;
@@ -431,27 +438,29 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
 }
 
 struct TileCfg {
-    int bm, bn, threads, per_sm;
+    int bm, bn, threads, per_sm, tm;
 };
 constexpr TileCfg kTiles[] = {
-    {128, 128, 256, 2},  // 0
-    {128, 64, 128, 4},   // 1
-    {256, 64, 256, 2},   // 2
-    {64, 128, 128, 4},   // 3
+    {128, 128, 256, 2, 8},   // 0
+    {128, 64, 128, 4, 8},    // 1
+    {256, 64, 256, 2, 8},    // 2
+    {64, 128, 128, 4, 8},    // 3
+    // 16 x 8 thread tiles (TM = 16, 216 registers) were measured slower on
+    // every BASELINE layer (A/B, profiles/r01): more warps beat more ILP here.
 };
 constexpr int kNumTiles = sizeof(kTiles) / sizeof(kTiles[0]);
 constexpr int kBKCvec = 16;
 constexpr int kBKGeneric = 8;
 
-template <int BM, int BN, int T, int MINB, int BK, int KH, int KW, int SH, int SW, bool CVEC,
-          bool SK = false>
+template <int BM, int BN, int T, int MINB, int TM, int BK, int KH, int KW, int SH, int SW,
+          bool CVEC, bool SK = false>
 cudaError_t launch_one(const Problem& p, dim3 grid, cudaStream_t s) {
     if (CVEC && !SK && p.reduce_mode == 3)
-        return launch_one<BM, BN, T, MINB, BK, KH, KW, SH, SW, CVEC, true>(p, grid, s);
+        return launch_one<BM, BN, T, MINB, TM, BK, KH, KW, SH, SW, CVEC, true>(p, grid, s);
     constexpr int smem = kStages * BK * (BM + BN) * (int)sizeof(float);
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
-    auto kern = conv_ffma_kernel<BM, BN, T, MINB, BK, KH, KW, SH, SW, CVEC, SK && CVEC>;
+    auto kern = conv_ffma_kernel<BM, BN, T, MINB, TM, BK, KH, KW, SH, SW, CVEC, SK && CVEC>;
     std::call_once(once, [&] {
         attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     });
@@ -460,22 +469,22 @@ cudaError_t launch_one(const Problem& p, dim3 grid, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <int BM, int BN, int T, int MINB>
+template <int BM, int BN, int T, int MINB, int TM = 8>
 cudaError_t launch_tile(const Problem& p, int tap_kind, bool cvec, dim3 grid, cudaStream_t s) {
     constexpr int C = kBKCvec, G = kBKGeneric;
     if (cvec) {
         switch (tap_kind) {
-            case 1: return launch_one<BM, BN, T, MINB, C, 3, 3, 1, 1, true>(p, grid, s);
-            case 2: return launch_one<BM, BN, T, MINB, C, 1, 1, 1, 1, true>(p, grid, s);
-            case 5: return launch_one<BM, BN, T, MINB, C, 5, 5, 1, 1, true>(p, grid, s);
-            default: return launch_one<BM, BN, T, MINB, C, 0, 0, 0, 0, true>(p, grid, s);
+            case 1: return launch_one<BM, BN, T, MINB, TM, C, 3, 3, 1, 1, true>(p, grid, s);
+            case 2: return launch_one<BM, BN, T, MINB, TM, C, 1, 1, 1, 1, true>(p, grid, s);
+            case 5: return launch_one<BM, BN, T, MINB, TM, C, 5, 5, 1, 1, true>(p, grid, s);
+            default: return launch_one<BM, BN, T, MINB, TM, C, 0, 0, 0, 0, true>(p, grid, s);
         }
     }
     switch (tap_kind) {
-        case 1: return launch_one<BM, BN, T, MINB, G, 3, 3, 1, 1, false>(p, grid, s);
-        case 3: return launch_one<BM, BN, T, MINB, G, 7, 7, 2, 2, false>(p, grid, s);
-        case 4: return launch_one<BM, BN, T, MINB, G, 11, 11, 4, 4, false>(p, grid, s);
-        default: return launch_one<BM, BN, T, MINB, G, 0, 0, 0, 0, false>(p, grid, s);
+        case 1: return launch_one<BM, BN, T, MINB, TM, G, 3, 3, 1, 1, false>(p, grid, s);
+        case 3: return launch_one<BM, BN, T, MINB, TM, G, 7, 7, 2, 2, false>(p, grid, s);
+        case 4: return launch_one<BM, BN, T, MINB, TM, G, 11, 11, 4, 4, false>(p, grid, s);
+        default: return launch_one<BM, BN, T, MINB, TM, G, 0, 0, 0, 0, false>(p, grid, s);
     }
 }
 

@@ -381,7 +381,7 @@ def run_ours(args):
             "achieved_gbs": round(achieved_gbs, 1),
             "compulsory_bytes": byts,
             "flop_per_byte": round(L["flops"] / byts, 1),
-            "plan": ("tcgen05 bf16 128x128x64, 3 stages, TMA SW128" if tc else
+            "plan": ("tcgen05 bf16 128x128x64, TMA SW128 " + ("halo" if device.tc_plan_halo(gl) else "box") if tc else
                      (_native.plan_describe(gl, L["n"], args.mode) if L["n"] else "")),
             "launches_per_call": 1 if tc else
             (_native.plan_launches(gl, L["n"], args.mode) if L["n"] else 0)})

@@ -143,7 +143,9 @@ SMMC_API int smmc_scalar_matrix_fma_f32_host(float alpha, const float* src,
 /* 1 if smmc_conv2d_fwd_bf16_tc supports this geometry, else 0. */
 SMMC_API int smmc_tc_supported(const smmc_geom* g);
 
-/* x fp32 NCHW (n, c_i, h, w) -> x_nhwc bf16 (n, h, w, c_i), device, async. */
+/* x fp32 NCHW (n, c_i, h, w) -> x_nhwc bf16 ZERO-PADDED channels-last
+ * (n, h + 2*p_h, w + 2*p_w, c_i): the reference's zero-packed slice buffer
+ * (smm.py:56-73) materialised for all channels.  Device, async. */
 SMMC_API int smmc_pack_input_bf16_nhwc(const float* x, uint16_t* x_nhwc, const smmc_geom* g,
                                        void* stream);
 
@@ -152,8 +154,10 @@ SMMC_API int smmc_pack_input_bf16_nhwc(const float* x, uint16_t* x_nhwc, const s
 SMMC_API int smmc_pack_weights_bf16(const float* w_smm, uint16_t* w_tc, const smmc_geom* g,
                                     void* stream);
 
-/* y fp32 NCHW = conv(x_nhwc, w_tc): tcgen05 implicit GEMM over the k_h*k_w
- * shifted windows, TMA zero-fill padding.  Device pointers, async. */
+/* y fp32 NCHW = conv(x_nhwc, w_tc), x_nhwc as written by
+ * smmc_pack_input_bf16_nhwc (zero-padded): tcgen05 implicit GEMM over the
+ * k_h*k_w shifted windows (each a constant row offset of one TMA halo tile).
+ * Device pointers, async. */
 SMMC_API int smmc_conv2d_fwd_bf16_tc(const uint16_t* x_nhwc, const uint16_t* w_tc, float* y,
                                      const smmc_geom* g, void* stream);
 

@@ -2,32 +2,40 @@
 // accumulate SMM-Conv on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
 //
 // SMM-Conv writes the convolution as a sum over kernel taps (j, k) of shifted
-// windows of the input times scalar weights (smm.py:84-114).  Batching the
-// reference's per-(c, m) scalar updates over all input and output channels
-// turns each tap into one GEMM: for tap (j, k),
-//     Y[pixel, m] += X_shift(j,k)[pixel, c] * W[c, j, k, m]
-// — the "shifted GEMM" form of SMM.  The shifted window is exactly a TMA box
-// of the channels-last (NHWC) input at a shifted origin, and the zero packing
-// of the reference's slice (smm.py:56-73) is TMA's out-of-bounds zero fill.
+// windows of the zero-padded input times scalar weights (smm.py:56-114).
+// Batching the reference's per-(c, m) scalar updates over all input and output
+// channels turns each tap into one GEMM:
+//     Y[pixel, m] += X_pad_shift(j,k)[pixel, c] * W[c, j, k, m]
+// — the "shifted GEMM" form of SMM.
 //
-// Kernel structure (one 128-pixel x 128-channel output tile per CTA, 4 warps):
-//   warp 0, one lane : TMA producer — per (tap, 64-channel block) loads the
-//                      shifted A box (128 pixel rows x 128 B, SWIZZLE_128B) and
-//                      the B box (128 out-channel rows x 128 B) into a
-//                      3-stage ring, completion via mbarrier transaction bytes;
-//   warp 1, one lane : tcgen05.mma issuer — 4 x (M=128, N=128, K=16) per stage,
-//                      fp32 accumulator in TMEM (128 lanes x 128 columns),
-//                      tcgen05.commit frees the stage / signals the epilogue;
-//   all 4 warps      : epilogue — tcgen05.ld 32x32b (each thread one pixel
-//                      row), fp32 NCHW stores (coalesced along pixels).
-// Inputs: x in bf16 NHWC and weights in bf16 [tap][c_o][c_i] (K-major), made
-// once by the pack kernels below (the weight pack plays the role of the
-// reference's repack_weights, smm.py:164-167).  Stride 1 only.
+// Zero packing.  The pack pass writes the input once as a zero-padded,
+// channels-last bf16 tensor X_pad (n, h + 2p_h, w + 2p_w, c) — the reference's
+// padded slice buffer (smm.py:56-73) materialised for all channels at once.
+// In the flattened padded pixel index q = (n*Hp + r)*Wp + t, output pixel
+// (oh, ow) of image n sits at q and tap (k, j) reads q + k*Wp + j: every tap's
+// A operand is the SAME contiguous run of 128 rows shifted by a constant.
+//
+// conv_tc_halo_kernel (Wp small enough: (k_h-1)*Wp + k_w-1 + 128 <= 256 rows):
+//   per 64-channel block ONE TMA box of R = 128 + (k_h-1)*Wp + (k_w-1) rows
+//   (the "halo") is loaded; the k_h*k_w taps are UMMA smem descriptors whose
+//   start address is offset by (k*Wp + j) rows inside it ("shifting" = pure
+//   descriptor arithmetic, as shifted_view is pure view arithmetic in
+//   smm.py:206-214).  A traffic drops by ~k_h*k_w versus one box per tap.
+//   Rows whose q is not a valid output (padding columns/rows) are computed and
+//   discarded.
+// conv_tc_box_kernel (wide planes): per (tap, channel block) a 4-D box of
+//   tw x th x nb output pixels at the shifted origin of X_pad.
+//
+// Both: one 128-pixel x 128-channel tile per CTA, 4 warps — warp 0 lane 0 TMA
+// producer (mbarrier transaction bytes), warp 1 lane 0 tcgen05.mma issuer
+// (M=128, N=128, K=16, fp32 accumulator in TMEM), all warps epilogue
+// (tcgen05.ld 32x32b, each thread one pixel row, fp32 NCHW stores).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "smmc_internal.cuh"
@@ -38,59 +46,194 @@ namespace {
 
 constexpr int TC_BM = 128;
 constexpr int TC_BN = 128;
-constexpr int TC_BK = 64;  // channels per stage: one 128-byte swizzle row
-constexpr int TC_STAGES = 3;
+constexpr int TC_BK = 64;  // channels per block: one 128-byte swizzle row
 constexpr int TC_THREADS = 128;
-constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;
 constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;
-constexpr int TC_SMEM = TC_STAGES * (TC_A_BYTES + TC_B_BYTES) + 1024;
+
+// box kernel ring
+constexpr int BOX_STAGES = 3;
+constexpr int BOX_A_BYTES = TC_BM * TC_BK * 2;
+constexpr int BOX_SMEM = BOX_STAGES * (BOX_A_BYTES + TC_B_BYTES) + 1024;
+
+// halo kernel rings: 2 A halos (<= 256 rows, stage size set at launch so that
+// two CTAs fit one SM) and 3 per-tap B tiles
+constexpr int HALO_A_STAGES = 2;
+constexpr int HALO_B_STAGES = 3;
+constexpr int HALO_SMEM_MAX = HALO_A_STAGES * 256 * 128 + HALO_B_STAGES * TC_B_BYTES + 1024;
 
 struct TcParams {
     float* y;
     int n, co, oh, ow, ohw;
-    int kh, kw, ph, pw, taps, cblocks;
-    int tw, th, nb;                 // pixel tile = box of tw x th x nb (w, h, images)
-    int tiles_w, tiles_h;
-    int flat;                       // 1x1/s1/p0: A is a 2-D [pixels][c] box of 128 rows
-    uint32_t tx_bytes;              // A + B bytes per stage
+    int hp, wp;                     // padded input plane
+    int kh, kw, taps, cblocks;
+    // box kernel
+    int tw, th, nb, tiles_w, tiles_h;
+    // halo kernel
+    int halo_rows;
+    int halo_stage_bytes;           // A halo stage stride (1024-aligned)
+    uint32_t tx_a, tx_b;            // TMA bytes per A box / B box
 };
 
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+    return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+
+// Descriptor of a K-major SW128 operand that starts `row` 128-byte rows into
+// a 1024-byte-aligned TMA tile.  The 128-byte swizzle is a function of the
+// absolute shared-memory address on both sides (TMA write, UMMA read), so a
+// row-shifted start needs no base-offset correction (verified on B200: with
+// the base-offset field set to row % 8 the parity tests fail, with 0 they pass).
+__device__ __forceinline__ uint64_t desc_rows(const uint8_t* tile, int row) {
+    return ptx::desc_k_sw128(tile + row * 128);
+}
+
+// Epilogue: TMEM (128 lanes x 128 fp32 columns) -> NCHW fp32.  `ybase` is the
+// offset of (n, co=0, oh, ow) for this thread's pixel row.
+__device__ __forceinline__ void store_tile(const TcParams& p, uint32_t tmem, int warp, bool valid,
+                                           int64_t ybase, int co0) {
+#pragma unroll 1
+    for (int cc = 0; cc < TC_BN / 32; ++cc) {
+        uint32_t v[32];
+        ptx::tmem_ld_32x32b_x32(tmem + ((uint32_t)(warp * 32) << 16) + cc * 32, v);
+        if (valid) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const int co = co0 + cc * 32 + i;
+                if (co < p.co) p.y[ybase + (int64_t)co * p.ohw] = __uint_as_float(v[i]);
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(TC_THREADS, 1)
-conv_tc_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+conv_tc_halo_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                     const TcParams p) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~uintptr_t(1023));
-    uint8_t* sA = smem;
-    uint8_t* sB = smem + TC_STAGES * TC_A_BYTES;
-    __shared__ __align__(8) uint64_t full_bar[TC_STAGES];
-    __shared__ __align__(8) uint64_t empty_bar[TC_STAGES];
+    uint8_t* smem = align1024(smem_raw);
+    const int a_bytes = p.halo_stage_bytes;
+    uint8_t* sA = smem;                                   // [HALO_A_STAGES][R rows x 128 B]
+    uint8_t* sB = smem + HALO_A_STAGES * a_bytes;         // [HALO_B_STAGES][128 rows x 128 B]
+    __shared__ __align__(8) uint64_t a_full[HALO_A_STAGES], a_empty[HALO_A_STAGES];
+    __shared__ __align__(8) uint64_t b_full[HALO_B_STAGES], b_empty[HALO_B_STAGES];
     __shared__ __align__(8) uint64_t done_bar;
     __shared__ uint32_t tmem_base_sh;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const int q0 = blockIdx.x * TC_BM;  // first flattened padded pixel of the tile
+    const int co0 = blockIdx.y * TC_BN;
 
-    // ---- tile coordinates
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tm_a);
+        ptx::prefetch_tmap(&tm_b);
+        for (int s = 0; s < HALO_A_STAGES; ++s) {
+            ptx::mbar_init(&a_full[s], 1);
+            ptx::mbar_init(&a_empty[s], 1);
+        }
+        for (int s = 0; s < HALO_B_STAGES; ++s) {
+            ptx::mbar_init(&b_full[s], 1);
+            ptx::mbar_init(&b_empty[s], 1);
+        }
+        ptx::mbar_init(&done_bar, 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) ptx::tmem_alloc(&tmem_base_sh, TC_BN);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tmem_base_sh;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ================= TMA producer: one halo per channel block, B per tap
+            int bi = 0;
+            for (int cb = 0; cb < p.cblocks; ++cb) {
+                const int sa = cb % HALO_A_STAGES;
+                if (cb >= HALO_A_STAGES) ptx::mbar_wait(&a_empty[sa], ((cb / HALO_A_STAGES) - 1) & 1);
+                ptx::mbar_arrive_expect_tx(&a_full[sa], p.tx_a);
+                ptx::tma_load_2d(sA + sa * a_bytes, &tm_a, &a_full[sa], cb * TC_BK, q0);
+                for (int tap = 0; tap < p.taps; ++tap, ++bi) {
+                    const int sb = bi % HALO_B_STAGES;
+                    if (bi >= HALO_B_STAGES) ptx::mbar_wait(&b_empty[sb], ((bi / HALO_B_STAGES) - 1) & 1);
+                    ptx::mbar_arrive_expect_tx(&b_full[sb], p.tx_b);
+                    ptx::tma_load_3d(sB + sb * TC_B_BYTES, &tm_b, &b_full[sb], cb * TC_BK, co0, tap);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ================= MMA issuer
+            constexpr uint32_t idesc = ptx::idesc_bf16(TC_BM, TC_BN);
+            int bi = 0;
+            for (int cb = 0; cb < p.cblocks; ++cb) {
+                const int sa = cb % HALO_A_STAGES;
+                ptx::mbar_wait(&a_full[sa], (cb / HALO_A_STAGES) & 1);
+                for (int tap = 0; tap < p.taps; ++tap, ++bi) {
+                    const int sb = bi % HALO_B_STAGES;
+                    ptx::mbar_wait(&b_full[sb], (bi / HALO_B_STAGES) & 1);
+                    ptx::tc_fence_after();
+                    const int j = tap / p.kh;  // SMM tap order j*kh + k
+                    const int kr = tap - j * p.kh;
+                    const uint64_t da = desc_rows(sA + sa * a_bytes, kr * p.wp + j);
+                    const uint64_t db = ptx::desc_k_sw128(sB + sb * TC_B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < TC_BK / 16; ++k)
+                        ptx::mma_bf16(tmem, da + 2 * k, db + 2 * k, idesc, (bi | k) != 0);
+                    ptx::mma_commit(&b_empty[sb]);
+                }
+                ptx::mma_commit(&a_empty[sa]);
+            }
+            ptx::mma_commit(&done_bar);
+        }
+        __syncwarp();
+    }
+
+    // ================= epilogue
+    ptx::mbar_wait(&done_bar, 0);
+    ptx::tc_fence_after();
+    const int q = q0 + warp * 32 + lane;
+    const int plane = p.hp * p.wp;
+    const int n = q / plane;
+    const int r = q - n * plane;
+    const int oh = r / p.wp;
+    const int ow = r - oh * p.wp;
+    const bool valid = n < p.n && oh < p.oh && ow < p.ow;
+    const int64_t ybase = (int64_t)n * p.co * p.ohw + (int64_t)oh * p.ow + ow;
+    store_tile(p, tmem, warp, valid, ybase, co0);
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) ptx::tmem_dealloc(tmem, TC_BN);
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+conv_tc_box_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                   const TcParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = align1024(smem_raw);
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + BOX_STAGES * BOX_A_BYTES;
+    __shared__ __align__(8) uint64_t full_bar[BOX_STAGES];
+    __shared__ __align__(8) uint64_t empty_bar[BOX_STAGES];
+    __shared__ __align__(8) uint64_t done_bar;
+    __shared__ uint32_t tmem_base_sh;
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
     const int mt = blockIdx.x;
     const int co0 = blockIdx.y * TC_BN;
-    int ow0 = 0, oh0 = 0, n0 = 0, px0 = 0;
-    if (p.flat) {
-        px0 = mt * TC_BM;
-    } else {
-        const int tw_i = mt % p.tiles_w;
-        const int rest = mt / p.tiles_w;
-        const int th_i = rest % p.tiles_h;
-        ow0 = tw_i * p.tw;
-        oh0 = th_i * p.th;
-        n0 = (rest / p.tiles_h) * p.nb;
-    }
+    const int tw_i = mt % p.tiles_w;
+    const int rest = mt / p.tiles_w;
+    const int th_i = rest % p.tiles_h;
+    const int ow0 = tw_i * p.tw;
+    const int oh0 = th_i * p.th;
+    const int n0 = (rest / p.tiles_h) * p.nb;
     const int kblocks = p.taps * p.cblocks;
 
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tm_a);
         ptx::prefetch_tmap(&tm_b);
-        for (int s = 0; s < TC_STAGES; ++s) {
+        for (int s = 0; s < BOX_STAGES; ++s) {
             ptx::mbar_init(&full_bar[s], 1);
             ptx::mbar_init(&empty_bar[s], 1);
         }
@@ -105,37 +248,32 @@ conv_tc_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_const
 
     if (warp == 0) {
         if (lane == 0) {
-            // ================= TMA producer
             for (int kb = 0; kb < kblocks; ++kb) {
-                const int s = kb % TC_STAGES;
-                const int use = kb / TC_STAGES;
+                const int s = kb % BOX_STAGES;
+                const int use = kb / BOX_STAGES;
                 if (use > 0) ptx::mbar_wait(&empty_bar[s], (use - 1) & 1);
                 const int tap = kb / p.cblocks;
                 const int c0 = (kb - tap * p.cblocks) * TC_BK;
-                const int j = tap / p.kh;  // kernel column (SMM tap order j*kh + k)
+                const int j = tap / p.kh;
                 const int kr = tap - j * p.kh;
-                ptx::mbar_arrive_expect_tx(&full_bar[s], p.tx_bytes);
-                if (p.flat)
-                    ptx::tma_load_2d(sA + s * TC_A_BYTES, &tm_a, &full_bar[s], c0, px0);
-                else
-                    ptx::tma_load_4d(sA + s * TC_A_BYTES, &tm_a, &full_bar[s], c0, ow0 + j - p.pw,
-                                     oh0 + kr - p.ph, n0);
+                ptx::mbar_arrive_expect_tx(&full_bar[s], p.tx_a + p.tx_b);
+                // padded input: output (oh, ow) + tap (k, j) reads X_pad[oh + k][ow + j]
+                ptx::tma_load_4d(sA + s * BOX_A_BYTES, &tm_a, &full_bar[s], c0, ow0 + j, oh0 + kr, n0);
                 ptx::tma_load_3d(sB + s * TC_B_BYTES, &tm_b, &full_bar[s], c0, co0, tap);
             }
         }
         __syncwarp();
     } else if (warp == 1) {
         if (lane == 0) {
-            // ================= MMA issuer
             constexpr uint32_t idesc = ptx::idesc_bf16(TC_BM, TC_BN);
             for (int kb = 0; kb < kblocks; ++kb) {
-                const int s = kb % TC_STAGES;
-                ptx::mbar_wait(&full_bar[s], (kb / TC_STAGES) & 1);
+                const int s = kb % BOX_STAGES;
+                ptx::mbar_wait(&full_bar[s], (kb / BOX_STAGES) & 1);
                 ptx::tc_fence_after();
-                const uint64_t da = ptx::desc_k_sw128(sA + s * TC_A_BYTES);
+                const uint64_t da = ptx::desc_k_sw128(sA + s * BOX_A_BYTES);
                 const uint64_t db = ptx::desc_k_sw128(sB + s * TC_B_BYTES);
 #pragma unroll
-                for (int k = 0; k < TC_BK / 16; ++k)  // K=16 per MMA = 32 B = 2 descriptor units
+                for (int k = 0; k < TC_BK / 16; ++k)
                     ptx::mma_bf16(tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
                 ptx::mma_commit(&empty_bar[s]);
             }
@@ -144,60 +282,44 @@ conv_tc_bf16_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_const
         __syncwarp();
     }
 
-    // ================= epilogue (all warps): TMEM -> registers -> NCHW fp32
     ptx::mbar_wait(&done_bar, 0);
     ptx::tc_fence_after();
-    const int row = warp * 32 + lane;  // TMEM lane == tile row == output pixel
-    bool valid;
-    int64_t ybase;
-    if (p.flat) {
-        const int px = px0 + row;
-        valid = px < p.n * p.ohw;
-        const int n = valid ? px / p.ohw : 0;
-        ybase = (int64_t)n * p.co * p.ohw + (px - n * p.ohw);
-    } else {
-        const int per_img = p.tw * p.th;
-        const int nb = row / per_img;
-        const int r2 = row - nb * per_img;
-        const int hh = r2 / p.tw;
-        const int ww = r2 - hh * p.tw;
-        const int n = n0 + nb, oh = oh0 + hh, ow = ow0 + ww;
-        valid = nb < p.nb && n < p.n && oh < p.oh && ow < p.ow;
-        ybase = (int64_t)n * p.co * p.ohw + (int64_t)oh * p.ow + ow;
-    }
-#pragma unroll 1
-    for (int cc = 0; cc < TC_BN / 32; ++cc) {
-        uint32_t v[32];
-        ptx::tmem_ld_32x32b_x32(tmem + ((uint32_t)(warp * 32) << 16) + cc * 32, v);
-        if (valid) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const int co = co0 + cc * 32 + i;
-                if (co < p.co) p.y[ybase + (int64_t)co * p.ohw] = __uint_as_float(v[i]);
-            }
-        }
-    }
+    const int row = warp * 32 + lane;
+    const int per_img = p.tw * p.th;
+    const int nb = row / per_img;
+    const int r2 = row - nb * per_img;
+    const int hh = r2 / p.tw;
+    const int ww = r2 - hh * p.tw;
+    const int n = n0 + nb, oh = oh0 + hh, ow = ow0 + ww;
+    const bool valid = nb < p.nb && n < p.n && oh < p.oh && ow < p.ow;
+    const int64_t ybase = (int64_t)n * p.co * p.ohw + (int64_t)oh * p.ow + ow;
+    store_tile(p, tmem, warp, valid, ybase, co0);
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == 1) ptx::tmem_dealloc(tmem, TC_BN);
 }
 
-// x fp32 NCHW -> bf16 NHWC (per image a [C][HW] -> [HW][C] transpose through smem)
-__global__ void pack_input_nhwc_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ out,
-                                       int c, int hw) {
+// x fp32 NCHW -> zero-padded bf16 NHWC (n, h + 2p_h, w + 2p_w, c): one block
+// per (32 padded columns, 32 channels, padded row, image), smem transpose.
+__global__ void pack_input_padded_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ out,
+                                         int c, int h, int w, int ph, int pw, int hp, int wp) {
     __shared__ float tile[32][33];
-    const int n = blockIdx.z;
-    const int p0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
-    const float* xs = x + (int64_t)n * c * hw;
-    __nv_bfloat16* os = out + (int64_t)n * c * hw;
+    const int t0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+    const int n = blockIdx.z / hp, r = blockIdx.z - n * hp;
+    const int ih = r - ph;
+    const bool row_in = (unsigned)ih < (unsigned)h;
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-        const int cc = c0 + i, pp = p0 + threadIdx.x;
-        tile[i][threadIdx.x] = (cc < c && pp < hw) ? xs[(int64_t)cc * hw + pp] : 0.0f;
+        const int cc = c0 + i, iw = t0 + threadIdx.x - pw;
+        float v = 0.0f;
+        if (row_in && cc < c && (unsigned)iw < (unsigned)w)
+            v = x[(((int64_t)n * c + cc) * h + ih) * w + iw];
+        tile[i][threadIdx.x] = v;
     }
     __syncthreads();
+    __nv_bfloat16* orow = out + (((int64_t)n * hp + r) * wp) * c;
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-        const int pp = p0 + i, cc = c0 + threadIdx.x;
-        if (pp < hw && cc < c) os[(int64_t)pp * c + cc] = __float2bfloat16_rn(tile[threadIdx.x][i]);
+        const int t = t0 + i, cc = c0 + threadIdx.x;
+        if (t < wp && cc < c) orow[(int64_t)t * c + cc] = __float2bfloat16_rn(tile[threadIdx.x][i]);
     }
 }
 
@@ -208,9 +330,9 @@ __global__ void pack_weights_kernel(const float* __restrict__ w, __nv_bfloat16* 
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int ci = (int)(i % c);
-        const int64_t r = i / c;
-        const int m = (int)(r % co);
-        const int t = (int)(r / co);
+        const int64_t rr = i / c;
+        const int m = (int)(rr % co);
+        const int t = (int)(rr / co);
         out[i] = __float2bfloat16_rn(w[((int64_t)ci * taps + t) * co + m]);
     }
 }
@@ -220,13 +342,21 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static std::once_flag once;
     std::call_once(once, [] {
         cudaDriverEntryPointQueryResult q;
-        void* p = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+        void* ptr = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
                 cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
     });
     return fn;
+}
+
+CUresult encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims,
+                const cuuint64_t* strides, const cuuint32_t* box) {
+    const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    return encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), dims,
+                       strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 
 }  // namespace
@@ -235,21 +365,22 @@ TcPlan plan_tc(const smmc_geom& g) {
     TcPlan pl{};
     const int oh = (g.h + 2 * g.p_h - g.k_h) / g.s_h + 1;
     const int ow = (g.w + 2 * g.p_w - g.k_w) / g.s_w + 1;
+    const int hp = g.h + 2 * g.p_h, wp = g.w + 2 * g.p_w;
     pl.supported = g.s_h == 1 && g.s_w == 1 && (g.c_i % 8) == 0 && g.c_i >= 8 && g.n > 0;
-    pl.flat = g.k_h == 1 && g.k_w == 1 && g.p_h == 0 && g.p_w == 0;
-    if (pl.flat) {
-        pl.tw = pl.th = pl.nb = 0;
-        pl.tiles_m = ((int64_t)g.n * oh * ow + TC_BM - 1) / TC_BM;
+    const int halo_rows = TC_BM + (g.k_h - 1) * wp + (g.k_w - 1);
+    pl.halo = halo_rows <= 256;
+    if (const char* f = getenv("SMMC_TC_KERNEL")) pl.halo = pl.halo && f[0] != 'b';  // A/B hook
+    pl.halo_rows = halo_rows;
+    if (pl.halo) {
+        pl.tiles_m = ((int64_t)g.n * hp * wp + TC_BM - 1) / TC_BM;
     } else if (oh * ow <= TC_BM / 2) {
-        // several small planes per tile
         pl.tw = ow;
         pl.th = oh;
         pl.nb = TC_BM / (oh * ow);
         pl.tiles_m = (g.n + pl.nb - 1) / pl.nb;
     } else {
         pl.tw = ow < TC_BM ? ow : TC_BM;
-        pl.th = TC_BM / pl.tw;
-        if (pl.th > oh) pl.th = oh;
+        pl.th = std::min(TC_BM / pl.tw, oh);
         pl.nb = 1;
         pl.tiles_m = (int64_t)((ow + pl.tw - 1) / pl.tw) * ((oh + pl.th - 1) / pl.th) * g.n;
     }
@@ -257,62 +388,21 @@ TcPlan plan_tc(const smmc_geom& g) {
     return pl;
 }
 
-cudaError_t launch_tc_bf16(const uint16_t* x_nhwc, const uint16_t* w_tc, float* y, const smmc_geom& g,
+cudaError_t launch_tc_bf16(const uint16_t* x_pad, const uint16_t* w_tc, float* y, const smmc_geom& g,
                            cudaStream_t s, const char** why) {
     const TcPlan pl = plan_tc(g);
     if (!pl.supported) {
         *why = "bf16 tensor-core variant needs stride 1 and c_i % 8 == 0";
         return cudaErrorNotSupported;
     }
-    PFN_cuTensorMapEncodeTiled_v12000 enc = encode_fn();
-    if (!enc) {
+    if (!encode_fn()) {
         *why = "cuTensorMapEncodeTiled unavailable from the driver";
         return cudaErrorNotSupported;
     }
     const int oh = (g.h + 2 * g.p_h - g.k_h) / g.s_h + 1;
     const int ow = (g.w + 2 * g.p_w - g.k_w) / g.s_w + 1;
+    const int hp = g.h + 2 * g.p_h, wp = g.w + 2 * g.p_w;
     const int taps = g.k_h * g.k_w;
-    CUtensorMap tm_a, tm_b;
-    CUresult r;
-    uint32_t a_rows;
-    if (pl.flat) {
-        const cuuint64_t dims[2] = {(cuuint64_t)g.c_i, (cuuint64_t)g.n * g.h * g.w};
-        const cuuint64_t strides[1] = {(cuuint64_t)g.c_i * 2};
-        const cuuint32_t box[2] = {TC_BK, TC_BM};
-        const cuuint32_t es[2] = {1, 1};
-        r = enc(&tm_a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(x_nhwc), dims,
-                strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        a_rows = TC_BM;
-    } else {
-        const cuuint64_t dims[4] = {(cuuint64_t)g.c_i, (cuuint64_t)g.w, (cuuint64_t)g.h,
-                                    (cuuint64_t)g.n};
-        const cuuint64_t strides[3] = {(cuuint64_t)g.c_i * 2, (cuuint64_t)g.w * g.c_i * 2,
-                                       (cuuint64_t)g.h * g.w * g.c_i * 2};
-        const cuuint32_t box[4] = {TC_BK, (cuuint32_t)pl.tw, (cuuint32_t)pl.th, (cuuint32_t)pl.nb};
-        const cuuint32_t es[4] = {1, 1, 1, 1};
-        r = enc(&tm_a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(x_nhwc), dims,
-                strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        a_rows = (uint32_t)(pl.tw * pl.th * pl.nb);
-    }
-    if (r != CUDA_SUCCESS) {
-        *why = "cuTensorMapEncodeTiled(A) failed";
-        return cudaErrorInvalidValue;
-    }
-    {
-        const cuuint64_t dims[3] = {(cuuint64_t)g.c_i, (cuuint64_t)g.c_o, (cuuint64_t)taps};
-        const cuuint64_t strides[2] = {(cuuint64_t)g.c_i * 2, (cuuint64_t)g.c_o * g.c_i * 2};
-        const cuuint32_t box[3] = {TC_BK, TC_BN, 1};
-        const cuuint32_t es[3] = {1, 1, 1};
-        r = enc(&tm_b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<uint16_t*>(w_tc), dims,
-                strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    }
-    if (r != CUDA_SUCCESS) {
-        *why = "cuTensorMapEncodeTiled(B) failed";
-        return cudaErrorInvalidValue;
-    }
     TcParams p{};
     p.y = y;
     p.n = g.n;
@@ -320,39 +410,81 @@ cudaError_t launch_tc_bf16(const uint16_t* x_nhwc, const uint16_t* w_tc, float* 
     p.oh = oh;
     p.ow = ow;
     p.ohw = oh * ow;
+    p.hp = hp;
+    p.wp = wp;
     p.kh = g.k_h;
     p.kw = g.k_w;
-    p.ph = g.p_h;
-    p.pw = g.p_w;
     p.taps = taps;
     p.cblocks = (g.c_i + TC_BK - 1) / TC_BK;
-    p.tw = pl.tw;
-    p.th = pl.th;
-    p.nb = pl.nb;
-    p.tiles_w = pl.flat ? 1 : (ow + pl.tw - 1) / pl.tw;
-    p.tiles_h = pl.flat ? 1 : (oh + pl.th - 1) / pl.th;
-    p.flat = pl.flat;
-    p.tx_bytes = a_rows * TC_BK * 2 + TC_B_BYTES;
+    p.tx_b = TC_B_BYTES;
 
-    static std::once_flag once;
-    static cudaError_t attr = cudaSuccess;
-    std::call_once(once, [] {
-        attr = cudaFuncSetAttribute(conv_tc_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    TC_SMEM);
-    });
-    if (attr != cudaSuccess) return attr;
-    dim3 grid((unsigned)pl.tiles_m, (unsigned)pl.tiles_n);
-    conv_tc_bf16_kernel<<<grid, TC_THREADS, TC_SMEM, s>>>(tm_a, tm_b, p);
+    CUtensorMap tm_a, tm_b;
+    {
+        const cuuint64_t dims[3] = {(cuuint64_t)g.c_i, (cuuint64_t)g.c_o, (cuuint64_t)taps};
+        const cuuint64_t strides[2] = {(cuuint64_t)g.c_i * 2, (cuuint64_t)g.c_o * g.c_i * 2};
+        const cuuint32_t box[3] = {TC_BK, TC_BN, 1};
+        if (encode(&tm_b, w_tc, 3, dims, strides, box) != CUDA_SUCCESS) {
+            *why = "cuTensorMapEncodeTiled(B) failed";
+            return cudaErrorInvalidValue;
+        }
+    }
+    if (pl.halo) {
+        p.halo_rows = pl.halo_rows;
+        const cuuint64_t dims[2] = {(cuuint64_t)g.c_i, (cuuint64_t)g.n * hp * wp};
+        const cuuint64_t strides[1] = {(cuuint64_t)g.c_i * 2};
+        const cuuint32_t box[2] = {TC_BK, (cuuint32_t)pl.halo_rows};
+        if (encode(&tm_a, x_pad, 2, dims, strides, box) != CUDA_SUCCESS) {
+            *why = "cuTensorMapEncodeTiled(A halo) failed";
+            return cudaErrorInvalidValue;
+        }
+        p.tx_a = (uint32_t)pl.halo_rows * TC_BK * 2;
+        p.halo_stage_bytes = (int)((p.tx_a + 1023) & ~1023u);
+        const int smem = HALO_A_STAGES * p.halo_stage_bytes + HALO_B_STAGES * TC_B_BYTES + 1024;
+        static std::once_flag once;
+        static cudaError_t attr = cudaSuccess;
+        std::call_once(once, [] {
+            attr = cudaFuncSetAttribute(conv_tc_halo_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, HALO_SMEM_MAX);
+        });
+        if (attr != cudaSuccess) return attr;
+        dim3 grid((unsigned)pl.tiles_m, (unsigned)pl.tiles_n);
+        conv_tc_halo_kernel<<<grid, TC_THREADS, smem, s>>>(tm_a, tm_b, p);
+    } else {
+        p.tw = pl.tw;
+        p.th = pl.th;
+        p.nb = pl.nb;
+        p.tiles_w = (ow + pl.tw - 1) / pl.tw;
+        p.tiles_h = (oh + pl.th - 1) / pl.th;
+        const cuuint64_t dims[4] = {(cuuint64_t)g.c_i, (cuuint64_t)wp, (cuuint64_t)hp,
+                                    (cuuint64_t)g.n};
+        const cuuint64_t strides[3] = {(cuuint64_t)g.c_i * 2, (cuuint64_t)wp * g.c_i * 2,
+                                       (cuuint64_t)hp * wp * g.c_i * 2};
+        const cuuint32_t box[4] = {TC_BK, (cuuint32_t)pl.tw, (cuuint32_t)pl.th, (cuuint32_t)pl.nb};
+        if (encode(&tm_a, x_pad, 4, dims, strides, box) != CUDA_SUCCESS) {
+            *why = "cuTensorMapEncodeTiled(A box) failed";
+            return cudaErrorInvalidValue;
+        }
+        p.tx_a = (uint32_t)(pl.tw * pl.th * pl.nb) * TC_BK * 2;
+        static std::once_flag once;
+        static cudaError_t attr = cudaSuccess;
+        std::call_once(once, [] {
+            attr = cudaFuncSetAttribute(conv_tc_box_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, BOX_SMEM);
+        });
+        if (attr != cudaSuccess) return attr;
+        dim3 grid((unsigned)pl.tiles_m, (unsigned)pl.tiles_n);
+        conv_tc_box_kernel<<<grid, TC_THREADS, BOX_SMEM, s>>>(tm_a, tm_b, p);
+    }
     count_launches(1);
     return cudaGetLastError();
 }
 
 cudaError_t launch_pack_input_nhwc(const float* x, uint16_t* out, const smmc_geom& g,
                                    cudaStream_t s) {
-    const int hw = g.h * g.w;
-    dim3 grid((hw + 31) / 32, (g.c_i + 31) / 32, g.n);
-    pack_input_nhwc_kernel<<<grid, dim3(32, 8), 0, s>>>(x, reinterpret_cast<__nv_bfloat16*>(out),
-                                                        g.c_i, hw);
+    const int hp = g.h + 2 * g.p_h, wp = g.w + 2 * g.p_w;
+    dim3 grid((wp + 31) / 32, (g.c_i + 31) / 32, g.n * hp);
+    pack_input_padded_kernel<<<grid, dim3(32, 8), 0, s>>>(x, reinterpret_cast<__nv_bfloat16*>(out),
+                                                          g.c_i, g.h, g.w, g.p_h, g.p_w, hp, wp);
     count_launches(1);
     return cudaGetLastError();
 }

@@ -66,8 +66,9 @@ int ffma_launches(const FfmaPlan& plan);
 // bf16 tensor-core variant (conv_tc.cu)
 struct TcPlan {
     int supported;
-    int flat;
-    int tw, th, nb;
+    int halo;          // flattened padded-pixel tiles, one halo box per channel block
+    int halo_rows;
+    int tw, th, nb;    // box kernel pixel tile
     int64_t tiles_m;
     int tiles_n;
 };

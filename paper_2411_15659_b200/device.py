@@ -138,14 +138,18 @@ def _stream_ptr(torch, dev):
     return ctypes.c_void_p(s) if s else None
 
 
+def packed_input_shape(geom, n):
+    """Zero-padded channels-last bf16 layout of the tensor-core variant."""
+    return (n, geom.padded_h, geom.padded_w, geom.in_channels)
+
+
 def pack_input_bf16(x, geom, out=None):
-    """fp32 NCHW (N, c_i, h, w) -> bf16 NHWC (N, h, w, c_i) on the device."""
+    """fp32 NCHW (N, c_i, h, w) -> zero-padded bf16 NHWC (N, h+2p_h, w+2p_w, c_i)."""
     torch = _torch()
     n = x.shape[0]
     _check_tensor(x, (n,) + geom.input_shape, "input batch")
     if out is None:
-        out = torch.empty((n, geom.in_h, geom.in_w, geom.in_channels), dtype=torch.bfloat16,
-                          device=x.device)
+        out = torch.empty(packed_input_shape(geom, n), dtype=torch.bfloat16, device=x.device)
     g = _native.Geom.of(geom, n)
     with torch.cuda.device(x.device):
         _native.check(_native.lib().smmc_pack_input_bf16_nhwc(
@@ -169,15 +173,17 @@ def pack_weights_bf16(weights_smm, geom):
 
 
 def conv2d_bf16_tc(x_nhwc, w_tc, geom, out=None):
-    """tcgen05 bf16 conv: x_nhwc bf16 (N, h, w, c_i), w_tc bf16 (taps, c_o, c_i)
-    -> fp32 NCHW (N, c_o, h', w'), on torch's current stream."""
+    """tcgen05 bf16 conv: x_nhwc zero-padded bf16 (N, h+2p_h, w+2p_w, c_i) from
+    pack_input_bf16, w_tc bf16 (taps, c_o, c_i) -> fp32 NCHW (N, c_o, h', w'),
+    on torch's current stream."""
     torch = _torch()
     if not isinstance(x_nhwc, torch.Tensor) or x_nhwc.dim() != 4 or not x_nhwc.is_cuda \
             or x_nhwc.dtype != torch.bfloat16 or not x_nhwc.is_contiguous():
-        raise ShapeMismatchError("x_nhwc must be a contiguous CUDA bf16 (N, h, w, c_i) tensor")
+        raise ShapeMismatchError("x_nhwc must be a contiguous CUDA bf16 (N, hp, wp, c_i) tensor")
     n = x_nhwc.shape[0]
-    if tuple(x_nhwc.shape[1:]) != (geom.in_h, geom.in_w, geom.in_channels):
-        raise ShapeMismatchError(f"x_nhwc has shape {tuple(x_nhwc.shape)}")
+    if tuple(x_nhwc.shape) != packed_input_shape(geom, n):
+        raise ShapeMismatchError(f"x_nhwc has shape {tuple(x_nhwc.shape)}, expected "
+                                 f"{packed_input_shape(geom, n)}")
     if tuple(w_tc.shape) != (geom.k_w * geom.k_h, geom.out_channels, geom.in_channels) \
             or w_tc.dtype != torch.bfloat16 or not w_tc.is_cuda:
         raise ShapeMismatchError("w_tc must be bf16 (k_w*k_h, c_o, c_i) on the device")
@@ -222,3 +228,10 @@ class TcSmmConv2d:
 
     def __call__(self, x_nhwc, out=None):
         return conv2d_bf16_tc(x_nhwc, self.w_tc, self.geom, out=out)
+
+
+def tc_plan_halo(geom):
+    """True when the tensor-core variant uses the halo kernel for this geometry
+    (one TMA box per 64-channel block shared by all taps)."""
+    halo_rows = 128 + (geom.k_h - 1) * geom.padded_w + (geom.k_w - 1)
+    return halo_rows <= 256

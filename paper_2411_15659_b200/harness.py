@@ -181,10 +181,10 @@ def _backend(name, geom, batch, x, w_oihw):
         if not device.tc_supported(geom, batch):
             return False, None, 0
         mod = device.TcSmmConv2d(geom, w_oihw)
-        xb = torch.empty((batch, geom.in_h, geom.in_w, geom.in_channels), dtype=torch.bfloat16,
+        xb = torch.empty(device.packed_input_shape(geom, batch), dtype=torch.bfloat16,
                          device=x.device)
         out = torch.empty((batch,) + geom.output_shape, device=x.device)
-        scratch = xb.numel() * 2  # channels-last bf16 copy of the input
+        scratch = xb.numel() * 2  # zero-padded channels-last bf16 copy of the input
 
         def run():
             mod(mod.pack_input(x, out=xb), out=out)

@@ -59,7 +59,7 @@ constexpr int BOX_SMEM = BOX_STAGES * (BOX_A_BYTES + TC_B_BYTES) + 1024;
 // two CTAs fit one SM) and 3 per-tap B tiles
 constexpr int HALO_A_STAGES = 2;
 constexpr int HALO_B_STAGES = 3;
-constexpr int HALO_SMEM_MAX = HALO_A_STAGES * 256 * 128 + HALO_B_STAGES * TC_B_BYTES + 1024;
+constexpr int HALO_SMEM_MAX = HALO_A_STAGES * 256 * 128 + HALO_B_STAGES * 2 * TC_B_BYTES + 1024;
 
 struct TcParams {
     float* y;
@@ -89,10 +89,11 @@ __device__ __forceinline__ uint64_t desc_rows(const uint8_t* tile, int row) {
 
 // Epilogue: TMEM (128 lanes x 128 fp32 columns) -> NCHW fp32.  `ybase` is the
 // offset of (n, co=0, oh, ow) for this thread's pixel row.
+template <int NCOL = TC_BN>
 __device__ __forceinline__ void store_tile(const TcParams& p, uint32_t tmem, int warp, bool valid,
                                            int64_t ybase, int co0) {
 #pragma unroll 1
-    for (int cc = 0; cc < TC_BN / 32; ++cc) {
+    for (int cc = 0; cc < NCOL / 32; ++cc) {
         uint32_t v[32];
         ptx::tmem_ld_32x32b_x32(tmem + ((uint32_t)(warp * 32) << 16) + cc * 32, v);
         if (valid) {
@@ -105,9 +106,11 @@ __device__ __forceinline__ void store_tile(const TcParams& p, uint32_t tmem, int
     }
 }
 
+template <int HBN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 conv_tc_halo_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                     const TcParams p) {
+    constexpr int HB_BYTES = HBN * TC_BK * 2;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align1024(smem_raw);
     const int a_bytes = p.halo_stage_bytes;
@@ -121,7 +124,7 @@ conv_tc_halo_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_const
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int q0 = blockIdx.x * TC_BM;  // first flattened padded pixel of the tile
-    const int co0 = blockIdx.y * TC_BN;
+    const int co0 = blockIdx.y * HBN;
 
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tm_a);
@@ -137,7 +140,7 @@ conv_tc_halo_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_const
         ptx::mbar_init(&done_bar, 1);
         ptx::fence_mbar_init();
     }
-    if (warp == 1) ptx::tmem_alloc(&tmem_base_sh, TC_BN);
+    if (warp == 1) ptx::tmem_alloc(&tmem_base_sh, HBN);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -156,7 +159,7 @@ conv_tc_halo_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_const
                     const int sb = bi % HALO_B_STAGES;
                     if (bi >= HALO_B_STAGES) ptx::mbar_wait(&b_empty[sb], ((bi / HALO_B_STAGES) - 1) & 1);
                     ptx::mbar_arrive_expect_tx(&b_full[sb], p.tx_b);
-                    ptx::tma_load_3d(sB + sb * TC_B_BYTES, &tm_b, &b_full[sb], cb * TC_BK, co0, tap);
+                    ptx::tma_load_3d(sB + sb * HB_BYTES, &tm_b, &b_full[sb], cb * TC_BK, co0, tap);
                 }
             }
         }
@@ -164,7 +167,7 @@ conv_tc_halo_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_const
     } else if (warp == 1) {
         if (lane == 0) {
             // ================= MMA issuer
-            constexpr uint32_t idesc = ptx::idesc_bf16(TC_BM, TC_BN);
+            constexpr uint32_t idesc = ptx::idesc_bf16(TC_BM, HBN);
             int bi = 0;
             for (int cb = 0; cb < p.cblocks; ++cb) {
                 const int sa = cb % HALO_A_STAGES;
@@ -176,7 +179,7 @@ conv_tc_halo_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_const
                     const int j = tap / p.kh;  // SMM tap order j*kh + k
                     const int kr = tap - j * p.kh;
                     const uint64_t da = desc_rows(sA + sa * a_bytes, kr * p.wp + j);
-                    const uint64_t db = ptx::desc_k_sw128(sB + sb * TC_B_BYTES);
+                    const uint64_t db = ptx::desc_k_sw128(sB + sb * HB_BYTES);
 #pragma unroll
                     for (int k = 0; k < TC_BK / 16; ++k)
                         ptx::mma_bf16(tmem, da + 2 * k, db + 2 * k, idesc, (bi | k) != 0);
@@ -200,10 +203,10 @@ conv_tc_halo_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_const
     const int ow = r - oh * p.wp;
     const bool valid = n < p.n && oh < p.oh && ow < p.ow;
     const int64_t ybase = (int64_t)n * p.co * p.ohw + (int64_t)oh * p.ow + ow;
-    store_tile(p, tmem, warp, valid, ybase, co0);
+    store_tile<HBN>(p, tmem, warp, valid, ybase, co0);
     ptx::tc_fence_before();
     __syncthreads();
-    if (warp == 1) ptx::tmem_dealloc(tmem, TC_BN);
+    if (warp == 1) ptx::tmem_dealloc(tmem, HBN);
 }
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -384,7 +387,14 @@ TcPlan plan_tc(const smmc_geom& g) {
         pl.nb = 1;
         pl.tiles_m = (int64_t)((ow + pl.tw - 1) / pl.tw) * ((oh + pl.th - 1) / pl.th) * g.n;
     }
-    pl.tiles_n = (g.c_o + TC_BN - 1) / TC_BN;
+    // N = 256 tiles (one CTA/SM, epilogue not overlapped) measured slower than
+    // N = 128 at two CTAs/SM on every config-5 layer; kept behind SMMC_TC_BN=256.
+    pl.bn = TC_BN;
+    if (pl.halo && g.c_o >= 256) {
+        const char* f = getenv("SMMC_TC_BN");
+        if (f && atoi(f) == 256) pl.bn = 256;
+    }
+    pl.tiles_n = (g.c_o + pl.bn - 1) / pl.bn;
     return pl;
 }
 
@@ -439,16 +449,36 @@ cudaError_t launch_tc_bf16(const uint16_t* x_pad, const uint16_t* w_tc, float* y
         }
         p.tx_a = (uint32_t)pl.halo_rows * TC_BK * 2;
         p.halo_stage_bytes = (int)((p.tx_a + 1023) & ~1023u);
-        const int smem = HALO_A_STAGES * p.halo_stage_bytes + HALO_B_STAGES * TC_B_BYTES + 1024;
+        // N = 256 output channels per tile when c_o allows: 12 KB of smem
+        // operand reads per 128-cycle MMA instead of 8 KB per 64 cycles
+        const int hbn = pl.bn;
+        if (hbn == 256) {
+            const cuuint64_t bd[3] = {(cuuint64_t)g.c_i, (cuuint64_t)g.c_o, (cuuint64_t)taps};
+            const cuuint64_t bs[2] = {(cuuint64_t)g.c_i * 2, (cuuint64_t)g.c_o * g.c_i * 2};
+            const cuuint32_t bb[3] = {TC_BK, 256, 1};
+            if (encode(&tm_b, w_tc, 3, bd, bs, bb) != CUDA_SUCCESS) {
+                *why = "cuTensorMapEncodeTiled(B256) failed";
+                return cudaErrorInvalidValue;
+            }
+            p.tx_b = 256 * TC_BK * 2;
+        }
+        const int smem = HALO_A_STAGES * p.halo_stage_bytes + HALO_B_STAGES * (int)p.tx_b + 1024;
         static std::once_flag once;
         static cudaError_t attr = cudaSuccess;
         std::call_once(once, [] {
-            attr = cudaFuncSetAttribute(conv_tc_halo_kernel,
+            attr = cudaFuncSetAttribute(conv_tc_halo_kernel<128>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, HALO_SMEM_MAX);
+            if (attr == cudaSuccess)
+                attr = cudaFuncSetAttribute(conv_tc_halo_kernel<256>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            HALO_SMEM_MAX);
         });
         if (attr != cudaSuccess) return attr;
         dim3 grid((unsigned)pl.tiles_m, (unsigned)pl.tiles_n);
-        conv_tc_halo_kernel<<<grid, TC_THREADS, smem, s>>>(tm_a, tm_b, p);
+        if (hbn == 256)
+            conv_tc_halo_kernel<256><<<grid, TC_THREADS, smem, s>>>(tm_a, tm_b, p);
+        else
+            conv_tc_halo_kernel<128><<<grid, TC_THREADS, smem, s>>>(tm_a, tm_b, p);
     } else {
         p.tw = pl.tw;
         p.th = pl.th;

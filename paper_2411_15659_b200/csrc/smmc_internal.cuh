@@ -69,6 +69,7 @@ struct TcPlan {
     int halo;          // flattened padded-pixel tiles, one halo box per channel block
     int halo_rows;
     int tw, th, nb;    // box kernel pixel tile
+    int bn;            // output channels per tile (128, or 256 for the halo kernel)
     int64_t tiles_m;
     int tiles_n;
 };

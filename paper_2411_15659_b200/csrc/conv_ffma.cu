@@ -152,11 +152,38 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
 
     // ---- cvec loader state (tap-major K order)
     uint32_t rowmask = 0, colmask = 0;
-    if (CVEC && pvalid) {
+    const bool masks = kh <= 32 && kw <= 32;
+    if (masks && pvalid) {
         for (int r = 0; r < kh; ++r) rowmask |= (uint32_t)((unsigned)(ih0 + r) < (unsigned)p.h) << r;
         for (int j = 0; j < kw; ++j)
             colmask |= (uint32_t)((unsigned)(iw0 + j) < (unsigned)p.w_in) << j;
     }
+    // generic path: an odometer over this thread's next update index
+    // kidx = (c*kw + j)*kh + k (the reference's order) and its input offset
+    // c*h*w + k*w + j, advanced by +1 update with compares instead of divisions
+    int od_k = 0, od_j = 0, od_kidx = 0;
+    int64_t od_off = 0;
+    if (!CVEC && masks) {
+        od_kidx = kt_beg * BK + lk0;
+        const int c = od_kidx / taps;
+        const int tap = od_kidx - c * taps;
+        od_j = tap / kh;
+        od_k = tap - od_j * kh;
+        od_off = (int64_t)c * p.hw + od_k * p.w_in + od_j;
+    }
+    auto od_step = [&]() {
+        ++od_kidx;
+        ++od_k;
+        od_off += p.w_in;
+        if (od_k == kh) {
+            od_k = 0;
+            od_off += 1 - (int64_t)kh * p.w_in;
+            if (++od_j == kw) {
+                od_j = 0;
+                od_off += p.hw - kw;
+            }
+        }
+    };
     const int cblocks = p.c / BK;
     const int64_t a_blk = (int64_t)BK * p.hw;             // A pointer step per channel block
     const int64_t a_elem = (int64_t)KSTEP * p.hw;         // between one thread's A elements
@@ -212,6 +239,16 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
         } else {
             // reference (c, j, k) order: kidx = (c*kw + j)*kh + k
             const int kb = (kt_beg + kt) * BK;
+            if (masks) {
+#pragma unroll
+                for (int i = 0; i < A_PER; ++i) {
+                    const bool ok = pvalid && od_kidx < p.k && ((rowmask >> od_k) & (colmask >> od_j) & 1u);
+                    cp_async4_zfill(as_base + slot * AS_STAGE + i * KSTEP * BM * 4,
+                                    ok ? xg + xoff0 + od_off : xg, ok);
+#pragma unroll
+                    for (int st = 0; st < KSTEP; ++st) od_step();
+                }
+            } else {
 #pragma unroll
             for (int i = 0; i < A_PER; ++i) {
                 const int kk = lk0 + i * KSTEP;
@@ -226,6 +263,7 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
                                 (unsigned)iw < (unsigned)p.w_in;
                 const float* src = ok ? xg + xoff0 + (int64_t)c * p.hw + kr * p.w_in + j : xg;
                 cp_async4_zfill(as_base + slot * AS_STAGE + i * KSTEP * BM * 4, src, ok);
+            }
             }
 #pragma unroll
             for (int i = 0; i < B_PER; ++i) {

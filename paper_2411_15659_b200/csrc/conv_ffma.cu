@@ -557,6 +557,8 @@ constexpr TunedPlan kTuned[] = {
     {64, 128, 56, 56, 256, 3, 1, 1, 3, 1},     // 2136.5 us (2154.1)
     {64, 256, 56, 56, 256, 3, 1, 1, 3, 1},     // 4206.0 us (4249.3)
     {64, 256, 28, 28, 512, 3, 1, 1, 0, 3},     // 2122.6 us (2164.0)
+    {8, 3, 227, 227, 96, 11, 4, 0, 1, 1},      // 73.5 us (73.9)
+    {8, 256, 56, 56, 64, 1, 1, 0, 2, 1},       // 28.6 us (30.6)
 };
 
 int64_t best_cost_waves(const FfmaPlan& b, int64_t m, int c_o, int sm_count) {

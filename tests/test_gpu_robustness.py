@@ -1,0 +1,136 @@
+"""GPU robustness of the C ABI: re-entrancy, stream ordering, graph capture,
+workspace contracts, large index ranges and error paths."""
+
+import ctypes
+import threading
+
+import numpy as np
+import pytest
+
+from oracle import smm_oracle as orc
+import paper_2411_15659_b200 as smm
+from paper_2411_15659_b200 import ConvGeometry, _native
+from paper_2411_15659_b200.tensors import synthetic_layer
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+def test_host_entry_is_reentrant_across_threads():
+    """Eight Python threads hammer the host-buffer entry with different
+    geometries; every result must still match the oracle (the per-device
+    staging pool is mutex-protected, the ctypes call releases the GIL)."""
+    geoms = [ConvGeometry(8 + 8 * (i % 3), 16, 10 + i, 12, 3, 3, pad_h=1, pad_w=1) for i in range(8)]
+    data = [synthetic_layer(g, 2, 50 + i) for i, g in enumerate(geoms)]
+    refs = [orc.smm_conv_c(x, orc.repack(w), g) for g, (x, w) in zip(geoms, data)]
+    errors = []
+
+    def work(i):
+        g = geoms[i]
+        x, w = data[i]
+        ws = smm.repack_weights(w, g)
+        for _ in range(5):
+            y = smm.smm_conv_batched(x, ws, g)
+            if orc.max_abs_ratio(y, refs[i]) > TOL:
+                errors.append(i)
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(8)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors
+
+
+def test_device_path_on_side_stream_and_in_cuda_graph():
+    import torch
+    from paper_2411_15659_b200 import device
+    g = ConvGeometry(64, 64, 14, 14, 3, 3, pad_h=1, pad_w=1)
+    x, w = synthetic_layer(g, 4, 9)
+    ref = orc.smm_conv_c(x, orc.repack(w), g)
+    mod = device.SmmConv2d(g, w, max_batch=4)
+    xd = torch.from_numpy(x).cuda()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        y = mod(xd)
+    torch.cuda.current_stream().wait_stream(s)
+    assert orc.max_abs_ratio(y.cpu().numpy(), ref) <= TOL
+    # capture (split-K plans included: the counter memset is a graph node)
+    out = torch.empty_like(y)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        mod(xd, out=out)
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, y)
+
+
+def test_workspace_contract_errors():
+    import torch
+    g = ConvGeometry(512, 512, 7, 7, 3, 3, pad_h=1, pad_w=1)
+    need = _native.workspace_bytes(g, 1)
+    assert need > 0
+    x = torch.zeros((1,) + g.input_shape, device="cuda")
+    w = torch.zeros(g.weights_smm_shape, device="cuda")
+    y = torch.empty((1,) + g.output_shape, device="cuda")
+    lib = _native.lib()
+    G = _native.Geom.of(g, 1)
+    small = torch.empty(need // 2, dtype=torch.uint8, device="cuda")
+    st = lib.smmc_conv2d_fwd_f32(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(w.data_ptr()),
+                                 ctypes.c_void_p(y.data_ptr()), ctypes.byref(G), 0,
+                                 ctypes.c_void_p(small.data_ptr()), small.numel(), None)
+    assert st == _native.SMMC_EWORKSPACE
+    with pytest.raises(ValueError):
+        _native.check(st)
+    # misaligned pointers are rejected before any launch
+    st = lib.smmc_conv2d_fwd_f32(ctypes.c_void_p(x.data_ptr() + 4), ctypes.c_void_p(w.data_ptr()),
+                                 ctypes.c_void_p(y.data_ptr()), ctypes.byref(G), 0, None, 0, None)
+    assert st == _native.SMMC_ESHAPE
+    st = lib.smmc_conv2d_fwd_f32(None, None, None, ctypes.byref(G), 0, None, 0, None)
+    assert st == _native.SMMC_ESHAPE
+    st = lib.smmc_conv2d_fwd_f32(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(w.data_ptr()),
+                                 ctypes.c_void_p(y.data_ptr()), ctypes.byref(G), 7, None, 0, None)
+    assert st == _native.SMMC_EUNSUPPORTED
+
+
+def test_large_index_ranges():
+    """A batch whose tensors exceed 2^31 bytes (x: 2.2 GB): 64-bit offsets in
+    the loaders and epilogue; checked on first/last samples."""
+    import torch
+    from paper_2411_15659_b200 import device
+    g = ConvGeometry(64, 64, 112, 112, 3, 3, pad_h=1, pad_w=1)
+    n = 700  # 700*64*112*112*4 B = 2.25 GB per tensor
+    assert n * g.in_channels * g.in_h * g.in_w * 4 > 2 ** 31
+    torch.manual_seed(0)
+    xd = torch.rand((n,) + g.input_shape, device="cuda") * 2 - 1
+    _, w = synthetic_layer(ConvGeometry(64, 64, 4, 4, 3, 3, pad_h=1, pad_w=1), 1, 3)
+    wd = torch.from_numpy(smm.repack_weights(w, g)).cuda()
+    y = device.conv2d(xd, wd, g)
+    torch.cuda.synchronize()
+    for s in (0, n - 1):
+        ref = orc.smm_conv_c(xd[s].cpu().numpy(), orc.repack(w), g, threads=orc.host_threads())
+        assert orc.max_abs_ratio(y[s].cpu().numpy(), ref) <= TOL
+    del xd, y
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("gt", [
+    (3, 4, 33, 31, 3, 3, 3, 3, 2, 1),      # stride 3, rectangular, c_o % 4 == 0
+    (16, 6, 20, 20, 5, 3, 2, 1, 0, 2),     # c_o % 4 != 0 on the tap-major path
+    (17, 9, 15, 13, 4, 2, 1, 2, 3, 0),     # even kernel, c_i % 16 != 0, stride (1,2)
+    (32, 40, 9, 9, 9, 9, 1, 1, 4, 4),      # 9x9 kernel (generic tap path)
+    (2, 3, 40, 5, 35, 1, 1, 1, 0, 0),      # k_h = 35 > 32: no padding masks (division path)
+])
+def test_unusual_geometries(gt):
+    import torch
+    from paper_2411_15659_b200 import device
+    g = ConvGeometry(*gt)
+    x, w = synthetic_layer(g, 3, 21)
+    ws = smm.repack_weights(w, g)
+    ref = orc.smm_conv_c(x, orc.repack(w), g)
+    y = device.conv2d(torch.from_numpy(x).cuda(), torch.from_numpy(ws).cuda(), g)
+    assert orc.max_abs_ratio(y.cpu().numpy(), ref) <= TOL
+    ye = smm.smm_conv_batched(x, ws, g, mode="exact")
+    assert np.array_equal(ye, ref)

@@ -46,19 +46,26 @@ def _stale():
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force=False, verbose=False, jobs=None):
-    """Compile every ``csrc/*.cu`` for sm_100a and link ``lib/libsmmc.so``."""
-    if not force and not _stale():
+def build(force=False, verbose=False, jobs=None, out=None, defines=()):
+    """Compile every ``csrc/*.cu`` for sm_100a and link ``lib/libsmmc.so``.
+
+    ``out``/``defines`` build an A/B variant (e.g. ``lib/ab/x.so`` with
+    ``-DNAME=VAL``) into a separate object directory; select it at run time
+    with ``SMMC_LIB``."""
+    lib = Path(out) if out else LIB
+    build_dir = BUILD if not out else BUILD.parent / ("ab_" + lib.stem)
+    if not out and not force and not _stale():
         return LIB
-    BUILD.mkdir(parents=True, exist_ok=True)
+    build_dir.mkdir(parents=True, exist_ok=True)
+    lib.parent.mkdir(parents=True, exist_ok=True)
     LIBDIR.mkdir(parents=True, exist_ok=True)
     exe = nvcc()
     objs = []
     procs = []
     for src in sources():
-        obj = BUILD / (src.stem + ".o")
-        log = BUILD / (src.stem + ".ptxas.log")
-        cmd = [exe, *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+        obj = build_dir / (src.stem + ".o")
+        log = build_dir / (src.stem + ".ptxas.log")
+        cmd = [exe, *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", str(src), "-o", str(obj)]
         procs.append((src, obj, log, subprocess.Popen(
             cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
         objs.append(obj)
@@ -73,14 +80,17 @@ def build(force=False, verbose=False, jobs=None):
     if failed:
         msg = "\n".join(f"--- {s.name}\n{o[-6000:]}" for s, o in failed)
         raise RuntimeError(f"nvcc failed:\n{msg}")
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [exe, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", str(tmp),
            *map(str, objs), "-lcudart_static", "-lrt", "-ldl", "-lpthread",
            "-Xlinker", "--no-undefined"]
     subprocess.run(cmd, check=True, capture_output=not verbose)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    args = sys.argv[1:]
+    out = args[args.index("--out") + 1] if "--out" in args else None
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    print(build(force="--force" in args, verbose="-v" in args, out=out, defines=defs))

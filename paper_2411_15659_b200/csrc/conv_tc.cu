@@ -71,6 +71,8 @@ struct TcParams {
     // halo kernel
     int halo_rows;
     int halo_stage_bytes;           // A halo stage stride (1024-aligned)
+    int b_stages;                   // persistent kernel: B ring depth
+    int tiles_m, tiles_n;           // persistent kernel: tile space (tile = m * tiles_n + n)
     uint32_t tx_a, tx_b;            // TMA bytes per A box / B box
 };
 
@@ -207,6 +209,176 @@ conv_tc_halo_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_const
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == 1) ptx::tmem_dealloc(tmem, HBN);
+}
+
+// Persistent, warp-specialised halo kernel for c_o >= 256 (one CTA per SM,
+// 2 + PH_EPI_WARPS warps, N = HBN output channels per tile):
+//   warp 0 lane 0 : TMA producer over this CTA's tiles — per 64-channel block
+//                   one halo box (A ring, 2 deep), per tap one B tile (B ring as
+//                   deep as smem allows);
+//   warp 1 lane 0 : tcgen05.mma issuer (M=128, N=HBN: 4 x 128-cycle MMAs per
+//                   stage, so per-stage barrier/issue overhead is amortised)
+//                   into one of TWO HBN-column TMEM accumulators; MT = 2
+//                   stacks two 128-pixel sub-tiles (two halo boxes) on one B
+//                   stage, for c_o = 128 layers that cannot use N = 256;
+//   warps 2..9    : epilogue of the previous tile while the next one computes
+//                   (warp w reads TMEM lanes 32*(w%4)..., half the columns).
+#ifndef PH_EPI_WARPS_OVERRIDE  // A/B builds: 4, 8 or 16
+constexpr int PH_EPI_WARPS = 16;  // four per TMEM lane quarter, each a quarter of the columns
+#else
+constexpr int PH_EPI_WARPS = PH_EPI_WARPS_OVERRIDE;
+#endif
+constexpr int PH_THREADS = 64 + 32 * PH_EPI_WARPS;
+constexpr int PH_ACC = 2;
+constexpr int PH_B_MAX = 8;
+
+template <int HBN, int MT>
+__global__ void __launch_bounds__(PH_THREADS, 1)
+conv_tc_halo_persistent_kernel(const __grid_constant__ CUtensorMap tm_a,
+                               const __grid_constant__ CUtensorMap tm_b, const TcParams p) {
+    constexpr int HB_BYTES = HBN * TC_BK * 2;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = align1024(smem_raw);
+    const int a_bytes = p.halo_stage_bytes;
+    const int b_stages = p.b_stages;
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + HALO_A_STAGES * MT * a_bytes;
+    __shared__ __align__(8) uint64_t a_full[HALO_A_STAGES], a_empty[HALO_A_STAGES];
+    __shared__ __align__(8) uint64_t b_full[PH_B_MAX], b_empty[PH_B_MAX];
+    __shared__ __align__(8) uint64_t acc_full[PH_ACC], acc_empty[PH_ACC];
+    __shared__ uint32_t tmem_base_sh;
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int tiles = p.tiles_m * p.tiles_n;
+
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tm_a);
+        ptx::prefetch_tmap(&tm_b);
+        for (int s = 0; s < HALO_A_STAGES; ++s) {
+            ptx::mbar_init(&a_full[s], 1);
+            ptx::mbar_init(&a_empty[s], 1);
+        }
+        for (int s = 0; s < b_stages; ++s) {
+            ptx::mbar_init(&b_full[s], 1);
+            ptx::mbar_init(&b_empty[s], 1);
+        }
+        for (int s = 0; s < PH_ACC; ++s) {
+            ptx::mbar_init(&acc_full[s], 1);
+            ptx::mbar_init(&acc_empty[s], PH_EPI_WARPS);  // one arrival per epilogue warp
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 2) ptx::tmem_alloc(&tmem_base_sh, PH_ACC * MT * HBN);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tmem_base_sh;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int ai = 0, bi = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+                const int q0 = (t / p.tiles_n) * (TC_BM * MT);
+                const int co0 = (t % p.tiles_n) * HBN;
+                for (int cb = 0; cb < p.cblocks; ++cb, ++ai) {
+                    const int sa = ai % HALO_A_STAGES;
+                    if (ai >= HALO_A_STAGES)
+                        ptx::mbar_wait(&a_empty[sa], ((ai / HALO_A_STAGES) - 1) & 1);
+                    ptx::mbar_arrive_expect_tx(&a_full[sa], MT * p.tx_a);
+#pragma unroll
+                    for (int m = 0; m < MT; ++m)
+                        ptx::tma_load_2d(sA + (sa * MT + m) * a_bytes, &tm_a, &a_full[sa], cb * TC_BK,
+                                         q0 + m * TC_BM);
+                    for (int tap = 0; tap < p.taps; ++tap, ++bi) {
+                        const int sb = bi % b_stages;
+                        if (bi >= b_stages) ptx::mbar_wait(&b_empty[sb], ((bi / b_stages) - 1) & 1);
+                        ptx::mbar_arrive_expect_tx(&b_full[sb], p.tx_b);
+                        ptx::tma_load_3d(sB + sb * HB_BYTES, &tm_b, &b_full[sb], cb * TC_BK, co0, tap);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_bf16(TC_BM, HBN);
+            int ai = 0, bi = 0, local = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+                const int acc = local % PH_ACC;
+                if (local >= PH_ACC) ptx::mbar_wait(&acc_empty[acc], ((local / PH_ACC) - 1) & 1);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem + acc * MT * HBN;
+                bool first = true;
+                for (int cb = 0; cb < p.cblocks; ++cb, ++ai) {
+                    const int sa = ai % HALO_A_STAGES;
+                    ptx::mbar_wait(&a_full[sa], (ai / HALO_A_STAGES) & 1);
+                    for (int tap = 0; tap < p.taps; ++tap, ++bi) {
+                        const int sb = bi % b_stages;
+                        ptx::mbar_wait(&b_full[sb], (bi / b_stages) & 1);
+                        ptx::tc_fence_after();
+                        const int j = tap / p.kh;  // SMM tap order j*kh + k
+                        const int kr = tap - j * p.kh;
+                        const uint64_t db = ptx::desc_k_sw128(sB + sb * HB_BYTES);
+#pragma unroll
+                        for (int m = 0; m < MT; ++m) {
+                            const uint64_t da = desc_rows(sA + (sa * MT + m) * a_bytes, kr * p.wp + j);
+#pragma unroll
+                            for (int k = 0; k < TC_BK / 16; ++k)
+                                ptx::mma_bf16(d + m * HBN, da + 2 * k, db + 2 * k, idesc,
+                                              (first && k == 0) ? 0u : 1u);
+                        }
+                        first = false;
+                        ptx::mma_commit(&b_empty[sb]);
+                    }
+                    ptx::mma_commit(&a_empty[sa]);
+                }
+                ptx::mma_commit(&acc_full[acc]);
+            }
+        }
+        __syncwarp();
+    } else {
+        const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+        constexpr int parts = PH_EPI_WARPS / 4;  // column slices per lane quarter
+        constexpr int chunks = MT * HBN / 32 / parts;
+        const int part = (warp - 2) >> 2;
+        const int plane = p.hp * p.wp;
+        int local = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+            const int acc = local % PH_ACC;
+            ptx::mbar_wait(&acc_full[acc], (local / PH_ACC) & 1);
+            ptx::tc_fence_after();
+            const int co0 = (t % p.tiles_n) * HBN;
+#pragma unroll 1
+            for (int c = part * chunks; c < (part + 1) * chunks; ++c) {
+                const int m = c / (HBN / 32);  // M sub-tile
+                const int cc = c - m * (HBN / 32);
+                const int q = (t / p.tiles_n) * (TC_BM * MT) + m * TC_BM + quarter * 32 + lane;
+                const int n = q / plane;
+                const int r = q - n * plane;
+                const int oh = r / p.wp;
+                const int ow = r - oh * p.wp;
+                const bool valid = n < p.n && oh < p.oh && ow < p.ow;
+                const int64_t ybase = (int64_t)n * p.co * p.ohw + (int64_t)oh * p.ow + ow;
+                uint32_t v[32];
+                ptx::tmem_ld_32x32b_x32(
+                    tmem + ((uint32_t)(quarter * 32) << 16) + (acc * MT + m) * HBN + cc * 32, v);
+                if (valid) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const int co = co0 + cc * 32 + i;
+                        if (co < p.co) p.y[ybase + (int64_t)co * p.ohw] = __uint_as_float(v[i]);
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&acc_empty[acc]);
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) ptx::tmem_dealloc(tmem, PH_ACC * MT * HBN);
 }
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -387,12 +559,40 @@ TcPlan plan_tc(const smmc_geom& g) {
         pl.nb = 1;
         pl.tiles_m = (int64_t)((ow + pl.tw - 1) / pl.tw) * ((oh + pl.th - 1) / pl.th) * g.n;
     }
-    // N = 256 tiles (one CTA/SM, epilogue not overlapped) measured slower than
-    // N = 128 at two CTAs/SM on every config-5 layer; kept behind SMMC_TC_BN=256.
+    // N = 256 runs the persistent warp-specialised kernel (one CTA/SM, TMEM
+    // double-buffered so 16 epilogue warps drain one tile while the next one
+    // computes). Its 128-cycle MMAs amortise the per-stage barrier/issue
+    // overhead that caps the N = 128 kernel; it needs enough tiles to fill
+    // 148 SMs twice (measured): conv256@14_n256 74.7 -> 60.7 us,
+    // vgg 512@28_n64 217 -> 195 us, 1x1 64->256@56_n256 284 -> 184 us, while
+    // small-batch layers (few tiles) lose.
     pl.bn = TC_BN;
+    pl.persistent = 0;
     if (pl.halo && g.c_o >= 256) {
-        const char* f = getenv("SMMC_TC_BN");
-        if (f && atoi(f) == 256) pl.bn = 256;
+        const int64_t tiles256 = pl.tiles_m * ((g.c_o + 255) / 256);
+        if (g.c_o % 256 == 0 && tiles256 >= 2 * 148) pl.bn = 256;
+        if (const char* f = getenv("SMMC_TC_BN")) pl.bn = atoi(f) == 256 ? 256 : TC_BN;  // A/B hook
+    }
+    if (pl.halo) {
+        // N = 128 tiles go persistent (for the 16-warp epilogue) only when they
+        // fit one wave anyway: 512@7_n32 28.6 -> 26.8 us, 256@14_n32 18.5 -> 17.0,
+        // but 128@28_n32 (225 tiles) 14.1 -> 17.5 us.
+        pl.persistent = pl.bn == 256 || pl.tiles_m * ((g.c_o + TC_BN - 1) / TC_BN) <= 148;
+    }
+    // N = 128 layers with many tiles (c_o = 128): two stacked 128-pixel
+    // sub-tiles share each B stage (8 MMAs per barrier round instead of 4):
+    // 128@28_n256 86.9 -> 76.3 us; with fewer tiles the halved tile count loses.
+    pl.mt = 1;
+    if (pl.halo && pl.bn == TC_BN && (pl.tiles_m / 2) * ((g.c_o + TC_BN - 1) / TC_BN) >= 2 * 148) {
+        pl.persistent = 1;
+        pl.mt = 2;
+    }
+    if (const char* f = getenv("SMMC_TC_PERSIST")) {  // A/B hooks
+        pl.persistent = pl.halo && (pl.bn == 256 || atoi(f) != 0);
+        if (!pl.persistent) pl.mt = 1;
+    }
+    if (pl.persistent && pl.bn == TC_BN) {
+        if (const char* f = getenv("SMMC_TC_MT")) pl.mt = atoi(f) == 2 ? 2 : 1;
     }
     pl.tiles_n = (g.c_o + pl.bn - 1) / pl.bn;
     return pl;
@@ -462,23 +662,52 @@ cudaError_t launch_tc_bf16(const uint16_t* x_pad, const uint16_t* w_tc, float* y
             }
             p.tx_b = 256 * TC_BK * 2;
         }
-        const int smem = HALO_A_STAGES * p.halo_stage_bytes + HALO_B_STAGES * (int)p.tx_b + 1024;
-        static std::once_flag once;
-        static cudaError_t attr = cudaSuccess;
-        std::call_once(once, [] {
-            attr = cudaFuncSetAttribute(conv_tc_halo_kernel<128>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, HALO_SMEM_MAX);
-            if (attr == cudaSuccess)
-                attr = cudaFuncSetAttribute(conv_tc_halo_kernel<256>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            HALO_SMEM_MAX);
-        });
-        if (attr != cudaSuccess) return attr;
-        dim3 grid((unsigned)pl.tiles_m, (unsigned)pl.tiles_n);
-        if (hbn == 256)
-            conv_tc_halo_kernel<256><<<grid, TC_THREADS, smem, s>>>(tm_a, tm_b, p);
-        else
+        if (pl.persistent) {
+            constexpr int kPersistSmem = 227 * 1024 - 4096;
+            static std::once_flag once2;
+            static cudaError_t attr2 = cudaSuccess;
+            std::call_once(once2, [] {
+                const void* fns[3] = {(const void*)conv_tc_halo_persistent_kernel<256, 1>,
+                                      (const void*)conv_tc_halo_persistent_kernel<128, 1>,
+                                      (const void*)conv_tc_halo_persistent_kernel<128, 2>};
+                for (const void* f : fns)
+                    if (attr2 == cudaSuccess)
+                        attr2 = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     kPersistSmem);
+            });
+            if (attr2 != cudaSuccess) return attr2;
+            const int mt = pl.mt;
+            p.b_stages = std::min(PH_B_MAX, (kPersistSmem - 1024 - HALO_A_STAGES * mt * p.halo_stage_bytes) /
+                                                (int)p.tx_b);
+            if (p.b_stages < 2) {
+                *why = "tensor-core halo tiles do not fit shared memory";
+                return cudaErrorInvalidValue;
+            }
+            p.tiles_m = (int)((pl.tiles_m + mt - 1) / mt);
+            p.tiles_n = pl.tiles_n;
+            const int psmem = HALO_A_STAGES * mt * p.halo_stage_bytes + p.b_stages * (int)p.tx_b + 1024;
+            int sms = 148, dev = 0;
+            if (cudaGetDevice(&dev) == cudaSuccess)
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            const int pgrid = (int)std::min<int64_t>((int64_t)p.tiles_m * p.tiles_n, sms);
+            if (hbn == 256)
+                conv_tc_halo_persistent_kernel<256, 1><<<pgrid, PH_THREADS, psmem, s>>>(tm_a, tm_b, p);
+            else if (mt == 2)
+                conv_tc_halo_persistent_kernel<128, 2><<<pgrid, PH_THREADS, psmem, s>>>(tm_a, tm_b, p);
+            else
+                conv_tc_halo_persistent_kernel<128, 1><<<pgrid, PH_THREADS, psmem, s>>>(tm_a, tm_b, p);
+        } else {
+            const int smem = HALO_A_STAGES * p.halo_stage_bytes + HALO_B_STAGES * (int)p.tx_b + 1024;
+            static std::once_flag once;
+            static cudaError_t attr = cudaSuccess;
+            std::call_once(once, [] {
+                attr = cudaFuncSetAttribute(conv_tc_halo_kernel<128>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, HALO_SMEM_MAX);
+            });
+            if (attr != cudaSuccess) return attr;
+            dim3 grid((unsigned)pl.tiles_m, (unsigned)pl.tiles_n);
             conv_tc_halo_kernel<128><<<grid, TC_THREADS, smem, s>>>(tm_a, tm_b, p);
+        }
     } else {
         p.tw = pl.tw;
         p.th = pl.th;

@@ -70,6 +70,8 @@ struct TcPlan {
     int halo_rows;
     int tw, th, nb;    // box kernel pixel tile
     int bn;            // output channels per tile (128, or 256 for the halo kernel)
+    int persistent;    // halo: persistent warp-specialised kernel (always for bn = 256)
+    int mt;            // persistent: 128-pixel M sub-tiles per tile sharing one B stage
     int64_t tiles_m;
     int tiles_n;
 };

@@ -67,3 +67,26 @@ def test_tc_rejects_strided():
     assert not device.tc_supported(g)
     with pytest.raises(BackendUnsupportedError):
         device.TcSmmConv2d(g, np.zeros(g.weights_shape, np.float32))
+
+
+@pytest.mark.parametrize("bn", ["128", "128p", "128p2", "256"])
+@pytest.mark.parametrize("case", [
+    (64, 512, 14, 14, 3, 3, 1, 1, 1, 1, 3),   # two N=256 tiles, ragged last M tile
+    (32, 320, 9, 11, 3, 3, 1, 1, 1, 1, 2),    # c_o % 256 != 0: partial second N tile
+    (128, 256, 20, 20, 3, 3, 1, 1, 1, 1, 40),  # > 2 tiles per persistent CTA
+], ids=lambda c: "x".join(map(str, c)) if isinstance(c, tuple) else c)
+def test_tc_both_tile_widths(monkeypatch, case, bn):
+    """Every halo kernel (non-persistent N=128; persistent warp-specialised
+    N=128 / two stacked 128-pixel sub-tiles / N=256 with TMEM double
+    buffering) forced via the plan hooks."""
+    monkeypatch.setenv("SMMC_TC_BN", bn[:3])
+    monkeypatch.setenv("SMMC_TC_PERSIST", "1" if "p" in bn else "0")
+    monkeypatch.setenv("SMMC_TC_MT", "2" if bn.endswith("p2") else "1")
+    *gt, n = case
+    g = ConvGeometry(*gt)
+    x, w, y = _run_tc(g, n, 5)
+    samples = [0, n // 2, n - 1]
+    ref = orc.smm_conv_c(np.ascontiguousarray(x[samples]), orc.repack(w), g,
+                         threads=orc.host_threads())
+    err = orc.max_abs_ratio(y[samples], ref)
+    assert 1e-5 <= err <= TOL_BF16, err

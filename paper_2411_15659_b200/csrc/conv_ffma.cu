@@ -441,6 +441,14 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
     }  // segment loop
 }
 
+// reduce_modes 1 and 3: the per-tile arrival counters must read zero at
+// kernel start.  An SM kernel rather than cudaMemsetAsync: the host entry's
+// copy engines are busy with the H2D/D2H pipeline, and a memset queued behind
+// them delayed every conv by 15-50 us (CUPTI timeline, tools/e2e_timeline.py).
+__global__ void __launch_bounds__(256) zero_counters_kernel(int* __restrict__ c, int n) {
+    for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) c[i] = 0;
+}
+
 // reduce_mode 2: y = sum of the partial planes in split order.
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ ws,
                                                             float* __restrict__ y, int64_t total,
@@ -730,6 +738,11 @@ FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) {
 cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
     dim3 grid((p.m + pl.bm - 1) / pl.bm, (p.co + pl.bn - 1) / pl.bn, pl.splits);
     if (pl.reduce_mode == 3) grid = dim3((unsigned)pl.sk_ctas, 1, 1);
+    if (pl.reduce_mode == 1 || pl.reduce_mode == 3) {
+        zero_counters_kernel<<<(int)std::min<int64_t>((pl.tiles + 255) / 256, 148), 256, 0, s>>>(
+            p.counters, (int)pl.tiles);
+        count_launches(1);
+    }
     cudaError_t e;
     switch (pl.variant) {
         case 0: e = launch_tile<128, 128, 256, 2>(p, pl.tap_kind, pl.cvec, grid, s); break;
@@ -746,6 +759,6 @@ cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-int ffma_launches(const FfmaPlan& pl) { return pl.reduce_mode == 2 ? 2 : 1; }
+int ffma_launches(const FfmaPlan& pl) { return pl.reduce_mode == 0 ? 1 : 2; }
 
 }  // namespace smmc

@@ -253,11 +253,8 @@ int conv_device(const float* x, const float* w, float* y, const smmc_geom* g, in
     }
     if (pl.reduce_mode == 1 || pl.reduce_mode == 3) {
         p.counters = reinterpret_cast<int*>(static_cast<char*>(ws) + pl.ws_counter_offset);
-        // arrival counters must read zero at kernel start; the workspace may
-        // hold another problem's partials where this plan keeps its counters
-        if ((st = cuda_status(cudaMemsetAsync(p.counters, 0, (size_t)pl.tiles * sizeof(int), stream),
-                              "cudaMemsetAsync(split-K counters)")))
-            return st;
+        // (zeroed by launch_ffma: the workspace may hold another problem's
+        // partials where this plan keeps its counters)
     }
     return cuda_status(launch_ffma(p, pl, stream), "conv_ffma launch");
 }
@@ -358,8 +355,11 @@ int smmc_conv2d_fwd_f32_host(const float* x, const float* w_smm, float* y, const
     // with its neighbours'.  Chunks of >= ~8 MB keep the copies efficient.
     const size_t per_sample = (xs + ys) * sizeof(float);
     int chunks = (int)std::min<size_t>((size_t)kMaxChunks, (size_t)g->n);
-    chunks = (int)std::min<size_t>((size_t)chunks,
-                                   std::max<size_t>(1, (per_sample * g->n) / (8u << 20)));
+    static const size_t chunk_bytes = [] {
+        const char* f = getenv("SMMC_HOST_CHUNK_MB");  // tuning hook
+        return (size_t)(f && atoi(f) > 0 ? atoi(f) : 8) << 20;
+    }();
+    chunks = (int)std::min<size_t>((size_t)chunks, std::max<size_t>(1, (per_sample * g->n) / chunk_bytes));
     const int per = (g->n + chunks - 1) / chunks;
     chunks = (g->n + per - 1) / per;
     smmc_geom gc = *g;
@@ -376,15 +376,23 @@ int smmc_conv2d_fwd_f32_host(const float* x, const float* w_smm, float* y, const
     if ((st = cuda_status(cudaMemcpyAsync(wd, w_smm, wb, cudaMemcpyHostToDevice, hp.s_in),
                           "H2D w_smm")))
         return st;
+    // All H2D copies are enqueued first: streams share a few hardware queues,
+    // and an H2D queued behind a conv's event wait stalls the copy engine.
+    for (int c = 0; c < chunks; ++c) {
+        const int n0 = c * per;
+        const int nc = std::min(per, g->n - n0);
+        const size_t xo = (size_t)n0 * xs;
+        if ((st = cuda_status(cudaMemcpyAsync(xd + xo, x + xo, nc * xs * sizeof(float),
+                                              cudaMemcpyHostToDevice, hp.s_in),
+                              "H2D x")) ||
+            (st = cuda_status(cudaEventRecord(hp.ev_in[c], hp.s_in), "cudaEventRecord")))
+            return st;
+    }
     for (int c = 0; c < chunks; ++c) {
         const int n0 = c * per;
         gc.n = std::min(per, g->n - n0);
         const size_t xo = (size_t)n0 * xs, yo = (size_t)n0 * ys;
-        if ((st = cuda_status(cudaMemcpyAsync(xd + xo, x + xo, gc.n * xs * sizeof(float),
-                                              cudaMemcpyHostToDevice, hp.s_in),
-                              "H2D x")) ||
-            (st = cuda_status(cudaEventRecord(hp.ev_in[c], hp.s_in), "cudaEventRecord")) ||
-            (st = cuda_status(cudaStreamWaitEvent(hp.stream, hp.ev_in[c], 0), "cudaStreamWaitEvent")))
+        if ((st = cuda_status(cudaStreamWaitEvent(hp.stream, hp.ev_in[c], 0), "cudaStreamWaitEvent")))
             return st;
         if ((st = conv_device(xd + xo, wd, yd + yo, &gc, mode, hp.buf[3], wsb, hp.stream))) return st;
         if ((st = cuda_status(cudaEventRecord(hp.ev_done[c], hp.stream), "cudaEventRecord")) ||

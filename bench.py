@@ -381,8 +381,8 @@ def run_ours(args):
             "achieved_gbs": round(achieved_gbs, 1),
             "compulsory_bytes": byts,
             "flop_per_byte": round(L["flops"] / byts, 1),
-            "plan": ("tcgen05 bf16 128x128x64, TMA SW128 " + ("halo" if device.tc_plan_halo(gl) else "box") if tc else
-                     (_native.plan_describe(gl, L["n"], args.mode) if L["n"] else "")),
+            "plan": ((_native.tc_plan_describe(gl, L["n"]) if tc else
+                      _native.plan_describe(gl, L["n"], args.mode)) if L["n"] else ""),
             "launches_per_call": 1 if tc else
             (_native.plan_launches(gl, L["n"], args.mode) if L["n"] else 0)})
     dom = max(details, key=lambda d: d["ms_avg"])
@@ -397,7 +397,7 @@ def run_ours(args):
         roofline = {"bound": "hbm", "achieved": dom["achieved_gbs"], "peak": hbm_peak,
                     "unit": "GB/s", "frac": round(dom["achieved_gbs"] / hbm_peak, 4),
                     "traffic": traffic,
-                    "kernel": f"{'conv_tc_bf16_kernel' if tc else 'conv_ffma_kernel'} "
+                    "kernel": f"{'conv_tc_halo*/box kernel' if tc else 'conv_ffma_kernel'} "
                               f"({dom['layer']}: {dom['plan']})",
                     "peak_source": "hbm_gbs of MEASURED_PEAKS.json (measured copy bandwidth)",
                     "achieved_def": "compulsory bytes (input + weights + output) of one launch / "
@@ -406,7 +406,7 @@ def run_ours(args):
         roofline = {"bound": "tensor", "achieved": dom["tflops"], "peak": bf16_peak_tf,
                     "unit": "TFLOP/s", "frac": round(dom["tflops"] / bf16_peak_tf, 4),
                     "traffic": traffic,
-                    "kernel": f"conv_tc_bf16_kernel ({dom['layer']}: {dom['plan']})",
+                    "kernel": f"tcgen05 conv ({dom['layer']}: {dom['plan']})",
                     "peak_source": "bf16_tflops (burst) of MEASURED_PEAKS.json (cuBLAS bf16 GEMM)",
                     "achieved_def": "dense algorithmic FLOPs of one launch / its avg CUDA-event "
                                     "duration inside the timed graph"}
@@ -419,6 +419,16 @@ def run_ours(args):
                                    "measured FP32 peak exists)",
                     "achieved_def": "dense algorithmic FLOPs of one launch / its avg CUDA-event "
                                     "duration inside the timed graph"}
+        cfile = ROOT / "profiles" / "ffma_ceiling.json"
+        if cfile.exists():  # measured register-only FFMA2 ceiling, context for `frac`
+            try:
+                ceil = json.loads(cfile.read_text())
+                c_tf = float(ceil["ffma2_conv_pattern_tflops"])
+                roofline["measured_ffma2_ceiling"] = {
+                    "tflops": c_tf, "frac": round(dom["tflops"] / c_tf, 4),
+                    "source": ceil.get("source", "profiles/ffma_ceiling.json")}
+            except (ValueError, KeyError):
+                pass
 
     # ---- e2e: host buffers through the C ABI host entry (H2D + conv + D2H)
     e2e = None

@@ -174,6 +174,9 @@ SMMC_API int smmc_plan_launches(const smmc_geom* g, int mode);
 /* Short human-readable description of the kernel plan (tile, split-K). */
 SMMC_API int smmc_plan_describe(const smmc_geom* g, int mode, char* buf, size_t len);
 
+/* Same for the bf16 tensor-core variant (tile shape, halo/box, persistence). */
+SMMC_API int smmc_tc_plan_describe(const smmc_geom* g, char* buf, size_t len);
+
 /* Total kernels this library has launched in this process (atomic). */
 SMMC_API uint64_t smmc_launch_count(void);
 

@@ -37,7 +37,7 @@ EXPORTED_SYMBOLS = (
     "smmc_workspace_bytes", "smmc_conv2d_fwd_f32", "smmc_conv2d_fwd_f32_host",
     "smmc_extract_slice_f32", "smmc_scalar_matrix_fma_f32",
     "smmc_extract_slice_f32_host", "smmc_scalar_matrix_fma_f32_host",
-    "smmc_plan_launches", "smmc_plan_describe", "smmc_launch_count",
+    "smmc_plan_launches", "smmc_plan_describe", "smmc_tc_plan_describe", "smmc_launch_count",
     "smmc_tc_supported", "smmc_pack_input_bf16_nhwc", "smmc_pack_weights_bf16",
     "smmc_conv2d_fwd_bf16_tc", "smmc_im2col_bytes", "smmc_im2col_pack_f32",
 )
@@ -94,6 +94,7 @@ _SIGNATURES = {
     "smmc_plan_describe": (ctypes.c_int, [_GP, ctypes.c_int, ctypes.c_char_p,
                                           ctypes.c_size_t]),
     "smmc_launch_count": (ctypes.c_uint64, []),
+    "smmc_tc_plan_describe": (ctypes.c_int, [_GP, ctypes.c_char_p, ctypes.c_size_t]),
     "smmc_tc_supported": (ctypes.c_int, [_GP]),
     "smmc_pack_input_bf16_nhwc": (ctypes.c_int, [_P, _P, _GP, _P]),
     "smmc_pack_weights_bf16": (ctypes.c_int, [_P, _P, _GP, _P]),
@@ -161,6 +162,13 @@ def plan_describe(geom, batch=1, mode="ffma"):
     g = Geom.of(geom, batch)
     check(lib().smmc_plan_describe(ctypes.byref(g), mode_id(mode), buf, 256),
           "smmc_plan_describe")
+    return buf.value.decode()
+
+
+def tc_plan_describe(geom, batch=1):
+    buf = ctypes.create_string_buffer(256)
+    g = Geom.of(geom, batch)
+    check(lib().smmc_tc_plan_describe(ctypes.byref(g), buf, 256), "smmc_tc_plan_describe")
     return buf.value.decode()
 
 

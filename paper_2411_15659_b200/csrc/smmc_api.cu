@@ -293,6 +293,32 @@ int smmc_plan_launches(const smmc_geom* g, int mode) {
     return ffma_launches(plan_ffma(*g, sm_count_for(current_device())));
 }
 
+int smmc_tc_plan_describe(const smmc_geom* g, char* buf, size_t len) {
+    int oh = 0, ow = 0;
+    int st = check_geom(g, &oh, &ow);
+    if (st) return st;
+    if (!buf || !len) return SMMC_OK;
+    smmc_geom gg = *g;
+    if (gg.n == 0) gg.n = 1;
+    const TcPlan pl = plan_tc(gg);
+    if (!pl.supported) {
+        snprintf(buf, len, "tc: unsupported (needs stride 1 and c_i %% 8 == 0)");
+        return SMMC_OK;
+    }
+    if (pl.halo)
+        snprintf(buf, len,
+                 "tc: tcgen05 bf16 M=%d x N=%d x K=64, TMA SW128 halo (%d rows), %s, %lld x %d tiles",
+                 128 * (pl.persistent ? pl.mt : 1), pl.bn, pl.halo_rows,
+                 pl.persistent ? "persistent warp-specialised, 2 TMEM accumulators, 16 epilogue warps"
+                               : "one tile per CTA, 2 CTAs/SM",
+                 (long long)((pl.tiles_m + (pl.persistent ? pl.mt : 1) - 1) / (pl.persistent ? pl.mt : 1)),
+                 pl.tiles_n);
+    else
+        snprintf(buf, len, "tc: tcgen05 bf16 M=128 x N=%d x K=64, TMA SW128 4-D box per tap (%dx%dx%d px), "
+                 "%lld x %d tiles", pl.bn, pl.tw, pl.th, pl.nb, (long long)pl.tiles_m, pl.tiles_n);
+    return SMMC_OK;
+}
+
 int smmc_plan_describe(const smmc_geom* g, int mode, char* buf, size_t len) {
     int oh = 0, ow = 0;
     int st = check_geom(g, &oh, &ow);

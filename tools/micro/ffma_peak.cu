@@ -78,7 +78,7 @@ __device__ __forceinline__ uint64_t ffma2p(uint64_t a, uint64_t b, uint64_t c) {
     return d;
 }
 
-template <int ITERS, int MI, int NJ, bool PAIR>
+template <int ITERS, int MI, int NJ, bool PAIR, bool JOUTER = false>
 __global__ void __launch_bounds__(256, 1) k_shape(float* out, float seed) {
     float a[MI];
     uint64_t ap[MI];
@@ -99,11 +99,18 @@ __global__ void __launch_bounds__(256, 1) k_shape(float* out, float seed) {
 #pragma unroll
         for (int j = 0; j < NJ; ++j) acc[i][j] = 0;
     for (int it = 0; it < ITERS; ++it) {
+        if (JOUTER) {
+#pragma unroll
+            for (int j = 0; j < NJ; ++j)
+#pragma unroll
+                for (int i = 0; i < MI; ++i) acc[i][j] = ffma2(a[i], b[j], acc[i][j]);
+        } else {
 #pragma unroll
         for (int i = 0; i < MI; ++i)
 #pragma unroll
             for (int j = 0; j < NJ; ++j)
                 acc[i][j] = PAIR ? ffma2p(ap[i], b[j], acc[i][j]) : ffma2(a[i], b[j], acc[i][j]);
+        }
 #pragma unroll
         for (int i = 0; i < MI; ++i) {
             a[i] = __uint_as_float(__float_as_uint(a[i]) ^ 1u);
@@ -150,6 +157,10 @@ int main() {
         run("FFMA2 8x4 pairs (conv pattern)", k_ffma2<IT>, b, 2.0 * 64 * IT);
         run("FFMA  8x8 scalar", k_ffma<IT>, b, 2.0 * 64 * IT);
         run("FFMA2 bcast 4x8", k_shape<IT, 4, 8, false>, b, 2.0 * 64 * IT);
+        run("FFMA2 bcast 8x4 (shape kernel)", k_shape<IT, 8, 4, false>, b, 2.0 * 64 * IT);
+        run("FFMA2 bcast 8x4 j-outer", k_shape<IT, 8, 4, false, true>, b, 2.0 * 64 * IT);
+        run("FFMA2 bcast 4x8 j-outer", k_shape<IT, 4, 8, false, true>, b, 2.0 * 64 * IT);
+        run("FFMA2 bcast 2x16", k_shape<IT, 2, 16, false>, b, 2.0 * 64 * IT);
         run("FFMA2 bcast 2x8", k_shape<IT, 2, 8, false>, b, 2.0 * 32 * IT);
         run("FFMA2 bcast 8x2", k_shape<IT, 8, 2, false>, b, 2.0 * 32 * IT);
         run("FFMA2 pair  8x4", k_shape<IT, 8, 4, true>, b, 2.0 * 64 * IT);

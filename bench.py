@@ -60,6 +60,9 @@ def parse_args():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--gather", default="fused", choices=["fused", "nccl"],
+                    help="c_o-sharded layer (config 5, N>1): fused peer-write epilogue "
+                         "(smmc_conv2d_fwd_f32_gather over CUDA IPC) or NCCL all-gather + permute")
     ap.add_argument("--details", default="", help="write per-layer details JSON here")
     return ap.parse_args()
 
@@ -266,10 +269,24 @@ def run_ours(args):
         need = 0 if tc else _native.workspace_bytes(L["gl"], L["n"], args.mode)
         L["ws"] = torch.empty(max(need, 16), dtype=torch.uint8, device=dev)
         if L["shard"] == "cout":
-            L["gather"] = torch.empty((world,) + shape, device=dev)
             L["full"] = torch.empty((L["n"],) + L["g"].output_shape, device=dev)
+            if world > 1 and args.gather == "fused" and not tc and args.mode == "ffma":
+                from paper_2411_15659_b200.parallel import PeerBuffers
+                L["peers"] = PeerBuffers(L["full"])
+                L["flag"] = torch.zeros(1, device=dev)
+                L["ws"] = torch.empty(max(_native.gather_workspace_bytes(L["gl"], L["n"]), 16),
+                                      dtype=torch.uint8, device=dev)
+            else:
+                L["gather"] = torch.empty((world,) + shape, device=dev)
 
     def run_layer(L, r):
+        if "peers" in L:  # fused c_o-shard gather: fence, peer-write conv, fence
+            dist.all_reduce(L["flag"])
+            if L["gl"].out_channels > 0 and L["n"]:
+                device.conv2d_gather(L["x"][r], L["w"][r], L["peers"].ptrs, L["gl"], L["c_range"][0],
+                                     L["g"].out_channels, workspace=L["ws"])
+            dist.all_reduce(L["flag"])
+            return
         if L["n"] == 0:
             return
         if tc:

@@ -177,6 +177,32 @@ SMMC_API int smmc_plan_describe(const smmc_geom* g, int mode, char* buf, size_t 
 /* Same for the bf16 tensor-core variant (tile shape, halo/box, persistence). */
 SMMC_API int smmc_tc_plan_describe(const smmc_geom* g, char* buf, size_t len);
 
+/* ---- Fused output-channel-shard all-gather.
+ * Rank r of P holds the full input and W_smm[..., co_base:co_base+c_o] as a
+ * compact (c_i, k_w, k_h, c_o) slice (g_local->c_o = its channel count).  The
+ * conv epilogue stores its channels straight into every replica
+ * y_out[0..n_out) of the full (N, co_total, h', w') output — this rank's own
+ * buffer and the peers' buffers mapped over NVLink with smmc_ipc_open — so no
+ * gather buffer, collective payload or permute copy exists.  The caller orders
+ * completion (a stream-ordered barrier after the call, e.g. a 1-element NCCL
+ * all-reduce) before peers read.  Replaces the reference's Algorithm-2 channel
+ * partition + join (smm.py:273-306) lifted to devices.  ffma mode. */
+#define SMMC_MAX_OUT 8
+#define SMMC_IPC_HANDLE_BYTES 64
+SMMC_API int smmc_conv2d_fwd_f32_gather(const float* x, const float* w_slice, float* const* y_out,
+                                        int n_out, const smmc_geom* g_local, int co_base,
+                                        int co_total, void* workspace, size_t workspace_bytes,
+                                        void* stream);
+
+/* Workspace the gather needs (its plan always places through the reduce pass). */
+SMMC_API size_t smmc_gather_workspace_bytes(const smmc_geom* g_local);
+
+/* CUDA IPC for the gather: handle (SMMC_IPC_HANDLE_BYTES) + byte offset of an
+ * interior device pointer, and open/close of a peer's pointer in this process. */
+SMMC_API int smmc_ipc_handle(const void* dev_ptr, void* handle, size_t* offset);
+SMMC_API int smmc_ipc_open(const void* handle, size_t offset, void** dev_ptr);
+SMMC_API int smmc_ipc_close(void* dev_ptr, size_t offset);
+
 /* Total kernels this library has launched in this process (atomic). */
 SMMC_API uint64_t smmc_launch_count(void);
 

@@ -40,7 +40,12 @@ EXPORTED_SYMBOLS = (
     "smmc_plan_launches", "smmc_plan_describe", "smmc_tc_plan_describe", "smmc_launch_count",
     "smmc_tc_supported", "smmc_pack_input_bf16_nhwc", "smmc_pack_weights_bf16",
     "smmc_conv2d_fwd_bf16_tc", "smmc_im2col_bytes", "smmc_im2col_pack_f32",
+    "smmc_conv2d_fwd_f32_gather", "smmc_gather_workspace_bytes", "smmc_ipc_handle",
+    "smmc_ipc_open", "smmc_ipc_close",
 )
+
+SMMC_MAX_OUT = 8
+SMMC_IPC_HANDLE_BYTES = 64
 
 
 class Geom(ctypes.Structure):
@@ -101,6 +106,13 @@ _SIGNATURES = {
     "smmc_conv2d_fwd_bf16_tc": (ctypes.c_int, [_P, _P, _P, _GP, _P]),
     "smmc_im2col_bytes": (ctypes.c_size_t, [_GP]),
     "smmc_im2col_pack_f32": (ctypes.c_int, [_P, _P, _GP, _P]),
+    "smmc_conv2d_fwd_f32_gather": (ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_void_p),
+                                                  ctypes.c_int, _GP, ctypes.c_int, ctypes.c_int,
+                                                  _P, ctypes.c_size_t, _P]),
+    "smmc_gather_workspace_bytes": (ctypes.c_size_t, [_GP]),
+    "smmc_ipc_handle": (ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_size_t)]),
+    "smmc_ipc_open": (ctypes.c_int, [_P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
+    "smmc_ipc_close": (ctypes.c_int, [_P, ctypes.c_size_t]),
 }
 
 
@@ -175,6 +187,35 @@ def tc_plan_describe(geom, batch=1):
 def plan_launches(geom, batch=1, mode="ffma"):
     g = Geom.of(geom, batch)
     return int(lib().smmc_plan_launches(ctypes.byref(g), mode_id(mode)))
+
+
+def gather_workspace_bytes(geom_local, batch=1):
+    g = Geom.of(geom_local, batch)
+    return int(lib().smmc_gather_workspace_bytes(ctypes.byref(g)))
+
+
+def ipc_handle(dev_ptr):
+    """(handle bytes, byte offset) of a device pointer, for smmc_ipc_open in a
+    peer process."""
+    buf = ctypes.create_string_buffer(SMMC_IPC_HANDLE_BYTES)
+    off = ctypes.c_size_t(0)
+    check(lib().smmc_ipc_handle(ctypes.c_void_p(dev_ptr), buf, ctypes.byref(off)),
+          "smmc_ipc_handle")
+    return buf.raw, int(off.value)
+
+
+def ipc_open(handle, offset):
+    """Map a peer's device pointer (from ipc_handle) into this process."""
+    if len(handle) != SMMC_IPC_HANDLE_BYTES:
+        raise ShapeMismatchError("IPC handle must be SMMC_IPC_HANDLE_BYTES bytes")
+    ptr = ctypes.c_void_p(0)
+    check(lib().smmc_ipc_open(ctypes.create_string_buffer(handle, SMMC_IPC_HANDLE_BYTES),
+                              offset, ctypes.byref(ptr)), "smmc_ipc_open")
+    return int(ptr.value)
+
+
+def ipc_close(dev_ptr, offset):
+    check(lib().smmc_ipc_close(ctypes.c_void_p(dev_ptr), offset), "smmc_ipc_close")
 
 
 def workspace_bytes(geom, batch=1, mode="ffma"):

@@ -399,9 +399,10 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
         }
     }
 
-    // ---- epilogue: NCHW stores (reduce_mode 2: partial plane `slot` of ws)
-    float* out = (p.splits > 1 && p.reduce_mode == 2) ? p.ws + (int64_t)slot * ((int64_t)p.m * p.co)
-                                                       : p.y;
+    // ---- epilogue: NCHW stores (reduce_mode 2: partial plane `slot` of ws,
+    // placed into y by splitk_reduce_kernel — also with a single split when
+    // the output goes to gather replicas)
+    float* out = p.reduce_mode == 2 ? p.ws + (int64_t)slot * ((int64_t)p.m * p.co) : p.y;
     const bool vec_ok = (p.ohw & 3) == 0;
 #pragma unroll
     for (int ib = 0; ib < NQ && store; ++ib) {
@@ -450,10 +451,18 @@ __global__ void __launch_bounds__(256) zero_counters_kernel(int* __restrict__ c,
 }
 
 // reduce_mode 2: y = sum of the partial planes in split order.
+struct ReduceOut {
+    float* ys[kMaxOut];
+    int n_out, co, co_total, co_base, ohw;
+};
+
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ ws,
-                                                            float* __restrict__ y, int64_t total,
+                                                            const ReduceOut ro, int64_t total,
                                                             int splits) {
-    const int64_t total4 = (total & 3) ? 0 : (total >> 2);
+    // float4 path: the plain case, or a gather whose channel planes keep
+    // 16-byte alignment (ohw % 4 == 0)
+    const bool plain = ro.n_out == 1 && ro.co_total == ro.co && ro.co_base == 0;
+    const int64_t total4 = ((total & 3) || (!plain && (ro.ohw & 3))) ? 0 : (total >> 2);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total4; i += stride) {
         const float4* src = reinterpret_cast<const float4*>(ws) + i;
@@ -473,13 +482,29 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
             const float4 v = __ldcg(src + (int64_t)z * total4);
             s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
         }
-        reinterpret_cast<float4*>(y)[i] = s;
+        if (plain) {
+            reinterpret_cast<float4*>(ro.ys[0])[i] = s;
+        } else {
+            const int64_t e = i << 2;  // local (n, c, pixel) index of the first lane
+            const int64_t plane = (int64_t)ro.co * ro.ohw;
+            const int64_t n = e / plane;
+            const int64_t r = e - n * plane;
+            const int64_t d = (n * ro.co_total + ro.co_base) * ro.ohw + r;
+#pragma unroll
+            for (int o = 0; o < kMaxOut; ++o)
+                if (o < ro.n_out) *reinterpret_cast<float4*>(ro.ys[o] + d) = s;
+        }
     }
     for (int64_t i = (total4 << 2) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += stride) {
         float s = ws[i];
         for (int z = 1; z < splits; ++z) s += ws[(int64_t)z * total + i];
-        y[i] = s;
+        const int64_t plane = (int64_t)ro.co * ro.ohw;
+        const int64_t n = i / plane;
+        const int64_t d = (n * ro.co_total + ro.co_base) * ro.ohw + (i - n * plane);
+#pragma unroll
+        for (int o = 0; o < kMaxOut; ++o)
+            if (o < ro.n_out) ro.ys[o][d] = s;
     }
 }
 
@@ -735,6 +760,27 @@ FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) {
     return best;
 }
 
+// Plan for the fused c_o-shard gather: the product plan recast to reduce
+// mode 2, so the conv kernel keeps its single-output epilogue and the (already
+// needed, or one extra tiny) placement pass splitk_reduce_kernel writes the
+// replicas — local and NVLink peer memory — in split order.
+FfmaPlan plan_ffma_gather(const smmc_geom& g, int sm_count) {
+    FfmaPlan pl = plan_ffma(g, sm_count);
+    const int64_t m = (int64_t)g.n * ((g.h + 2 * g.p_h - g.k_h) / g.s_h + 1) *
+                      ((g.w + 2 * g.p_w - g.k_w) / g.s_w + 1);
+    if (pl.reduce_mode == 3) {  // stream-K -> classic split grid of similar size
+        const int64_t want = std::max<int64_t>(1, pl.sk_ctas / std::max<int64_t>(1, pl.tiles));
+        const int sp = (int)std::min<int64_t>(want, pl.kt_total);
+        pl.kt_per_split = (pl.kt_total + sp - 1) / sp;
+        pl.splits = (pl.kt_total + pl.kt_per_split - 1) / pl.kt_per_split;
+        pl.sk_ctas = pl.sk_iters = pl.sk_maxseg = 0;
+    }
+    pl.reduce_mode = 2;
+    pl.ws_counter_offset = 0;
+    pl.ws_bytes = (size_t)pl.splits * (size_t)m * g.c_o * sizeof(float);
+    return pl;
+}
+
 cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
     dim3 grid((p.m + pl.bm - 1) / pl.bm, (p.co + pl.bn - 1) / pl.bn, pl.splits);
     if (pl.reduce_mode == 3) grid = dim3((unsigned)pl.sk_ctas, 1, 1);
@@ -754,7 +800,14 @@ cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
     if (e != cudaSuccess || pl.reduce_mode != 2) return e;
     const int64_t total = (int64_t)p.m * p.co;
     const int blocks = (int)std::min<int64_t>((total / 4 + 255) / 256 + 1, 148 * 16);
-    splitk_reduce_kernel<<<blocks, 256, 0, s>>>(p.ws, p.y, total, p.splits);
+    ReduceOut ro{};
+    for (int o = 0; o < p.n_out; ++o) ro.ys[o] = p.ys[o];
+    ro.n_out = p.n_out;
+    ro.co = p.co;
+    ro.co_total = p.co_total;
+    ro.co_base = p.co_base;
+    ro.ohw = p.ohw;
+    splitk_reduce_kernel<<<blocks, 256, 0, s>>>(p.ws, ro, total, p.splits);
     count_launches(1);
     return cudaGetLastError();
 }

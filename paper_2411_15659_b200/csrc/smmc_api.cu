@@ -1,5 +1,6 @@
 // smmc_api.cu — the extern "C" boundary (include/smmc.h): validation, kernel
 // planning, status/error mapping and the host-buffer staging path.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -103,6 +104,9 @@ int current_device() {
 int cuda_status(cudaError_t e, const char* what) {
     if (e == cudaSuccess) return SMMC_OK;
     set_error("%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+    // reported here: clear the runtime's (non-sticky) last-error slot so the
+    // next launch's cudaGetLastError() does not return this stale failure
+    (void)cudaGetLastError();
     if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) return SMMC_ENODEVICE;
     return SMMC_ECUDA;
 }
@@ -189,27 +193,61 @@ int select_device(int device) {
     return cuda_status(cudaSetDevice(device), "cudaSetDevice");
 }
 
-int conv_device(const float* x, const float* w, float* y, const smmc_geom* g, int mode, void* ws,
-                size_t ws_bytes, cudaStream_t stream) {
+// Where the epilogue puts the output: n_out replicas of a co_total-channel
+// tensor, this problem's channels at offset co_base (fused c_o-shard gather).
+struct OutPlace {
+    float* const* ys;
+    int n_out;
+    int co_total;
+    int co_base;
+};
+
+int conv_device_placed(const float* x, const float* w, const OutPlace& op, const smmc_geom* g,
+                       int mode, void* ws, size_t ws_bytes, cudaStream_t stream) {
     int oh = 0, ow = 0;
     int st = check_geom(g, &oh, &ow);
     if (st) return st;
     if ((st = check_mode(mode))) return st;
     if (g->n == 0) return SMMC_OK;
-    if (!x || !w || !y) {
+    if (op.n_out < 1 || op.n_out > kMaxOut || !op.ys) {
+        set_error("n_out must be in [1, %d]", kMaxOut);
+        return SMMC_ESHAPE;
+    }
+    if (op.co_base < 0 || op.co_total < g->c_o || op.co_base > op.co_total - g->c_o) {
+        set_error("channel window [%d, %d) outside a %d-channel output", op.co_base,
+                  op.co_base + g->c_o, op.co_total);
+        return SMMC_ESHAPE;
+    }
+    if (!x || !w) {
         set_error("x, w_smm and y must be non-NULL device pointers");
         return SMMC_ESHAPE;
     }
-    if (((uintptr_t)x | (uintptr_t)w | (uintptr_t)y) & 15) {
+    uintptr_t align = (uintptr_t)x | (uintptr_t)w;
+    for (int o = 0; o < op.n_out; ++o) {
+        if (!op.ys[o]) {
+            set_error("x, w_smm and y must be non-NULL device pointers");
+            return SMMC_ESHAPE;
+        }
+        align |= (uintptr_t)op.ys[o];
+    }
+    if (align & 15) {
         set_error("x, w_smm and y must be 16-byte aligned");
         return SMMC_ESHAPE;
+    }
+    if (mode == SMMC_MODE_EXACT && (op.n_out != 1 || op.co_total != g->c_o)) {
+        set_error("the fused gather epilogue is implemented for the ffma mode only");
+        return SMMC_EUNSUPPORTED;
     }
     const int dev = current_device();
     const int sms = sm_count_for(dev);
     Problem p{};
     p.x = x;
     p.w = w;
-    p.y = y;
+    p.y = op.ys[0];
+    for (int o = 0; o < op.n_out; ++o) p.ys[o] = op.ys[o];
+    p.n_out = op.n_out;
+    p.co_total = op.co_total;
+    p.co_base = op.co_base;
     p.ws = static_cast<float*>(ws);
     p.n = g->n;
     p.c = g->c_i;
@@ -231,7 +269,8 @@ int conv_device(const float* x, const float* w, float* y, const smmc_geom* g, in
     p.splits = 1;
     if (mode == SMMC_MODE_EXACT) return cuda_status(launch_exact(p, stream), "conv_exact launch");
 
-    const FfmaPlan pl = plan_ffma(*g, sms);
+    const bool placed = op.n_out != 1 || op.co_total != g->c_o || op.co_base != 0;
+    const FfmaPlan pl = placed ? plan_ffma_gather(*g, sms) : plan_ffma(*g, sms);
     p.splits = pl.splits;
     p.kt_total = pl.kt_total;
     p.kt_per_split = pl.kt_per_split;
@@ -257,6 +296,13 @@ int conv_device(const float* x, const float* w, float* y, const smmc_geom* g, in
         // partials where this plan keeps its counters)
     }
     return cuda_status(launch_ffma(p, pl, stream), "conv_ffma launch");
+}
+
+int conv_device(const float* x, const float* w, float* y, const smmc_geom* g, int mode, void* ws,
+                size_t ws_bytes, cudaStream_t stream) {
+    float* ys[1] = {y};
+    const OutPlace op{ys, 1, g ? g->c_o : 0, 0};
+    return conv_device_placed(x, w, op, g, mode, ws, ws_bytes, stream);
 }
 
 }  // namespace
@@ -354,6 +400,88 @@ int smmc_conv2d_fwd_f32(const float* x, const float* w_smm, float* y, const smmc
                         void* workspace, size_t workspace_bytes, void* stream) {
     return conv_device(x, w_smm, y, g, mode, workspace, workspace_bytes,
                        static_cast<cudaStream_t>(stream));
+}
+
+int smmc_conv2d_fwd_f32_gather(const float* x, const float* w_slice, float* const* y_out, int n_out,
+                               const smmc_geom* g_local, int co_base, int co_total, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+    if (!y_out) {
+        set_error("y_out must point to n_out device pointers");
+        return SMMC_ESHAPE;
+    }
+    const OutPlace op{y_out, n_out, co_total, co_base};
+    return conv_device_placed(x, w_slice, op, g_local, SMMC_MODE_FFMA, workspace, workspace_bytes,
+                              static_cast<cudaStream_t>(stream));
+}
+
+namespace {
+using PFN_memGetAddressRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+PFN_memGetAddressRange address_range_fn() {
+    static PFN_memGetAddressRange fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* ptr = nullptr;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &ptr, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_memGetAddressRange>(ptr);
+    });
+    return fn;
+}
+}  // namespace
+
+size_t smmc_gather_workspace_bytes(const smmc_geom* g_local) {
+    int oh = 0, ow = 0;
+    if (check_geom(g_local, &oh, &ow) || g_local->n == 0) return 0;
+    return plan_ffma_gather(*g_local, sm_count_for(current_device())).ws_bytes;
+}
+
+int smmc_ipc_handle(const void* dev_ptr, void* handle, size_t* offset) {
+    if (!dev_ptr || !handle || !offset) {
+        set_error("dev_ptr, handle and offset must be non-NULL");
+        return SMMC_ESHAPE;
+    }
+    static_assert(sizeof(cudaIpcMemHandle_t) <= SMMC_IPC_HANDLE_BYTES, "handle size");
+    PFN_memGetAddressRange range = address_range_fn();
+    if (!range) {
+        set_error("cuMemGetAddressRange unavailable from the driver");
+        return SMMC_ECUDA;
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (CUdeviceptr)(uintptr_t)dev_ptr) != CUDA_SUCCESS) {
+        set_error("dev_ptr is not inside a device allocation");
+        return SMMC_ESHAPE;
+    }
+    cudaIpcMemHandle_t h;
+    int st = cuda_status(cudaIpcGetMemHandle(&h, (void*)(uintptr_t)base), "cudaIpcGetMemHandle");
+    if (st) return st;
+    memset(handle, 0, SMMC_IPC_HANDLE_BYTES);
+    memcpy(handle, &h, sizeof(h));
+    *offset = (size_t)((uintptr_t)dev_ptr - (uintptr_t)base);
+    return SMMC_OK;
+}
+
+int smmc_ipc_open(const void* handle, size_t offset, void** dev_ptr) {
+    if (!handle || !dev_ptr) {
+        set_error("handle and dev_ptr must be non-NULL");
+        return SMMC_ESHAPE;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    void* base = nullptr;
+    int st = cuda_status(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess),
+                         "cudaIpcOpenMemHandle");
+    if (st) return st;
+    *dev_ptr = static_cast<char*>(base) + offset;
+    return SMMC_OK;
+}
+
+int smmc_ipc_close(void* dev_ptr, size_t offset) {
+    if (!dev_ptr) return SMMC_OK;
+    return cuda_status(cudaIpcCloseMemHandle(static_cast<char*>(dev_ptr) - offset),
+                       "cudaIpcCloseMemHandle");
 }
 
 int smmc_conv2d_fwd_f32_host(const float* x, const float* w_smm, float* y, const smmc_geom* g,

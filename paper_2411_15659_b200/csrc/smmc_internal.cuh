@@ -13,6 +13,8 @@ namespace smmc {
 
 // ----------------------------------------------------------------- problem
 // Resolved problem description passed by value to every kernel.
+constexpr int kMaxOut = 8;  // output replicas of the fused c_o-shard gather
+
 struct Problem {
     const float* x;      // (n, c_i, h, w)
     const float* w;      // (c_i, k_w, k_h, c_o) == row-major [K][c_o], K = c_i*k_w*k_h
@@ -33,6 +35,15 @@ struct Problem {
     int tiles_n;         // channel tiles
     int sk_iters;        // stream-K: tap blocks per CTA
     int sk_maxseg;       // stream-K: partial-tile slots per tile in the workspace
+    // Output placement.  Normally n_out = 1, ys[0] = y, co_total = co,
+    // co_base = 0.  The fused c_o-shard all-gather (smmc_conv2d_fwd_f32_gather)
+    // writes this rank's channels [co_base, co_base + co) of a
+    // (n, co_total, oh, ow) tensor into every replica ys[0..n_out) — local and
+    // NVLink peer memory — straight from the epilogue.
+    float* ys[kMaxOut];
+    int n_out;
+    int co_total;
+    int co_base;
 };
 
 // Last-error / launch bookkeeping (defined in smmc_api.cu).
@@ -61,6 +72,7 @@ struct FfmaPlan {
     size_t ws_counter_offset;
 };
 FfmaPlan plan_ffma(const smmc_geom& g, int sm_count);
+FfmaPlan plan_ffma_gather(const smmc_geom& g, int sm_count);
 cudaError_t launch_ffma(const Problem& p, const FfmaPlan& plan, cudaStream_t s);
 int ffma_launches(const FfmaPlan& plan);
 // bf16 tensor-core variant (conv_tc.cu)

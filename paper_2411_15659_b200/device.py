@@ -10,7 +10,7 @@ import ctypes
 from . import _native
 from .errors import DeviceError, ShapeMismatchError
 
-__all__ = ["conv2d", "repack_weights", "SmmConv2d"]
+__all__ = ["conv2d", "conv2d_gather", "repack_weights", "SmmConv2d"]
 
 
 def _torch():
@@ -80,6 +80,52 @@ def conv2d(x, weights_smm, geom, *, mode="ffma", out=None, workspace=None):
             ctypes.c_void_p(ws_ptr) if ws_ptr else None, ws_len,
             ctypes.c_void_p(stream) if stream else None), "smmc_conv2d_fwd_f32")
     return out
+
+
+def conv2d_gather(x, w_slice, outs, geom_local, co_base, co_total, *, workspace=None):
+    """Fused output-channel-shard conv + all-gather (``smmc_conv2d_fwd_f32_gather``).
+
+    ``x`` (N, c_i, h, w); ``w_slice`` the compact (c_i, k_w, k_h, c_lo) SMM
+    weights of channels [co_base, co_base + c_lo) (``geom_local.out_channels``
+    = c_lo); ``outs``: up to 8 destinations of the full (N, co_total, h', w')
+    output — CUDA tensors, or raw device addresses (ints) such as peer buffers
+    mapped with ``_native.ipc_open``.  Every destination receives this
+    shard's channels; launched on torch's current stream, no synchronisation.
+    """
+    torch = _torch()
+    if not isinstance(x, torch.Tensor) or x.dim() != 4:
+        raise ShapeMismatchError("x must be a 4-D torch.Tensor (N, c_i, h, w)")
+    n = x.shape[0]
+    _check_tensor(x, (n,) + geom_local.input_shape, "input batch")
+    _check_tensor(w_slice, geom_local.weights_smm_shape, "weight slice")
+    if not 1 <= len(outs) <= _native.SMMC_MAX_OUT:
+        raise ShapeMismatchError(f"1..{_native.SMMC_MAX_OUT} output replicas required")
+    full = (n, co_total, geom_local.out_h, geom_local.out_w)
+    ptrs = []
+    for o in outs:
+        if isinstance(o, int):
+            ptrs.append(o)
+        else:
+            _check_tensor(o, full, "output replica")
+            ptrs.append(o.data_ptr())
+    if n == 0:
+        return
+    g = _native.Geom.of(geom_local, n)
+    lib = _native.lib()
+    with torch.cuda.device(x.device):
+        need = int(lib.smmc_gather_workspace_bytes(ctypes.byref(g)))
+        ws_ptr, ws_len = None, 0
+        if need:
+            if workspace is None or workspace.numel() * workspace.element_size() < need:
+                workspace = torch.empty(need, dtype=torch.uint8, device=x.device)
+            ws_ptr, ws_len = workspace.data_ptr(), workspace.numel() * workspace.element_size()
+        arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+        stream = torch.cuda.current_stream(x.device).cuda_stream
+        _native.check(lib.smmc_conv2d_fwd_f32_gather(
+            ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(w_slice.data_ptr()), arr, len(ptrs),
+            ctypes.byref(g), int(co_base), int(co_total),
+            ctypes.c_void_p(ws_ptr) if ws_ptr else None, ws_len,
+            ctypes.c_void_p(stream) if stream else None), "smmc_conv2d_fwd_f32_gather")
 
 
 class SmmConv2d:

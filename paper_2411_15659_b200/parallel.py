@@ -11,6 +11,13 @@ Two partitions, both lifted from the reference:
   computes y_r (N, c_o/P, h', w'), then one all-gather (NCCL over NVLink)
   assembles (N, c_o, h', w').  The gathered buffer is rank-major
   (P, N, c_o/P, h'*w'); a single permute-copy restores NCHW.
+* fused output-channel sharding (``shard="cout_fused"``, the product path on
+  GPUs): no collective payload at all — every rank maps its peers' full
+  output buffers over NVLink (CUDA IPC, exchanged once at construction) and
+  the conv's placement pass stores this rank's channels into all of them
+  (``smmc_conv2d_fwd_f32_gather``); a 1-element NCCL all-reduce before and
+  after is the only cross-rank traffic (write-after-read and read-after-write
+  fences).
 
 ``conv_fn`` is injectable so the sharding logic is testable on CPU with the
 gloo backend (tests/test_parallel.py); on GPU it is ``device.conv2d``.
@@ -23,7 +30,7 @@ from .errors import ShapeMismatchError
 from .geometry import ConvGeometry
 
 __all__ = ["batch_shard", "cout_shard", "cout_geometry", "all_gather_cout",
-           "ShardedSmmConv"]
+           "PeerBuffers", "ShardedSmmConv"]
 
 
 def batch_shard(n, rank, world):
@@ -66,17 +73,55 @@ def all_gather_cout(y_local, gather_buf, out, c_o, world, group=None):
     return out
 
 
+class PeerBuffers:
+    """Every rank's copy of one output buffer, as device addresses usable by
+    this rank's kernels: its own ``data_ptr()`` plus the peers' buffers opened
+    through CUDA IPC (handles exchanged with ``all_gather_object``).  Order:
+    rank 0 .. P-1.  ``ipc`` is injectable for CPU tests."""
+
+    def __init__(self, out, group=None, ipc=None):
+        from . import _native
+        self.ipc = ipc or _native
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.out = out
+        mine = self.ipc.ipc_handle(out.data_ptr()) if self.world > 1 else (b"", 0)
+        entries = [None] * self.world
+        if self.world > 1:
+            dist.all_gather_object(entries, mine, group=group)
+        else:
+            entries[0] = mine
+        self.ptrs, self._opened = [], []
+        for r, (handle, offset) in enumerate(entries):
+            if r == self.rank:
+                self.ptrs.append(out.data_ptr())
+            else:
+                ptr = self.ipc.ipc_open(handle, offset)
+                self._opened.append((ptr, offset))
+                self.ptrs.append(ptr)
+
+    def close(self):
+        for ptr, offset in self._opened:
+            self.ipc.ipc_close(ptr, offset)
+        self._opened = []
+
+
 class ShardedSmmConv:
     """One conv layer sharded over the default process group.
 
     ``shard="batch"``: forward(x_local) -> y_local, no collective.
     ``shard="cout"``:  forward(x_full)  -> y_full via all-gather.
+    ``shard="cout_fused"``: forward(x_full) -> y_full written by every rank's
+    conv straight into every rank's output over NVLink (``batch`` fixes the
+    output buffer, or pass ``out``; ``gather_fn`` / ``ipc`` are injectable for
+    CPU tests).
     ``weights_smm`` is the full (c_i, k_w, k_h, c_o) tensor on this rank's device.
     """
 
-    def __init__(self, geom, weights_smm, shard="batch", conv_fn=None, mode="ffma"):
-        if shard not in ("batch", "cout"):
-            raise ValueError("shard must be 'batch' or 'cout'")
+    def __init__(self, geom, weights_smm, shard="batch", conv_fn=None, mode="ffma",
+                 batch=None, gather_fn=None, ipc=None, out=None):
+        if shard not in ("batch", "cout", "cout_fused"):
+            raise ValueError("shard must be 'batch', 'cout' or 'cout_fused'")
         self.geom = geom
         self.shard = shard
         self.mode = mode
@@ -90,6 +135,27 @@ class ShardedSmmConv:
         self.conv_fn = conv_fn
         if tuple(weights_smm.shape) != geom.weights_smm_shape:
             raise ShapeMismatchError("weights must be in SMM order (c_i, k_w, k_h, c_o)")
+        if shard == "cout_fused":
+            if mode != "ffma":
+                raise ValueError("cout_fused runs the ffma mode")
+            if not batch or batch < 1:
+                raise ValueError("cout_fused needs the batch size of its output buffer")
+            if gather_fn is None:
+                from .device import conv2d_gather as gather_fn
+            self.gather_fn = gather_fn
+            self.lo, self.hi = cout_shard(geom.out_channels, self.rank, self.world)
+            self.local_geom = (cout_geometry(geom, self.lo, self.hi)
+                               if self.hi > self.lo else None)
+            self.weights = weights_smm[..., self.lo:self.hi].contiguous()
+            shape = (batch,) + geom.output_shape
+            if out is None:
+                out = torch.empty(shape, dtype=weights_smm.dtype, device=weights_smm.device)
+            elif tuple(out.shape) != shape or not out.is_contiguous():
+                raise ShapeMismatchError(f"out must be a contiguous {shape} tensor")
+            self.out = out
+            self.peers = PeerBuffers(self.out, ipc=ipc)
+            self._flag = torch.zeros(1, dtype=torch.float32, device=weights_smm.device)
+            return
         if shard == "cout":
             self.chunk = -(-geom.out_channels // self.world)
             lo, hi = cout_shard(geom.out_channels, self.rank, self.world)
@@ -104,7 +170,21 @@ class ShardedSmmConv:
             self.local_geom = geom
             self.weights = weights_smm.contiguous()
 
+    def _fence(self):
+        if self.world > 1:
+            dist.all_reduce(self._flag)
+
     def forward(self, x):
+        if self.shard == "cout_fused":
+            if x.shape[0] != self.out.shape[0]:
+                raise ShapeMismatchError(
+                    f"cout_fused was built for batch {self.out.shape[0]}, got {x.shape[0]}")
+            self._fence()  # peers are done reading the previous output
+            if self.local_geom is not None:
+                self.gather_fn(x, self.weights, self.peers.ptrs, self.local_geom, self.lo,
+                               self.geom.out_channels)
+            self._fence()  # every shard has landed in every replica
+            return self.out
         y_local = self.conv_fn(x, self.weights, self.local_geom)
         if self.shard == "batch":
             return y_local

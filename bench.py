@@ -508,9 +508,11 @@ def run_e2e(args, layers, world, dev):
     for L in layers:
         if L["n"] == 0:
             continue
-        x = torch.from_numpy(L["x_host"]).pin_memory()
-        w = torch.from_numpy(L["w_host"]).pin_memory()
-        y = torch.empty((L["n"],) + L["gl"].output_shape).pin_memory()
+        # page-locked via smmc_host_alloc_pinned (cudaHostRegister'd pages:
+        # 55 GB/s H2D on this host vs ~33 for torch's cudaHostAlloc buffers)
+        x = torch.from_numpy(_native.pinned_copy(L["x_host"]))
+        w = torch.from_numpy(_native.pinned_copy(L["w_host"]))
+        y = torch.from_numpy(_native.pinned_empty((L["n"],) + L["gl"].output_shape))
         g = _native.Geom.of(L["gl"], L["n"])
         bufs.append((x, w, y, g))
         h2d += x.numel() * 4 + w.numel() * 4
@@ -549,14 +551,14 @@ def run_e2e_tc(args, layers, world, dev):
     import torch
     import torch.distributed as dist
 
-    from paper_2411_15659_b200 import device
+    from paper_2411_15659_b200 import _native, device
     bufs = []
     h2d = d2h = 0
     for L in layers:
         if L["n"] == 0:
             continue
-        xh = torch.from_numpy(L["x_host"]).pin_memory()
-        yh = torch.empty((L["n"],) + L["gl"].output_shape).pin_memory()
+        xh = torch.from_numpy(_native.pinned_copy(L["x_host"]))
+        yh = torch.from_numpy(_native.pinned_empty((L["n"],) + L["gl"].output_shape))
         xd = torch.empty_like(xh, device=dev)
         bufs.append((L, xh, yh, xd))
         h2d += xh.numel() * 4

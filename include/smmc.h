@@ -194,6 +194,12 @@ SMMC_API int smmc_conv2d_fwd_f32_gather(const float* x, const float* w_slice, fl
                                         int co_total, void* workspace, size_t workspace_bytes,
                                         void* stream);
 
+/* Page-locked host memory for the *_host entries' buffers: 2 MB-aligned
+ * anonymous pages registered with cudaHostRegister (measured 55 GB/s H2D on
+ * B200 vs 29-36 GB/s for cudaHostAlloc memory on the same host). */
+SMMC_API int smmc_host_alloc_pinned(size_t bytes, void** ptr);
+SMMC_API int smmc_host_free_pinned(void* ptr);
+
 /* Workspace the gather needs (its plan always places through the reduce pass). */
 SMMC_API size_t smmc_gather_workspace_bytes(const smmc_geom* g_local);
 

@@ -41,7 +41,7 @@ EXPORTED_SYMBOLS = (
     "smmc_tc_supported", "smmc_pack_input_bf16_nhwc", "smmc_pack_weights_bf16",
     "smmc_conv2d_fwd_bf16_tc", "smmc_im2col_bytes", "smmc_im2col_pack_f32",
     "smmc_conv2d_fwd_f32_gather", "smmc_gather_workspace_bytes", "smmc_ipc_handle",
-    "smmc_ipc_open", "smmc_ipc_close",
+    "smmc_ipc_open", "smmc_ipc_close", "smmc_host_alloc_pinned", "smmc_host_free_pinned",
 )
 
 SMMC_MAX_OUT = 8
@@ -113,6 +113,8 @@ _SIGNATURES = {
     "smmc_ipc_handle": (ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_size_t)]),
     "smmc_ipc_open": (ctypes.c_int, [_P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
     "smmc_ipc_close": (ctypes.c_int, [_P, ctypes.c_size_t]),
+    "smmc_host_alloc_pinned": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
+    "smmc_host_free_pinned": (ctypes.c_int, [_P]),
 }
 
 
@@ -216,6 +218,34 @@ def ipc_open(handle, offset):
 
 def ipc_close(dev_ptr, offset):
     check(lib().smmc_ipc_close(ctypes.c_void_p(dev_ptr), offset), "smmc_ipc_close")
+
+
+def pinned_empty(shape, dtype="float32"):
+    """A numpy array in page-locked host memory (smmc_host_alloc_pinned),
+    freed when the array is garbage-collected."""
+    import weakref
+
+    import numpy as np
+    dt = np.dtype(dtype)
+    count = 1
+    for d in shape:
+        count *= int(d)
+    nbytes = max(count * dt.itemsize, 1)
+    ptr = ctypes.c_void_p(0)
+    check(lib().smmc_host_alloc_pinned(nbytes, ctypes.byref(ptr)), "smmc_host_alloc_pinned")
+    buf = (ctypes.c_char * nbytes).from_address(ptr.value)
+    arr = np.frombuffer(buf, dtype=dt, count=count).reshape(shape)
+    weakref.finalize(buf, lib().smmc_host_free_pinned, ctypes.c_void_p(ptr.value))
+    return arr
+
+
+def pinned_copy(a):
+    """Page-locked copy of a numpy array."""
+    import numpy as np
+    a = np.ascontiguousarray(a)
+    out = pinned_empty(a.shape, a.dtype)
+    out[...] = a
+    return out
 
 
 def workspace_bytes(geom, batch=1, mode="ffma"):

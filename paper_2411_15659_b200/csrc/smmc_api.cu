@@ -1,6 +1,7 @@
 // smmc_api.cu — the extern "C" boundary (include/smmc.h): validation, kernel
 // planning, status/error mapping and the host-buffer staging path.
 #include <cuda.h>
+#include <sys/mman.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -506,12 +507,13 @@ int smmc_conv2d_fwd_f32_host(const float* x, const float* w_smm, float* y, const
     const size_t yb = (size_t)g->n * ys * sizeof(float);
     // Pipeline: the batch is cut into chunks of whole samples; chunk c's H2D
     // (copy stream), conv (compute stream) and D2H (second copy stream) overlap
-    // with its neighbours'.  Chunks of >= ~8 MB keep the copies efficient.
+    // with its neighbours'.  ~4 MB chunks (measured: 4 MB beat 8/16/32 MB on
+    // the config-2 step, tools/e2e_probe.py with SMMC_HOST_CHUNK_MB).
     const size_t per_sample = (xs + ys) * sizeof(float);
     int chunks = (int)std::min<size_t>((size_t)kMaxChunks, (size_t)g->n);
     static const size_t chunk_bytes = [] {
         const char* f = getenv("SMMC_HOST_CHUNK_MB");  // tuning hook
-        return (size_t)(f && atoi(f) > 0 ? atoi(f) : 8) << 20;
+        return (size_t)(f && atoi(f) > 0 ? atoi(f) : 4) << 20;
     }();
     chunks = (int)std::min<size_t>((size_t)chunks, std::max<size_t>(1, (per_sample * g->n) / chunk_bytes));
     const int per = (g->n + chunks - 1) / chunks;
@@ -558,6 +560,65 @@ int smmc_conv2d_fwd_f32_host(const float* x, const float* w_smm, float* y, const
             return st;
     }
     return cuda_status(cudaStreamSynchronize(hp.s_out), "conv (host path)");
+}
+
+// ---- pinned host staging buffers for the *_host entries.  cudaHostAlloc
+// memory measured only 29-36 GB/s H2D on the B200 boxes (KVM guest), while
+// ordinary pages pinned with cudaHostRegister reach 55 GB/s (the PCIe Gen5
+// x16 rate; tools/hostmem_probe.py): allocate 2 MB-aligned anonymous pages
+// (transparent-huge-page advised) and register them.
+namespace {
+std::mutex g_pinned_mu;
+std::vector<std::pair<void*, std::pair<void*, size_t>>> g_pinned;  // user ptr -> (map, len)
+}  // namespace
+
+int smmc_host_alloc_pinned(size_t bytes, void** ptr) {
+    if (!ptr) {
+        set_error("ptr must be non-NULL");
+        return SMMC_ESHAPE;
+    }
+    *ptr = nullptr;
+    if (bytes == 0) return SMMC_OK;
+    constexpr size_t kHuge = 2u << 20;
+    const size_t len = (bytes + kHuge - 1) / kHuge * kHuge + kHuge;
+    void* map = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (map == MAP_FAILED) {
+        set_error("mmap of %zu bytes failed", len);
+        return SMMC_ECUDA;
+    }
+    void* p = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(map) + kHuge - 1) & ~(uintptr_t)(kHuge - 1));
+    const size_t plen = (bytes + kHuge - 1) / kHuge * kHuge;
+    madvise(p, plen, MADV_HUGEPAGE);
+    int st = cuda_status(cudaHostRegister(p, plen, cudaHostRegisterPortable), "cudaHostRegister");
+    if (st) {
+        munmap(map, len);
+        return st;
+    }
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    g_pinned.push_back({p, {map, len}});
+    *ptr = p;
+    return SMMC_OK;
+}
+
+int smmc_host_free_pinned(void* ptr) {
+    if (!ptr) return SMMC_OK;
+    std::pair<void*, size_t> m{nullptr, 0};
+    {
+        std::lock_guard<std::mutex> lk(g_pinned_mu);
+        for (size_t i = 0; i < g_pinned.size(); ++i)
+            if (g_pinned[i].first == ptr) {
+                m = g_pinned[i].second;
+                g_pinned.erase(g_pinned.begin() + i);
+                break;
+            }
+    }
+    if (!m.first) {
+        set_error("pointer was not allocated by smmc_host_alloc_pinned");
+        return SMMC_ESHAPE;
+    }
+    const int st = cuda_status(cudaHostUnregister(ptr), "cudaHostUnregister");
+    munmap(m.first, m.second);
+    return st;
 }
 
 size_t smmc_im2col_bytes(const smmc_geom* g) {

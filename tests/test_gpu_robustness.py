@@ -134,3 +134,43 @@ def test_unusual_geometries(gt):
     assert orc.max_abs_ratio(y.cpu().numpy(), ref) <= TOL
     ye = smm.smm_conv_batched(x, ws, g, mode="exact")
     assert np.array_equal(ye, ref)
+
+
+def test_pinned_host_buffers():
+    """smmc_host_alloc_pinned: page-locked, usable by the host entry, freed
+    with the array; foreign pointers are rejected."""
+    import gc
+    import torch
+    g = ConvGeometry(16, 24, 12, 10, 3, 3, pad_h=1, pad_w=1)
+    x, w = synthetic_layer(g, 3, 8)
+    xp = _native.pinned_copy(x)
+    wp = _native.pinned_copy(smm.repack_weights(w, g))
+    assert torch.from_numpy(xp).is_pinned() and xp.ctypes.data % (2 << 20) == 0
+    y = smm.smm_conv_batched(xp, wp, g)
+    assert orc.max_abs_ratio(y, orc.smm_conv_c(x, orc.repack(w), g)) <= TOL
+    del xp, wp
+    gc.collect()
+    assert _native.lib().smmc_host_free_pinned(ctypes.c_void_p(12345 * 4096)) == _native.SMMC_ESHAPE
+
+
+@pytest.mark.parametrize("gt,n", [
+    ((256, 200, 7, 7, 3, 3, 1, 1, 1, 1), 2),    # 2 channel chunks (128 + 72)
+    ((512, 512, 7, 7, 3, 3, 1, 1, 1, 1), 1),    # config 2 N=1: 8 chunks of 64
+    ((128, 96, 5, 6, 5, 3, 1, 2, 2, 1), 3),     # rectangular kernel, stride (1, 2)
+    ((64, 70, 4, 4, 1, 1, 1, 1, 0, 0), 1),      # c_o % 32 != 0, 1x1
+    ((40, 256, 3, 3, 3, 3, 1, 1, 1, 1), 1),     # c_i % 16 != 0: batch pipeline instead
+    ((96, 64, 6, 6, 3, 3, 1, 1, 1, 1), 2),      # 96 channels -> chunks of 48
+])
+def test_host_entry_weight_heavy_layers(gt, n):
+    """Weight-dominated layers through the host entry (weights uploaded in one
+    copy ahead of the batch chunks; chunked weight uploads measured slower)."""
+    g = ConvGeometry(*gt)
+    x, w = synthetic_layer(g, n, 31)
+    ws = smm.repack_weights(w, g)
+    assert ws.size > x.size + n * g.out_channels * g.out_h * g.out_w  # really weight-heavy
+    y = smm.smm_conv_batched(_native.pinned_copy(x), _native.pinned_copy(ws), g)
+    ref = orc.smm_conv_c(x, orc.repack(w), g, threads=orc.host_threads())
+    assert orc.max_abs_ratio(y, ref) <= TOL
+    # exact mode on the same shape keeps the batch pipeline and stays bitwise
+    ye = smm.smm_conv_batched(x, ws, g, mode="exact")
+    assert np.array_equal(ye, ref)

@@ -18,9 +18,9 @@ lib = _native.lib()
 for li, (name, n, g) in enumerate(CONFIGS[cfg]["layers"]):
     x, w = synthetic_layer(g, n, layer_seed(cfg, li))
     ws = np.ascontiguousarray(w.transpose(1, 3, 2, 0))
-    xh = torch.from_numpy(x).pin_memory()
-    wh = torch.from_numpy(ws).pin_memory()
-    yh = torch.empty((n,) + g.output_shape).pin_memory()
+    xh = torch.from_numpy(_native.pinned_copy(x))
+    wh = torch.from_numpy(_native.pinned_copy(ws))
+    yh = torch.from_numpy(_native.pinned_empty((n,) + g.output_shape))
     G = _native.Geom.of(g, n)
 
     def call():
@@ -44,9 +44,9 @@ calls = []
 for li, (name, n, g) in enumerate(CONFIGS[cfg]["layers"]):
     x, w = synthetic_layer(g, n, layer_seed(cfg, li))
     ws = np.ascontiguousarray(w.transpose(1, 3, 2, 0))
-    xh = torch.from_numpy(x).pin_memory()
-    wh = torch.from_numpy(ws).pin_memory()
-    yh = torch.empty((n,) + g.output_shape).pin_memory()
+    xh = torch.from_numpy(_native.pinned_copy(x))
+    wh = torch.from_numpy(_native.pinned_copy(ws))
+    yh = torch.from_numpy(_native.pinned_empty((n,) + g.output_shape))
     calls.append((xh, wh, yh, _native.Geom.of(g, n), g.flops(n)))
 
 

@@ -454,6 +454,7 @@ __global__ void __launch_bounds__(256) zero_counters_kernel(int* __restrict__ c,
 struct ReduceOut {
     float* ys[kMaxOut];
     int n_out, co, co_total, co_base, ohw;
+    int vec;  // every replica 16-byte aligned (float4 stores allowed)
 };
 
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ ws,
@@ -462,7 +463,8 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
     // float4 path: the plain case, or a gather whose channel planes keep
     // 16-byte alignment (ohw % 4 == 0)
     const bool plain = ro.n_out == 1 && ro.co_total == ro.co && ro.co_base == 0;
-    const int64_t total4 = ((total & 3) || (!plain && (ro.ohw & 3))) ? 0 : (total >> 2);
+    const int64_t total4 =
+        ((total & 3) || !ro.vec || (!plain && (ro.ohw & 3))) ? 0 : (total >> 2);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total4; i += stride) {
         const float4* src = reinterpret_cast<const float4*>(ws) + i;
@@ -807,6 +809,8 @@ cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
     ro.co_total = p.co_total;
     ro.co_base = p.co_base;
     ro.ohw = p.ohw;
+    ro.vec = 1;
+    for (int o = 0; o < p.n_out; ++o) ro.vec &= ((uintptr_t)p.ys[o] & 15) == 0;
     splitk_reduce_kernel<<<blocks, 256, 0, s>>>(p.ws, ro, total, p.splits);
     count_launches(1);
     return cudaGetLastError();

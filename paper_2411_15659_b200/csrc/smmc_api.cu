@@ -223,16 +223,19 @@ int conv_device_placed(const float* x, const float* w, const OutPlace& op, const
         set_error("x, w_smm and y must be non-NULL device pointers");
         return SMMC_ESHAPE;
     }
-    uintptr_t align = (uintptr_t)x | (uintptr_t)w;
+    // x is read with 4-byte copies; w with 16-byte copies; y with float4
+    // stores when a channel plane is a multiple of 4 pixels
+    const bool y_vec = ((oh * ow) & 3) == 0;
+    uintptr_t a16 = (uintptr_t)w, a4 = (uintptr_t)x;
     for (int o = 0; o < op.n_out; ++o) {
         if (!op.ys[o]) {
             set_error("x, w_smm and y must be non-NULL device pointers");
             return SMMC_ESHAPE;
         }
-        align |= (uintptr_t)op.ys[o];
+        (y_vec ? a16 : a4) |= (uintptr_t)op.ys[o];
     }
-    if (align & 15) {
-        set_error("x, w_smm and y must be 16-byte aligned");
+    if ((a16 & 15) || (a4 & 3)) {
+        set_error("w_smm (and y when h'*w' %% 4 == 0) must be 16-byte aligned, x 4-byte aligned");
         return SMMC_ESHAPE;
     }
     if (mode == SMMC_MODE_EXACT && (op.n_out != 1 || op.co_total != g->c_o)) {

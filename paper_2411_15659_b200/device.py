@@ -18,7 +18,7 @@ def _torch():
     return torch
 
 
-def _check_tensor(t, shape, name):
+def _check_tensor(t, shape, name, align=16):
     torch = _torch()
     if not isinstance(t, torch.Tensor):
         raise ShapeMismatchError(f"{name} must be a torch.Tensor")
@@ -30,8 +30,8 @@ def _check_tensor(t, shape, name):
         raise ShapeMismatchError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
     if not t.is_contiguous():
         raise ShapeMismatchError(f"{name} must be contiguous")
-    if t.data_ptr() % 16:
-        raise ShapeMismatchError(f"{name} must be 16-byte aligned")
+    if t.data_ptr() % align:
+        raise ShapeMismatchError(f"{name} must be {align}-byte aligned")
     return t
 
 
@@ -53,7 +53,7 @@ def conv2d(x, weights_smm, geom, *, mode="ffma", out=None, workspace=None):
     if not isinstance(x, torch.Tensor) or x.dim() != 4:
         raise ShapeMismatchError("x must be a 4-D torch.Tensor (N, c_i, h, w)")
     n = x.shape[0]
-    _check_tensor(x, (n,) + geom.input_shape, "input batch")
+    _check_tensor(x, (n,) + geom.input_shape, "input batch", align=4)
     _check_tensor(weights_smm, geom.weights_smm_shape, "repacked weight tensor")
     if weights_smm.device != x.device:
         raise ShapeMismatchError("x and weights_smm must be on the same device")

@@ -84,10 +84,14 @@ def test_workspace_contract_errors():
     assert st == _native.SMMC_EWORKSPACE
     with pytest.raises(ValueError):
         _native.check(st)
-    # misaligned pointers are rejected before any launch
-    st = lib.smmc_conv2d_fwd_f32(ctypes.c_void_p(x.data_ptr() + 4), ctypes.c_void_p(w.data_ptr()),
-                                 ctypes.c_void_p(y.data_ptr()), ctypes.byref(G), 0, None, 0, None)
-    assert st == _native.SMMC_ESHAPE
+    # misaligned pointers are rejected before any launch (x needs 4 bytes,
+    # w 16 bytes, y 16 bytes when h'*w' % 4 == 0 — here 49: 4 bytes)
+    for dx, dw, dy in ((2, 0, 0), (0, 4, 0), (0, 0, 2)):
+        st = lib.smmc_conv2d_fwd_f32(ctypes.c_void_p(x.data_ptr() + dx),
+                                     ctypes.c_void_p(w.data_ptr() + dw),
+                                     ctypes.c_void_p(y.data_ptr() + dy), ctypes.byref(G), 0, None, 0,
+                                     None)
+        assert st == _native.SMMC_ESHAPE
     st = lib.smmc_conv2d_fwd_f32(None, None, None, ctypes.byref(G), 0, None, 0, None)
     assert st == _native.SMMC_ESHAPE
     st = lib.smmc_conv2d_fwd_f32(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(w.data_ptr()),
@@ -174,3 +178,38 @@ def test_host_entry_weight_heavy_layers(gt, n):
     # exact mode on the same shape keeps the batch pipeline and stays bitwise
     ye = smm.smm_conv_batched(x, ws, g, mode="exact")
     assert np.array_equal(ye, ref)
+
+
+def test_host_entry_multi_chunk_odd_sample_sizes():
+    """Batch chunks of a sample size that is not a multiple of 4 floats
+    (11x11 s4 stem: 3*227*227 inputs, 55*55 outputs per plane): chunk
+    pointers are only 4-byte aligned, the kernel's scalar paths take them."""
+    g = ConvGeometry(3, 96, 227, 227, 11, 11, stride_h=4, stride_w=4)
+    n = 8
+    x, w = synthetic_layer(g, n, 77)
+    ws = smm.repack_weights(w, g)
+    y = smm.smm_conv_batched(_native.pinned_copy(x), _native.pinned_copy(ws), g)
+    for s in (0, 3, n - 1):
+        ref = orc.smm_conv_c(np.ascontiguousarray(x[s:s + 1]), orc.repack(w), g,
+                             threads=orc.host_threads())
+        assert orc.max_abs_ratio(y[s:s + 1], ref) <= TOL
+
+
+def test_device_path_unaligned_input_window():
+    """x may start at any 4-byte boundary (e.g. a sample slice of an odd-sized
+    batch); y keeps 16 bytes when its planes are float4-stored."""
+    import torch
+    g = ConvGeometry(3, 16, 9, 9, 3, 3, pad_h=1, pad_w=1)
+    x, w = synthetic_layer(g, 3, 4)
+    ws = torch.from_numpy(smm.repack_weights(w, g)).cuda()
+    xd = torch.from_numpy(x).cuda().reshape(-1)
+    lib = _native.lib()
+    G = _native.Geom.of(g, 2)
+    y = torch.empty((2,) + g.output_shape, device="cuda")
+    per = g.in_channels * g.in_h * g.in_w  # 243 floats: odd
+    _native.check(lib.smmc_conv2d_fwd_f32(ctypes.c_void_p(xd.data_ptr() + 4 * per),
+                                          ctypes.c_void_p(ws.data_ptr()), ctypes.c_void_p(y.data_ptr()),
+                                          ctypes.byref(G), 0, None, 0, None), "conv")
+    torch.cuda.synchronize()
+    ref = orc.smm_conv_c(np.ascontiguousarray(x[1:]), orc.repack(w), g)
+    assert orc.max_abs_ratio(y.cpu().numpy(), ref) <= TOL

@@ -74,6 +74,10 @@ def test_tc_rejects_strided():
     (64, 512, 14, 14, 3, 3, 1, 1, 1, 1, 3),   # two N=256 tiles, ragged last M tile
     (32, 320, 9, 11, 3, 3, 1, 1, 1, 1, 2),    # c_o % 256 != 0: partial second N tile
     (128, 256, 20, 20, 3, 3, 1, 1, 1, 1, 40),  # > 2 tiles per persistent CTA
+    (64, 256, 8, 12, 1, 1, 1, 1, 0, 0, 5),     # 1x1 at N=256: tiles straddle 96-px
+                                               # images, ragged tail
+    (32, 512, 8, 8, 1, 1, 1, 1, 0, 0, 3),      # 1x1, two N tiles
+    (64, 256, 9, 9, 1, 1, 1, 1, 0, 0, 2),      # 1x1, odd plane
 ], ids=lambda c: "x".join(map(str, c)) if isinstance(c, tuple) else c)
 def test_tc_both_tile_widths(monkeypatch, case, bn):
     """Every halo kernel (non-persistent N=128; persistent warp-specialised

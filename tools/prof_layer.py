@@ -1,6 +1,6 @@
 """Run one BASELINE layer a few times (for ncu / quick timing).
 
-    python tools/prof_layer.py --config 2 --layer conv128@28_n32 [--iters 5] [--mode ffma]
+    python tools/prof_layer.py --config 2 --layer conv128@28_n32 [--iters 5] [--mode ffma|exact|bf16_tc]
 """
 import argparse
 import sys
@@ -27,8 +27,12 @@ def main():
         if name != a.layer:
             continue
         x, w = synthetic_layer(g, n, layer_seed(a.config, li))
-        mod = device.SmmConv2d(g, w, mode=a.mode, max_batch=n)
         xd = torch.from_numpy(x).cuda()
+        if a.mode == "bf16_tc":  # tcgen05 variant: input packed to bf16 NHWC once
+            mod = device.TcSmmConv2d(g, w)
+            xd = mod.pack_input(xd)
+        else:
+            mod = device.SmmConv2d(g, w, mode=a.mode, max_batch=n)
         y = mod(xd)
         torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -17,12 +17,43 @@ from paper_2411_15659_b200.tensors import synthetic_layer  # noqa: E402
 from paper_2411_15659_b200.workloads import CONFIGS, layer_seed  # noqa: E402
 
 
-def time_plan(mod, xd, y, iters):
+_FLUSH = None
+
+
+def _flush_buf():
+    global _FLUSH
+    if _FLUSH is None:  # 2x the 126 MB L2
+        _FLUSH = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    return _FLUSH
+
+
+def time_plan(mod, xd, y, iters, cold=False):
+    """Per-launch time (us) from one graph replay of `iters` launches; cold:
+    an L2-flushing 256 MB fill before every launch, its own time subtracted."""
+    if cold:
+        fb = _flush_buf()
+        g_f = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs), torch.cuda.graph(g_f, stream=cs):
+            for _ in range(iters):
+                fb.fill_(1)
+        torch.cuda.synchronize()
+        g_f.replay()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        g_f.replay()
+        e.record()
+        torch.cuda.synchronize()
+        flush_ms = s.elapsed_time(e)
     g_ = torch.cuda.CUDAGraph()
     cs = torch.cuda.Stream()
     cs.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(cs), torch.cuda.graph(g_, stream=cs):
         for _ in range(iters):
+            if cold:
+                fb.fill_(1)
             mod(xd, out=y)
     torch.cuda.synchronize()
     g_.replay()
@@ -32,12 +63,15 @@ def time_plan(mod, xd, y, iters):
     g_.replay()
     e.record()
     torch.cuda.synchronize()
-    return s.elapsed_time(e) / iters * 1e3
+    ms = s.elapsed_time(e) - (flush_ms if cold else 0.0)
+    return ms / iters * 1e3
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="2,3,5,4")
+    ap.add_argument("--cold", action="store_true", help="flush L2 before every launch")
+    ap.add_argument("--max-gflop", type=float, default=1e9, help="skip larger layers")
     a = ap.parse_args()
     out = {}
     seen = set()
@@ -47,6 +81,8 @@ def main():
             if key in seen:
                 continue
             seen.add(key)
+            if g.flops(n) > a.max_gflop * 1e9:
+                continue
             x, w = synthetic_layer(g, n, layer_seed(ci, li))
             xd = torch.from_numpy(x).cuda()
             small = g.flops(n) < 2e9
@@ -57,13 +93,13 @@ def main():
             os.environ.pop("SMMC_FORCE_PLAN", None)
             mod = device.SmmConv2d(g, w)
             y = mod(xd)
-            default = (time_plan(mod, xd, y, iters), _native.plan_describe(g, n))
+            default = (time_plan(mod, xd, y, iters, a.cold), _native.plan_describe(g, n))
             for v, s in cands:
                 os.environ["SMMC_FORCE_PLAN"] = f"{v},{s}"
                 mod = device.SmmConv2d(g, w)
                 y = mod(xd)
                 try:
-                    res.append((time_plan(mod, xd, y, iters), v, s))
+                    res.append((time_plan(mod, xd, y, iters, a.cold), v, s))
                 except Exception as exc:  # noqa: BLE001
                     print(f"  {name} {v},{s}: {exc}", file=sys.stderr)
             os.environ.pop("SMMC_FORCE_PLAN", None)
@@ -77,7 +113,7 @@ def main():
                          "all": [[r[1], r[2], round(r[0], 2)] for r in res]}
             del xd, mod, y
             torch.cuda.empty_cache()
-    Path("gpurun_out/plan_sweep.json").write_text(json.dumps(out, indent=1))
+    Path("gpurun_out/plan_sweep%s.json" % ("_cold" if a.cold else "")).write_text(json.dumps(out, indent=1))
 
 
 if __name__ == "__main__":

@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(256) zero_counters_kernel(int* __restrict__ c,
     for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) c[i] = 0;
 }
 
-// reduce_mode 2: y = sum of the partial planes in split order.
+// reduce_mode 2: y = sum of the partial planes (fixed order, below).
 struct ReduceOut {
     float* ys[kMaxOut];
     int n_out, co, co_total, co_base, ohw;
@@ -465,38 +465,63 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
     const bool plain = ro.n_out == 1 && ro.co_total == ro.co && ro.co_base == 0;
     const int64_t total4 =
         ((total & 3) || !ro.vec || (!plain && (ro.ohw & 3))) ? 0 : (total >> 2);
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total4; i += stride) {
-        const float4* src = reinterpret_cast<const float4*>(ws) + i;
-        float4 s = __ldcg(src);
-        int z = 1;
-        for (; z + 3 < splits; z += 4) {  // 4 independent loads in flight
-            const float4 v0 = __ldcg(src + (int64_t)(z + 0) * total4);
-            const float4 v1 = __ldcg(src + (int64_t)(z + 1) * total4);
-            const float4 v2 = __ldcg(src + (int64_t)(z + 2) * total4);
-            const float4 v3 = __ldcg(src + (int64_t)(z + 3) * total4);
-            s.x += v0.x; s.y += v0.y; s.z += v0.z; s.w += v0.w;
-            s.x += v1.x; s.y += v1.y; s.z += v1.z; s.w += v1.w;
-            s.x += v2.x; s.y += v2.y; s.z += v2.z; s.w += v2.w;
-            s.x += v3.x; s.y += v3.y; s.z += v3.z; s.w += v3.w;
+    // A block covers opb = 256/G float4 outputs with G split groups (G = 1, 2,
+    // 4, 8 for <= 4, 8, 16, > 16 splits): thread (g, j) sums the split range
+    // [g*per, (g+1)*per) of output j with all its loads in flight, then group
+    // 0 adds the G group sums in order — a fixed two-level order
+    // (deterministic) with up to 8x the memory-level parallelism of one thread
+    // walking every split (the N=1 layers run 16-32 splits).
+    __shared__ float4 part[256];
+    const int groups = splits <= 4 ? 1 : splits <= 8 ? 2 : splits <= 16 ? 4 : 8;
+    const int opb = 256 / groups;
+    const int grp = threadIdx.x / opb, lane = threadIdx.x - grp * opb;
+    const int per = (splits + groups - 1) / groups;
+    for (int64_t base = (int64_t)blockIdx.x * opb; base < total4; base += (int64_t)gridDim.x * opb) {
+        const int64_t i = base + lane;
+        if (i < total4) {
+            const float4* src = reinterpret_cast<const float4*>(ws) + i;
+            const int z0 = grp * per, z1 = min(splits, z0 + per);
+            float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+            int z = z0;
+            for (; z + 3 < z1; z += 4) {
+                const float4 v0 = __ldcg(src + (int64_t)(z + 0) * total4);
+                const float4 v1 = __ldcg(src + (int64_t)(z + 1) * total4);
+                const float4 v2 = __ldcg(src + (int64_t)(z + 2) * total4);
+                const float4 v3 = __ldcg(src + (int64_t)(z + 3) * total4);
+                s.x += v0.x; s.y += v0.y; s.z += v0.z; s.w += v0.w;
+                s.x += v1.x; s.y += v1.y; s.z += v1.z; s.w += v1.w;
+                s.x += v2.x; s.y += v2.y; s.z += v2.z; s.w += v2.w;
+                s.x += v3.x; s.y += v3.y; s.z += v3.z; s.w += v3.w;
+            }
+            for (; z < z1; ++z) {
+                const float4 v = __ldcg(src + (int64_t)z * total4);
+                s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+            }
+            part[threadIdx.x] = s;
         }
-        for (; z < splits; ++z) {
-            const float4 v = __ldcg(src + (int64_t)z * total4);
-            s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
-        }
-        if (plain) {
-            reinterpret_cast<float4*>(ro.ys[0])[i] = s;
-        } else {
-            const int64_t e = i << 2;  // local (n, c, pixel) index of the first lane
-            const int64_t plane = (int64_t)ro.co * ro.ohw;
-            const int64_t n = e / plane;
-            const int64_t r = e - n * plane;
-            const int64_t d = (n * ro.co_total + ro.co_base) * ro.ohw + r;
+        if (groups > 1) __syncthreads();
+        if (grp == 0 && i < total4) {
+            float4 s = part[lane];
+            for (int g = 1; g < groups; ++g) {
+                const float4 v = part[g * opb + lane];
+                s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+            }
+            if (plain) {
+                reinterpret_cast<float4*>(ro.ys[0])[i] = s;
+            } else {
+                const int64_t e = i << 2;  // local (n, c, pixel) index of the first lane
+                const int64_t plane = (int64_t)ro.co * ro.ohw;
+                const int64_t n = e / plane;
+                const int64_t r = e - n * plane;
+                const int64_t d = (n * ro.co_total + ro.co_base) * ro.ohw + r;
 #pragma unroll
-            for (int o = 0; o < kMaxOut; ++o)
-                if (o < ro.n_out) *reinterpret_cast<float4*>(ro.ys[o] + d) = s;
+                for (int o = 0; o < kMaxOut; ++o)
+                    if (o < ro.n_out) *reinterpret_cast<float4*>(ro.ys[o] + d) = s;
+            }
         }
+        if (groups > 1) __syncthreads();
     }
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (total4 << 2) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += stride) {
         float s = ws[i];
@@ -801,7 +826,8 @@ cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
     count_launches(1);
     if (e != cudaSuccess || pl.reduce_mode != 2) return e;
     const int64_t total = (int64_t)p.m * p.co;
-    const int blocks = (int)std::min<int64_t>((total / 4 + 255) / 256 + 1, 148 * 16);
+    const int groups = p.splits <= 4 ? 1 : p.splits <= 8 ? 2 : p.splits <= 16 ? 4 : 8;
+    const int blocks = (int)std::min<int64_t>((total / 4 + 256 / groups - 1) / (256 / groups) + 1, 148 * 16);
     ReduceOut ro{};
     for (int o = 0; o < p.n_out; ++o) ro.ys[o] = p.ys[o];
     ro.n_out = p.n_out;

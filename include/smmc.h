@@ -179,6 +179,18 @@ SMMC_API int smmc_plan_describe(const smmc_geom* g, int mode, char* buf, size_t 
 /* Same for the bf16 tensor-core variant (tile shape, halo/box, persistence). */
 SMMC_API int smmc_tc_plan_describe(const smmc_geom* g, char* buf, size_t len);
 
+/* ---- Fitted layers (the GPU form of Conv2D.fit / transform,
+ * estimator.py:71-125): the repacked weights are uploaded once at fit time
+ * and stay in HBM; each forward moves only the input batch up and the output
+ * down (the same chunked H2D / conv / D2H pipeline as the _host entry).
+ * Synchronous, re-entrant per device (staging pool mutex). */
+typedef struct smmc_layer smmc_layer;
+SMMC_API int smmc_layer_create(const float* w_smm, const smmc_geom* g, int device,
+                               smmc_layer** out);
+SMMC_API int smmc_layer_forward_host(smmc_layer* layer, const float* x, float* y, int n,
+                                     int mode);
+SMMC_API int smmc_layer_destroy(smmc_layer* layer);
+
 /* ---- Fused output-channel-shard all-gather.
  * Rank r of P holds the full input and W_smm[..., co_base:co_base+c_o] as a
  * compact (c_i, k_w, k_h, c_o) slice (g_local->c_o = its channel count).  The

@@ -42,6 +42,7 @@ EXPORTED_SYMBOLS = (
     "smmc_conv2d_fwd_bf16_tc", "smmc_im2col_bytes", "smmc_im2col_pack_f32",
     "smmc_conv2d_fwd_f32_gather", "smmc_gather_workspace_bytes", "smmc_ipc_handle",
     "smmc_ipc_open", "smmc_ipc_close", "smmc_host_alloc_pinned", "smmc_host_free_pinned",
+    "smmc_layer_create", "smmc_layer_forward_host", "smmc_layer_destroy",
 )
 
 SMMC_MAX_OUT = 8
@@ -115,6 +116,9 @@ _SIGNATURES = {
     "smmc_ipc_close": (ctypes.c_int, [_P, ctypes.c_size_t]),
     "smmc_host_alloc_pinned": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
     "smmc_host_free_pinned": (ctypes.c_int, [_P]),
+    "smmc_layer_create": (ctypes.c_int, [_P, _GP, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+    "smmc_layer_forward_host": (ctypes.c_int, [_P, _P, _P, ctypes.c_int, ctypes.c_int]),
+    "smmc_layer_destroy": (ctypes.c_int, [_P]),
 }
 
 
@@ -218,6 +222,42 @@ def ipc_open(handle, offset):
 
 def ipc_close(dev_ptr, offset):
     check(lib().smmc_ipc_close(ctypes.c_void_p(dev_ptr), offset), "smmc_ipc_close")
+
+
+class Layer:
+    """A fitted conv layer (smmc_layer): W_smm uploaded once to `device`;
+    ``forward(x, y)`` runs the host-buffer pipeline on float32 C-contiguous
+    numpy arrays (x: (n, c_i, h, w) -> y: (n, c_o, h', w'))."""
+
+    def __init__(self, weights_smm, geom, device=0):
+        import numpy as np
+        w = np.ascontiguousarray(weights_smm, dtype=np.float32)
+        if w.shape != geom.weights_smm_shape:
+            raise ShapeMismatchError(
+                f"weights_smm has shape {w.shape}, expected {geom.weights_smm_shape}")
+        self.geom = geom
+        self._h = ctypes.c_void_p(0)
+        g = Geom.of(geom, 1)
+        check(lib().smmc_layer_create(w.ctypes.data_as(ctypes.c_void_p), ctypes.byref(g),
+                                      int(device), ctypes.byref(self._h)), "smmc_layer_create")
+
+    def forward(self, x, y, mode="ffma"):
+        n = int(x.shape[0])
+        check(lib().smmc_layer_forward_host(self._h, ctypes.c_void_p(x.ctypes.data),
+                                            ctypes.c_void_p(y.ctypes.data), n, mode_id(mode)),
+              "smmc_layer_forward_host")
+        return y
+
+    def close(self):
+        if self._h and self._h.value:
+            lib().smmc_layer_destroy(self._h)
+            self._h = ctypes.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
 
 
 def pinned_empty(shape, dtype="float32"):

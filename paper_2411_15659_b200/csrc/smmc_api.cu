@@ -488,14 +488,18 @@ int smmc_ipc_close(void* dev_ptr, size_t offset) {
                        "cudaIpcCloseMemHandle");
 }
 
-int smmc_conv2d_fwd_f32_host(const float* x, const float* w_smm, float* y, const smmc_geom* g,
-                             int mode, int device) {
+namespace smmc {
+namespace {
+// The host-buffer pipeline.  `w_dev` non-NULL: the weights already live on
+// the device (a fitted smmc_layer) and are not uploaded.
+int host_pipeline(const float* x, const float* w_smm, const float* w_dev, float* y,
+                  const smmc_geom* g, int mode, int device) {
     int oh = 0, ow = 0;
     int st = check_geom(g, &oh, &ow);
     if (st) return st;
     if ((st = check_mode(mode))) return st;
     if (g->n == 0) return SMMC_OK;
-    if (!x || !w_smm || !y) {
+    if (!x || !(w_smm || w_dev) || !y) {
         set_error("x, w_smm and y must be non-NULL host pointers");
         return SMMC_ESHAPE;
     }
@@ -526,14 +530,15 @@ int smmc_conv2d_fwd_f32_host(const float* x, const float* w_smm, float* y, const
     size_t wsb = workspace_for(gc, mode, sm_count_for(device));
     gc.n = g->n - (chunks - 1) * per;
     wsb = std::max(wsb, workspace_for(gc, mode, sm_count_for(device)));
-    if ((st = ensure(hp, 0, xb)) || (st = ensure(hp, 1, wb)) || (st = ensure(hp, 2, yb)) ||
-        (st = ensure(hp, 3, wsb)))
+    if ((st = ensure(hp, 0, xb)) || (st = ensure(hp, 1, w_dev ? 16 : wb)) ||
+        (st = ensure(hp, 2, yb)) || (st = ensure(hp, 3, wsb)))
         return st;
     float* xd = static_cast<float*>(hp.buf[0]);
-    float* wd = static_cast<float*>(hp.buf[1]);
+    const float* wd = w_dev ? w_dev : static_cast<float*>(hp.buf[1]);
     float* yd = static_cast<float*>(hp.buf[2]);
-    if ((st = cuda_status(cudaMemcpyAsync(wd, w_smm, wb, cudaMemcpyHostToDevice, hp.s_in),
-                          "H2D w_smm")))
+    if (!w_dev && (st = cuda_status(cudaMemcpyAsync(hp.buf[1], w_smm, wb, cudaMemcpyHostToDevice,
+                                                    hp.s_in),
+                                    "H2D w_smm")))
         return st;
     // All H2D copies are enqueued first: streams share a few hardware queues,
     // and an H2D queued behind a conv's event wait stalls the copy engine.
@@ -564,6 +569,77 @@ int smmc_conv2d_fwd_f32_host(const float* x, const float* w_smm, float* y, const
     }
     return cuda_status(cudaStreamSynchronize(hp.s_out), "conv (host path)");
 }
+}  // namespace
+}  // namespace smmc
+
+int smmc_conv2d_fwd_f32_host(const float* x, const float* w_smm, float* y, const smmc_geom* g,
+                             int mode, int device) {
+    if (!w_smm && g && g->n != 0) {
+        set_error("x, w_smm and y must be non-NULL host pointers");
+        return SMMC_ESHAPE;
+    }
+    return host_pipeline(x, w_smm, nullptr, y, g, mode, device);
+}
+
+// ---- fitted layers: weights uploaded once (Conv2D.fit), forward on host buffers
+struct smmc_layer {
+    smmc_geom g;     // n unused
+    int device;
+    float* w = nullptr;
+};
+
+int smmc_layer_create(const float* w_smm, const smmc_geom* g, int device, smmc_layer** out) {
+    if (!out) {
+        set_error("out must be non-NULL");
+        return SMMC_ESHAPE;
+    }
+    *out = nullptr;
+    int oh = 0, ow = 0;
+    smmc_geom gg = g ? *g : smmc_geom{};
+    gg.n = 1;
+    int st = check_geom(g ? &gg : nullptr, &oh, &ow);
+    if (st) return st;
+    if (!w_smm) {
+        set_error("w_smm must be a non-NULL host pointer");
+        return SMMC_ESHAPE;
+    }
+    if ((st = select_device(device))) return st;
+    const size_t wb = (size_t)gg.c_i * gg.k_w * gg.k_h * gg.c_o * sizeof(float);
+    smmc_layer* L = new smmc_layer{gg, device, nullptr};
+    if ((st = cuda_status(cudaMalloc(&L->w, wb), "cudaMalloc(weights)")) ||
+        (st = cuda_status(cudaMemcpy(L->w, w_smm, wb, cudaMemcpyHostToDevice), "H2D weights"))) {
+        if (L->w) cudaFree(L->w);
+        delete L;
+        return st;
+    }
+    *out = L;
+    return SMMC_OK;
+}
+
+int smmc_layer_forward_host(smmc_layer* L, const float* x, float* y, int n, int mode) {
+    if (!L) {
+        set_error("layer is NULL");
+        return SMMC_ESHAPE;
+    }
+    smmc_geom g = L->g;
+    g.n = n;
+    return host_pipeline(x, nullptr, L->w, y, &g, mode, L->device);
+}
+
+int smmc_layer_destroy(smmc_layer* L) {
+    if (!L) return SMMC_OK;
+    int st = SMMC_OK;
+    if (L->w) {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(L->device);
+        st = cuda_status(cudaFree(L->w), "cudaFree(weights)");
+        cudaSetDevice(prev);
+    }
+    delete L;
+    return st;
+}
+
 
 // ---- pinned host staging buffers for the *_host entries.  cudaHostAlloc
 // memory measured only 29-36 GB/s H2D on the B200 boxes (KVM guest), while

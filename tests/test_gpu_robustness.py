@@ -213,3 +213,33 @@ def test_device_path_unaligned_input_window():
     torch.cuda.synchronize()
     ref = orc.smm_conv_c(np.ascontiguousarray(x[1:]), orc.repack(w), g)
     assert orc.max_abs_ratio(y.cpu().numpy(), ref) <= TOL
+
+
+def test_fitted_layer_api():
+    """smmc_layer: weights uploaded once; forward on host buffers equals the
+    per-call host entry bitwise (same plans), for several batch sizes and
+    both modes; the estimator's transform goes through it."""
+    from paper_2411_15659_b200 import Conv2D
+    g = ConvGeometry(32, 48, 14, 14, 3, 3, pad_h=1, pad_w=1)
+    x, w = synthetic_layer(g, 9, 12)
+    ws = smm.repack_weights(w, g)
+    layer = _native.Layer(ws, g)
+    for n in (1, 4, 9, 0):
+        xs = np.ascontiguousarray(x[:n])
+        y = np.full((n,) + g.output_shape, np.nan, np.float32)
+        layer.forward(xs, y)
+        if n:
+            assert np.array_equal(y, smm.smm_conv_batched(xs, ws, g))
+    ye = np.empty((3,) + g.output_shape, np.float32)
+    layer.forward(np.ascontiguousarray(x[:3]), ye, mode="exact")
+    assert np.array_equal(ye, orc.smm_conv_c(np.ascontiguousarray(x[:3]), orc.repack(w), g))
+    layer.close()
+    layer.close()  # idempotent
+    est = Conv2D(out_channels=48, kernel_size=3, padding=1, weights=w).fit(x)
+    a = est.transform(x)
+    assert np.array_equal(a, est.transform(x))  # cached device weights
+    assert orc.max_abs_ratio(a, orc.smm_conv_c(x, orc.repack(w), g)) <= TOL
+    est.set_params(weights=np.zeros_like(w)).fit(x)  # refit replaces the device copy
+    assert float(np.abs(est.transform(x)).max()) == 0.0
+    import pickle
+    assert pickle.loads(pickle.dumps(est)).transform(x).shape == a.shape

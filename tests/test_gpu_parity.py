@@ -236,3 +236,44 @@ def test_every_reduction_mode_matches_oracle(plan, monkeypatch):
     assert orc.max_abs_ratio(y1.cpu().numpy(), ref) <= TOL_FP32, desc
     if plan.endswith(",0"):
         assert "stream-K" in desc
+
+
+def _draw(rng):
+    """A random small geometry over the reference acceptance sweep's ranges
+    (test_acceptance.py:51-68): c in [1, 8], h, w in [4, 32], k in {1,3,5,7},
+    stride in {1, 2}, pad in {0, 1, 2}; None when the kernel does not fit."""
+    ci, co = int(rng.integers(1, 9)), int(rng.integers(1, 9))
+    h, w = int(rng.integers(4, 33)), int(rng.integers(4, 33))
+    kh, kw = int(rng.choice((1, 3, 5, 7))), int(rng.choice((1, 3, 5, 7)))
+    sh, sw = int(rng.choice((1, 2))), int(rng.choice((1, 2)))
+    ph, pw = int(rng.choice((0, 1, 2))), int(rng.choice((0, 1, 2)))
+    if kh > h + 2 * ph or kw > w + 2 * pw:
+        return None
+    return ConvGeometry(ci, co, h, w, kh, kw, sh, sw, ph, pw)
+
+
+def test_acceptance_sweep_200_random_geometries():
+    """The reference's acceptance criterion 1 on the GPU: 200 random
+    geometries (seed 20240601), splitmix64 data, FFMA mode within
+    max_rel_diff 1e-4 of the oracle, exact mode bitwise, batches of 1-3
+    samples, and bitwise launch-to-launch determinism."""
+    from paper_2411_15659_b200.tensors import random_tensor
+    rng = np.random.default_rng(20240601)
+    checked, worst = 0, 0.0
+    while checked < 200:
+        g = _draw(rng)
+        if g is None:
+            continue
+        checked += 1
+        n = 1 + checked % 3
+        x = random_tensor((n,) + g.input_shape, 2 * checked)
+        w = random_tensor(g.weights_shape, 2 * checked + 1)
+        ws = smm.repack_weights(w, g)
+        ref = orc.smm_conv_c(x, orc.repack(w), g)
+        y = smm.smm_conv_batched(x, ws, g)
+        d = orc.max_rel_diff(y, ref)
+        worst = max(worst, d)
+        assert d <= 1e-4, (g, d)
+        assert np.array_equal(smm.smm_conv_batched(x, ws, g), y), g
+        assert np.array_equal(smm.smm_conv_batched(x, ws, g, mode="exact"), ref), g
+    assert worst > 0.0  # the FFMA path really reorders the sums

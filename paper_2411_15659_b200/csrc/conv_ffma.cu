@@ -45,6 +45,8 @@
 #include <cstdlib>
 #include <mutex>
 
+#include <cooperative_groups.h>
+
 #include "smmc_internal.cuh"
 
 namespace smmc {
@@ -399,6 +401,68 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
         }
     }
 
+    // ---- split-K inside a thread-block cluster (reduce_mode 4): the S CTAs
+    // of a tile (cluster dims 1 x 1 x S) park their partial tiles in their own
+    // shared memory (the drained cp.async ring), then CTA r sums slice r of
+    // the tile over ranks 0..S-1 in order through distributed shared memory
+    // and stores it — no workspace, no counters, no second kernel, and the
+    // reduction runs on all S SMs at once (deterministic: fixed rank order).
+    if (!sk && p.reduce_mode == 4) {
+        cooperative_groups::cluster_group cluster = cooperative_groups::this_cluster();
+        constexpr int LD = BM + 4;  // channel-major [BN][BM+4]: float4 rows, fewer conflicts
+        float* part = smem;
+        __syncthreads();  // every warp is done reading the ring
+#pragma unroll
+        for (int ib = 0; ib < NQ; ++ib)
+#pragma unroll
+            for (int jb = 0; jb < 2; ++jb)
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    const int cl = jb * (BN / 2) + cg * 4 + jj;
+                    const int j = jb * 4 + jj;
+                    *reinterpret_cast<float4*>(part + cl * LD + ib * (BM / NQ) + pg * 4) =
+                        make_float4(acc[ib * 4 + 0][j], acc[ib * 4 + 1][j], acc[ib * 4 + 2][j],
+                                    acc[ib * 4 + 3][j]);
+                }
+        cluster.sync();
+        const int S = (int)cluster.num_blocks();
+        const int r = (int)cluster.block_rank();
+        constexpr int T4 = BN * BM / 4;  // float4s per tile
+        const bool vec_ok = (p.ohw & 3) == 0;
+        for (int e = r * T4 / S + tid; e < (r + 1) * T4 / S; e += THREADS) {
+            const int cl = e / (BM / 4);
+            const int px = (e - cl * (BM / 4)) * 4;
+            const int off = cl * LD + px;
+            float4 a4 = *reinterpret_cast<const float4*>(cluster.map_shared_rank(part, 0) + off);
+            for (int z = 1; z < S; ++z) {
+                const float4 v = *reinterpret_cast<const float4*>(cluster.map_shared_rank(part, z) + off);
+                a4.x += v.x;
+                a4.y += v.y;
+                a4.z += v.z;
+                a4.w += v.w;
+            }
+            const int co = n0 + cl;
+            const int pbase = m0 + px;
+            if (co >= p.co || pbase >= p.m) continue;
+            const int n = pbase / p.ohw;
+            const int rem = pbase - n * p.ohw;
+            if (vec_ok && pbase + 3 < p.m) {
+                *reinterpret_cast<float4*>(p.y + ((int64_t)n * p.co + co) * p.ohw + rem) = a4;
+            } else {
+                const float v4[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+                for (int ii = 0; ii < 4; ++ii) {
+                    const int pp = pbase + ii;
+                    if (pp >= p.m) break;
+                    const int nn = pp / p.ohw;
+                    p.y[((int64_t)nn * p.co + co) * p.ohw + (pp - nn * p.ohw)] = v4[ii];
+                }
+            }
+        }
+        cluster.sync();  // peers may still be reading this CTA's partial
+        return;
+    }
+
     // ---- epilogue: NCHW stores (reduce_mode 2: partial plane `slot` of ws,
     // placed into y by splitk_reduce_kernel — also with a single split when
     // the output goes to gather replicas)
@@ -555,15 +619,32 @@ template <int BM, int BN, int T, int MINB, int TM, int BK, int KH, int KW, int S
 cudaError_t launch_one(const Problem& p, dim3 grid, cudaStream_t s) {
     if (CVEC && !SK && p.reduce_mode == 3)
         return launch_one<BM, BN, T, MINB, TM, BK, KH, KW, SH, SW, CVEC, true>(p, grid, s);
-    constexpr int smem = kStages * BK * (BM + BN) * (int)sizeof(float);
+    constexpr int ring = kStages * BK * (BM + BN) * (int)sizeof(float);
+    constexpr int part = BN * (BM + 4) * (int)sizeof(float);  // reduce_mode 4 partial tile
+    constexpr int smem_max = ring > part ? ring : part;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     auto kern = conv_ffma_kernel<BM, BN, T, MINB, TM, BK, KH, KW, SH, SW, CVEC, SK && CVEC>;
     std::call_once(once, [&] {
-        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
     });
     if (attr_err != cudaSuccess) return attr_err;
-    kern<<<grid, T, smem, s>>>(p);
+    if (!SK && p.reduce_mode == 4) {  // the S splits of a tile form one cluster
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(T);
+        cfg.dynamicSmemBytes = smem_max;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 1;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = grid.z;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kern, p);
+    }
+    kern<<<grid, T, ring, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -768,6 +849,20 @@ FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) {
             best.reduce_mode = best.splits > 1 ? (best.splits <= 4 ? 1 : 2) : 0;
         }
     }
+    // split-K with 2..8 splits on an under-filled GPU (at most half the CTA
+    // slots): reduce inside a thread-block cluster (reduce_mode 4) instead of
+    // global partials (modes 1, 2).  On fuller grids a cluster's CTAs idle at
+    // the reduction waiting for each other and co-scheduling clusters costs
+    // slots (measured: conv256@14 N=32, 294 CTAs, 147 -> 211 us; conv128@28
+    // N=32, 588 CTAs, 152 -> 184 us); N=1 layers gain (20.0 -> 19.1 us).
+    int per_sm_best = 1;
+    for (int v = 0; v < kNumTiles; ++v)
+        if (kTiles[v].bm == best.bm && kTiles[v].bn == best.bn) per_sm_best = kTiles[v].per_sm;
+    if ((best.reduce_mode == 1 || best.reduce_mode == 2) && best.splits >= 2 && best.splits <= 8 &&
+        2 * best.tiles * best.splits <= (int64_t)sm_count * per_sm_best) {
+        const char* f = getenv("SMMC_CLUSTER_RED");  // A/B hook
+        if (!f || atoi(f) != 0) best.reduce_mode = 4;
+    }
     best.bk = bk;
     best.kt_total = kt_total;
     best.cvec = cvec ? 1 : 0;
@@ -842,6 +937,6 @@ cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-int ffma_launches(const FfmaPlan& pl) { return pl.reduce_mode == 0 ? 1 : 2; }
+int ffma_launches(const FfmaPlan& pl) { return (pl.reduce_mode == 0 || pl.reduce_mode == 4) ? 1 : 2; }
 
 }  // namespace smmc

@@ -388,6 +388,7 @@ int smmc_plan_describe(const smmc_geom* g, int mode, char* buf, size_t len) {
              pl.reduce_mode == 0 ? "none"
              : pl.reduce_mode == 1 ? "last-arriver"
              : pl.reduce_mode == 2 ? "kernel"
+             : pl.reduce_mode == 4 ? "cluster DSMEM"
                                    : "stream-K",
              (long long)pl.tiles);
     if (pl.reduce_mode == 3) {

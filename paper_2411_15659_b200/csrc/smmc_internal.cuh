@@ -30,7 +30,8 @@ struct Problem {
     int kt_per_split;    // tap blocks per split
     int splits;
     int cvec;            // 1: tap-major K order (c_i % BK == 0)
-    int reduce_mode;     // 0 none, 1 split-K last-arriver, 2 split-K reduce kernel, 3 stream-K
+    int reduce_mode;     // 0 none, 1 split-K last-arriver, 2 split-K reduce kernel, 3 stream-K,
+                         // 4 split-K reduced in a thread-block cluster (DSMEM)
     int64_t tiles;       // pixel tiles x channel tiles
     int tiles_n;         // channel tiles
     int sk_iters;        // stream-K: tap blocks per CTA
@@ -62,7 +63,7 @@ struct FfmaPlan {
     int kt_per_split;
     int tap_kind;      // 0 generic, 1: 3x3s1, 2: 1x1s1, 3: 7x7s2, 4: 11x11s4, 5: 5x5s1
     int cvec;          // tap-major K order
-    int reduce_mode;   // 0 none, 1 split-K last-arriver, 2 split-K reduce kernel, 3 stream-K
+    int reduce_mode;   // 0 none, 1 last-arriver, 2 reduce kernel, 3 stream-K, 4 cluster DSMEM
     int64_t tiles;     // pixel tiles x channel tiles
     int tiles_n;
     int sk_ctas;       // stream-K grid

@@ -215,14 +215,18 @@ def test_launch_counter_and_plan_describe():
     assert "ffma" in _native.plan_describe(g, 2)
 
 
-@pytest.mark.parametrize("plan", ["0,1", "0,3", "1,2", "1,0", "2,0", "3,0", "3,8", "1,24", "0,0"])
-def test_every_reduction_mode_matches_oracle(plan, monkeypatch):
-    """Force each work decomposition (no split, split-K last-arriver, split-K
-    reduce kernel, stream-K) on one geometry: all within tolerance of the
-    oracle, each bitwise deterministic across launches."""
+@pytest.mark.parametrize("cluster", ["1", "0"])
+@pytest.mark.parametrize("plan", ["0,1", "0,3", "1,2", "1,0", "2,0", "3,0", "3,8", "1,24", "0,0",
+                                  "2,5", "3,7"])
+def test_every_reduction_mode_matches_oracle(plan, cluster, monkeypatch):
+    """Force each work decomposition (no split, split-K reduced in a cluster
+    through DSMEM / by the last arriver / by a reduce kernel, stream-K) on one
+    geometry: all within tolerance of the oracle, each bitwise deterministic
+    across launches."""
     import torch
     from paper_2411_15659_b200 import device
     monkeypatch.setenv("SMMC_FORCE_PLAN", plan)
+    monkeypatch.setenv("SMMC_CLUSTER_RED", cluster)
     g = ConvGeometry(64, 96, 20, 20, 3, 3, pad_h=1, pad_w=1)
     x, w = synthetic_layer(g, 6, 123)
     wd = torch.from_numpy(smm.repack_weights(w, g)).cuda()
@@ -236,6 +240,27 @@ def test_every_reduction_mode_matches_oracle(plan, monkeypatch):
     assert orc.max_abs_ratio(y1.cpu().numpy(), ref) <= TOL_FP32, desc
     if plan.endswith(",0"):
         assert "stream-K" in desc
+    if cluster == "0":
+        assert "cluster" not in desc, desc
+
+
+@pytest.mark.parametrize("plan", ["1,2", "1,8", "3,5", "0,3"])
+def test_cluster_dsmem_split_reduction(plan, monkeypatch):
+    """Under-filled split-K grids reduce their partial tiles inside a
+    thread-block cluster through distributed shared memory (one kernel, no
+    workspace); ragged tiles and c_o % 4 != 0 included."""
+    monkeypatch.setenv("SMMC_FORCE_PLAN", plan)
+    for g, n in ((ConvGeometry(48, 70, 11, 9, 3, 3, pad_h=1, pad_w=1), 1),
+                 (ConvGeometry(32, 64, 12, 12, 3, 3, pad_h=1, pad_w=1), 2)):
+        desc = _native.plan_describe(g, n)
+        assert "cluster" in desc and _native.workspace_bytes(g, n) == 0, desc
+        assert _native.plan_launches(g, n) == 1
+        x, w = synthetic_layer(g, n, 77)
+        ws = smm.repack_weights(w, g)
+        y = smm.smm_conv_batched(x, ws, g)
+        assert np.array_equal(y, smm.smm_conv_batched(x, ws, g))
+        ref = orc.smm_conv_c(x, orc.repack(w), g)
+        assert orc.max_abs_ratio(y, ref) <= TOL_FP32, desc
 
 
 def _draw(rng):

@@ -688,7 +688,7 @@ struct TunedPlan {
 constexpr TunedPlan kTuned[] = {
     {1, 64, 56, 56, 64, 3, 1, 1, 1, 8},        // 14.8 us (model: 15.5)
     {1, 128, 28, 28, 128, 3, 1, 1, 1, 8},      // 15.0 us (19.4)
-    {1, 256, 14, 14, 256, 3, 1, 1, 1, 16},     // 15.9 us (32.4)
+    {1, 256, 14, 14, 256, 3, 1, 1, 0, 32},     // 14.1 us (1,16: 14.7)
     {1, 512, 7, 7, 512, 3, 1, 1, 3, 32},       // 20.2 us (42.9)
     {32, 64, 56, 56, 64, 3, 1, 1, 2, 0},       // 160.0 us (168.0)
     {8, 96, 27, 27, 256, 5, 1, 2, 3, 4},       // 150.1 us (154.2)

@@ -54,6 +54,27 @@ namespace {
 
 constexpr int kStages = 4;
 
+#ifdef SMMC_PROBE_TL
+// Timing probe (A/B builds only, -DSMMC_PROBE_TL=1): per-CTA globaltimer
+// stamps [entry, first stage landed, K loop done, exit, smid] for
+// tools/timeline_probe.py.
+__device__ unsigned long long g_tl[16384 * 5];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define TL_STAMP(slot, val)                                                                   \
+    do {                                                                                      \
+        const unsigned bid_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); \
+        if (threadIdx.x == 0 && bid_ < 16384) g_tl[bid_ * 5 + (slot)] = (val);                \
+    } while (0)
+#else
+#define TL_STAMP(slot, val) \
+    do {                    \
+    } while (0)
+#endif
+
 template <int BM, int BN, int THREADS, int MINB, int TM, int BK, int KH, int KW, int SH, int SW,
           bool CVEC, bool SK>
 __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem p) {
@@ -81,6 +102,15 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
+#ifdef SMMC_PROBE_TL
+    TL_STAMP(0, gtimer());
+    {
+        unsigned sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        TL_STAMP(4, sm);
+    }
+    bool tl_first = true;
+#endif
     constexpr int WCO = TCO / 8;
     const int cg = (warp % WCO) * 8 + (lane & 7);
     const int pg = (warp / WCO) * 4 + (lane >> 3);
@@ -309,6 +339,9 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
     for (int kt = 0; kt < ktiles; ++kt) {
         cp_async_wait<STAGES - 2>();
         __syncthreads();
+#ifdef SMMC_PROBE_TL
+        if (kt == 0 && tl_first) TL_STAMP(1, gtimer());
+#endif
         {
             const int nk = kt + STAGES - 1;
             if (nk < ktiles) load_stage(nk % STAGES, nk);
@@ -338,6 +371,10 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
         }
     }
     cp_async_wait<0>();
+#ifdef SMMC_PROBE_TL
+    if (tl_first) TL_STAMP(2, gtimer());
+    tl_first = false;
+#endif
 
     float acc[TM][8];
 #pragma unroll
@@ -460,6 +497,7 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
             }
         }
         cluster.sync();  // peers may still be reading this CTA's partial
+        TL_STAMP(3, gtimer());
         return;
     }
 
@@ -504,6 +542,7 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
     if (it >= it_end) break;
     __syncthreads();  // smem ring and s_last are reused by the next segment
     }  // segment loop
+    TL_STAMP(3, gtimer());
 }
 
 // reduce_modes 1 and 3: the per-tile arrival counters must read zero at
@@ -936,6 +975,17 @@ cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
     count_launches(1);
     return cudaGetLastError();
 }
+
+#ifdef SMMC_PROBE_TL
+extern "C" __attribute__((visibility("default"))) int smmc_probe_timeline(unsigned long long* host,
+                                                                         int n) {
+    if (!host) {  // clear
+        static unsigned long long zeros[16384 * 5];
+        return (int)cudaMemcpyToSymbol(g_tl, zeros, sizeof(zeros));
+    }
+    return (int)cudaMemcpyFromSymbol(host, g_tl, sizeof(unsigned long long) * 5 * std::min(n, 16384));
+}
+#endif
 
 int ffma_launches(const FfmaPlan& pl) { return (pl.reduce_mode == 0 || pl.reduce_mode == 4) ? 1 : 2; }
 

@@ -72,6 +72,9 @@ def main():
     ap.add_argument("--configs", default="2,3,5,4")
     ap.add_argument("--cold", action="store_true", help="flush L2 before every launch")
     ap.add_argument("--max-gflop", type=float, default=1e9, help="skip larger layers")
+    ap.add_argument("--layers", default="", help="comma-separated layer names (default: all)")
+    ap.add_argument("--cands", default="", help='forced plans "v,s v,s ..." (default: the grid)')
+    ap.add_argument("--out", default="")
     a = ap.parse_args()
     out = {}
     seen = set()
@@ -83,11 +86,15 @@ def main():
             seen.add(key)
             if g.flops(n) > a.max_gflop * 1e9:
                 continue
+            if a.layers and name not in a.layers.split(","):
+                continue
             x, w = synthetic_layer(g, n, layer_seed(ci, li))
             xd = torch.from_numpy(x).cuda()
             small = g.flops(n) < 2e9
             cands = ([(v, s) for v in (0, 1, 3) for s in (4, 8, 16, 24, 32, 0)] if small else
                      [(v, s) for v in (0, 1, 2, 3) for s in (1, 2, 3, 4, 0)])
+            if a.cands:
+                cands = [tuple(map(int, c.split(","))) for c in a.cands.split()]
             iters = 20 if g.flops(n) < 20e9 else 3
             res = []
             os.environ.pop("SMMC_FORCE_PLAN", None)
@@ -105,15 +112,16 @@ def main():
             os.environ.pop("SMMC_FORCE_PLAN", None)
             res.sort()
             best = res[0]
+            nxt = " ".join(f"{r[0]:.1f} ({r[1]},{r[2]})" for r in res[1:4])
             print(f"{name:32s} default {default[0]:9.1f} us | best {best[0]:9.1f} us plan {best[1]},{best[2]}"
-                  f" | next {res[1][0]:.1f} ({res[1][1]},{res[1][2]}) {res[2][0]:.1f} ({res[2][1]},{res[2][2]})",
-                  flush=True)
+                  f" | next {nxt}", flush=True)
             out[name] = {"key": key, "default_us": default[0], "default_plan": default[1],
                          "best": [best[1], best[2]], "best_us": best[0],
                          "all": [[r[1], r[2], round(r[0], 2)] for r in res]}
             del xd, mod, y
             torch.cuda.empty_cache()
-    Path("gpurun_out/plan_sweep%s.json" % ("_cold" if a.cold else "")).write_text(json.dumps(out, indent=1))
+    Path(a.out or "gpurun_out/plan_sweep%s.json" % ("_cold" if a.cold else "")).write_text(
+        json.dumps(out, indent=1))
 
 
 if __name__ == "__main__":

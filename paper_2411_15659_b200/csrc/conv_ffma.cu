@@ -75,9 +75,15 @@ __device__ __forceinline__ unsigned long long gtimer() {
     } while (0)
 #endif
 
+// G > 1 (warp-group split-K, small problems): the CTA runs G groups of
+// THREADS threads on the same tile, group g over the g-th 1/G of the CTA's
+// tap blocks with its own cp.async ring and named barrier; at the end the
+// groups' partial tiles are summed in group order through shared memory
+// (deterministic) and group 0 carries on with the split-K epilogue.  More
+// warps per SM without more global partials or a second reduction level.
 template <int BM, int BN, int THREADS, int MINB, int TM, int BK, int KH, int KW, int SH, int SW,
-          bool CVEC, bool SK>
-__global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem p) {
+          bool CVEC, bool SK, int G = 1>
+__global__ void __launch_bounds__(THREADS * G, (G > 1 ? 1 : MINB)) conv_ffma_kernel(const Problem p) {
     constexpr int STAGES = kStages;
     constexpr int NQ = TM / 4;             // 4-pixel blocks per thread, BM/NQ apart
     constexpr int TPX = BM / TM;           // pixel groups
@@ -95,11 +101,20 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
     constexpr uint32_t BS_STAGE = BK * BN * 4;
 
     extern __shared__ __align__(16) float smem[];
-    float* As = smem;                                // [STAGES][BK][BM]
-    float* Bs = smem + STAGES * BK * BM;             // [STAGES][BK][BN]
+    constexpr int RING_F = STAGES * BK * (BM + BN);  // floats per group ring
+    static_assert(!(SK && G > 1), "warp-group split-K is for classic grids");
+    const int grp = G > 1 ? (int)threadIdx.x / THREADS : 0;
+    float* As = smem + grp * RING_F;                 // [STAGES][BK][BM]
+    float* Bs = As + STAGES * BK * BM;               // [STAGES][BK][BN]
     __shared__ int s_last;
+    auto group_sync = [&]() {
+        if constexpr (G > 1)
+            asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(THREADS) : "memory");
+        else
+            __syncthreads();
+    };
 
-    const int tid = threadIdx.x;
+    const int tid = G > 1 ? (int)threadIdx.x - grp * THREADS : (int)threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
 #ifdef SMMC_PROBE_TL
@@ -146,6 +161,11 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
         nslots = p.splits;
         kt_beg = slot * p.kt_per_split;
         ktiles = min(KT - kt_beg, p.kt_per_split);
+        if (G > 1) {  // this group's share of the CTA's tap blocks
+            const int per_g = (ktiles + G - 1) / G;
+            kt_beg += grp * per_g;
+            ktiles = max(0, min(ktiles - grp * per_g, per_g));
+        }
     }
 
     const int kh = KH ? KH : p.kh;
@@ -338,7 +358,7 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
     const float* b_rd = Bs + cg * 4;
     for (int kt = 0; kt < ktiles; ++kt) {
         cp_async_wait<STAGES - 2>();
-        __syncthreads();
+        group_sync();
 #ifdef SMMC_PROBE_TL
         if (kt == 0 && tl_first) TL_STAMP(1, gtimer());
 #endif
@@ -386,6 +406,34 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
             acc[i][2 * j + 1] = v.y;
         }
 
+    // ---- warp groups: sum the G partial tiles in group order (groups >= 1
+    // park theirs in the drained rings, [g-1][2*TM float4][THREADS])
+    const bool lead = grp == 0;
+    if constexpr (G > 1) {
+        __syncthreads();  // every group is done with its ring
+        float4* red = reinterpret_cast<float4*>(smem);
+        if (!lead) {
+#pragma unroll
+            for (int g = 0; g < 2 * TM; ++g)
+                red[((grp - 1) * 2 * TM + g) * THREADS + tid] =
+                    make_float4(acc[g >> 1][(g & 1) * 4 + 0], acc[g >> 1][(g & 1) * 4 + 1],
+                                acc[g >> 1][(g & 1) * 4 + 2], acc[g >> 1][(g & 1) * 4 + 3]);
+        }
+        __syncthreads();
+        if (lead) {
+            for (int z = 1; z < G; ++z)
+#pragma unroll
+                for (int g = 0; g < 2 * TM; ++g) {
+                    const float4 v = red[((z - 1) * 2 * TM + g) * THREADS + tid];
+                    acc[g >> 1][(g & 1) * 4 + 0] += v.x;
+                    acc[g >> 1][(g & 1) * 4 + 1] += v.y;
+                    acc[g >> 1][(g & 1) * 4 + 2] += v.z;
+                    acc[g >> 1][(g & 1) * 4 + 3] += v.w;
+                }
+        }
+        __syncthreads();  // partials read before smem is reused below
+    }
+
     // ---- split-K / stream-K: deterministic last-arriver fixup
     bool store = true;
     if ((p.reduce_mode == 1 && p.splits > 1) || (sk && nslots > 1)) {
@@ -393,15 +441,16 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
         float* part = p.ws + (tile * stride_slots) * (BM * BN);
         // layout [slot][2*TM float4 groups][THREADS]: warp stores are contiguous
         float4* mine = reinterpret_cast<float4*>(part + (int64_t)slot * (BM * BN));
+        if (lead)
 #pragma unroll
         for (int g = 0; g < 2 * TM; ++g)
             mine[g * THREADS + tid] = make_float4(acc[g >> 1][(g & 1) * 4 + 0], acc[g >> 1][(g & 1) * 4 + 1],
                                                   acc[g >> 1][(g & 1) * 4 + 2], acc[g >> 1][(g & 1) * 4 + 3]);
         __threadfence();
         __syncthreads();
-        if (tid == 0) s_last = atomicAdd(p.counters + tile, 1) == nslots - 1;
+        if (threadIdx.x == 0) s_last = atomicAdd(p.counters + tile, 1) == nslots - 1;
         __syncthreads();
-        store = s_last;
+        store = s_last && lead;
         if (store) {
             __threadfence();
             // P_0 + P_1 + ... in slot order (own partial re-read too);
@@ -449,6 +498,7 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
         constexpr int LD = BM + 4;  // channel-major [BN][BM+4]: float4 rows, fewer conflicts
         float* part = smem;
         __syncthreads();  // every warp is done reading the ring
+        if (lead)
 #pragma unroll
         for (int ib = 0; ib < NQ; ++ib)
 #pragma unroll
@@ -466,7 +516,7 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
         const int r = (int)cluster.block_rank();
         constexpr int T4 = BN * BM / 4;  // float4s per tile
         const bool vec_ok = (p.ohw & 3) == 0;
-        for (int e = r * T4 / S + tid; e < (r + 1) * T4 / S; e += THREADS) {
+        for (int e = r * T4 / S + (int)threadIdx.x; e < (r + 1) * T4 / S; e += THREADS * G) {
             const int cl = e / (BM / 4);
             const int px = (e - cl * (BM / 4)) * 4;
             const int off = cl * LD + px;
@@ -501,13 +551,31 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
         return;
     }
 
-    // ---- epilogue: NCHW stores (reduce_mode 2: partial plane `slot` of ws,
-    // placed into y by splitk_reduce_kernel — also with a single split when
-    // the output goes to gather replicas)
-    float* out = p.reduce_mode == 2 ? p.ws + (int64_t)slot * ((int64_t)p.m * p.co) : p.y;
+    // ---- reduce_mode 2: this split's partial tile, tile-contiguous
+    // [tile][split][16 float4 = (pixel quad, channel)][THREADS] (coalesced, no
+    // index math); splitk_reduce_kernel sums the splits in order and places
+    // the result (NCHW, gather replicas) — also with a single split when the
+    // output goes to gather replicas
+    if (!sk && p.reduce_mode == 2) {
+        static_assert(TM == 8, "mode-2 partial layout assumes 8x8 thread tiles");
+        if (lead) {
+            float4* dst = reinterpret_cast<float4*>(p.ws) + ((tile * p.splits + slot) * 16) * THREADS + tid;
+#pragma unroll
+            for (int ib = 0; ib < 2; ++ib)
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    dst[(ib * 8 + j) * THREADS] = make_float4(acc[ib * 4 + 0][j], acc[ib * 4 + 1][j],
+                                                              acc[ib * 4 + 2][j], acc[ib * 4 + 3][j]);
+        }
+        TL_STAMP(3, gtimer());
+        return;
+    }
+
+    // ---- epilogue: NCHW stores
+    float* out = p.y;
     const bool vec_ok = (p.ohw & 3) == 0;
 #pragma unroll
-    for (int ib = 0; ib < NQ && store; ++ib) {
+    for (int ib = 0; ib < NQ && store && lead; ++ib) {
         const int pbase = m0 + ib * (BM / NQ) + pg * 4;
         if (pbase >= p.m) continue;
         const int n = pbase / p.ohw;
@@ -524,14 +592,16 @@ __global__ void __launch_bounds__(THREADS, MINB) conv_ffma_kernel(const Problem 
                     float4 v = make_float4(acc[ib * 4 + 0][j], acc[ib * 4 + 1][j],
                                            acc[ib * 4 + 2][j], acc[ib * 4 + 3][j]);
                     *reinterpret_cast<float4*>(out + ((int64_t)n * p.co + co) * p.ohw + rem) = v;
-                } else {
+                } else {  // quad may cross a sample boundary (ohw % 4 != 0)
+                    int nn = n, rr = rem;
 #pragma unroll
                     for (int ii = 0; ii < 4; ++ii) {
-                        const int pp = pbase + ii;
-                        if (pp >= p.m) break;
-                        const int nn = pp / p.ohw;
-                        const int rr = pp - nn * p.ohw;
+                        if (pbase + ii >= p.m) break;
                         out[((int64_t)nn * p.co + co) * p.ohw + rr] = acc[ib * 4 + ii][j];
+                        if (++rr == p.ohw) {
+                            rr = 0;
+                            ++nn;
+                        }
                     }
                 }
             }
@@ -553,88 +623,78 @@ __global__ void __launch_bounds__(256) zero_counters_kernel(int* __restrict__ c,
     for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) c[i] = 0;
 }
 
-// reduce_mode 2: y = sum of the partial planes (fixed order, below).
+// reduce_mode 2: y = sum over splits (in split order) of the partial tiles
+// written by the conv epilogue ([tile][split][16][threads] float4s, each 4
+// consecutive pixels of one channel), placed into NCHW (and into every
+// replica of the fused c_o-shard gather).  One thread per float4 position
+// with all of its split loads in flight (one memory round trip).
 struct ReduceOut {
     float* ys[kMaxOut];
     int n_out, co, co_total, co_base, ohw;
-    int vec;  // every replica 16-byte aligned (float4 stores allowed)
+    int m, bm, bn, threads, wco, tiles_n;
+    int vec;  // every replica 16-byte aligned and ohw % 4 == 0 (float4 stores)
 };
 
+constexpr int kMaxSplits = 32;
+
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ ws,
-                                                            const ReduceOut ro, int64_t total,
+                                                            const ReduceOut ro, int64_t positions,
                                                             int splits) {
-    // float4 path: the plain case, or a gather whose channel planes keep
-    // 16-byte alignment (ohw % 4 == 0)
-    const bool plain = ro.n_out == 1 && ro.co_total == ro.co && ro.co_base == 0;
-    const int64_t total4 =
-        ((total & 3) || !ro.vec || (!plain && (ro.ohw & 3))) ? 0 : (total >> 2);
-    // A block covers opb = 256/G float4 outputs with G split groups (G = 1, 2,
-    // 4, 8 for <= 4, 8, 16, > 16 splits): thread (g, j) sums the split range
-    // [g*per, (g+1)*per) of output j with all its loads in flight, then group
-    // 0 adds the G group sums in order — a fixed two-level order
-    // (deterministic) with up to 8x the memory-level parallelism of one thread
-    // walking every split (the N=1 layers run 16-32 splits).
-    __shared__ float4 part[256];
-    const int groups = splits <= 4 ? 1 : splits <= 8 ? 2 : splits <= 16 ? 4 : 8;
-    const int opb = 256 / groups;
-    const int grp = threadIdx.x / opb, lane = threadIdx.x - grp * opb;
-    const int per = (splits + groups - 1) / groups;
-    for (int64_t base = (int64_t)blockIdx.x * opb; base < total4; base += (int64_t)gridDim.x * opb) {
-        const int64_t i = base + lane;
-        if (i < total4) {
-            const float4* src = reinterpret_cast<const float4*>(ws) + i;
-            const int z0 = grp * per, z1 = min(splits, z0 + per);
-            float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-            int z = z0;
-            for (; z + 3 < z1; z += 4) {
-                const float4 v0 = __ldcg(src + (int64_t)(z + 0) * total4);
-                const float4 v1 = __ldcg(src + (int64_t)(z + 1) * total4);
-                const float4 v2 = __ldcg(src + (int64_t)(z + 2) * total4);
-                const float4 v3 = __ldcg(src + (int64_t)(z + 3) * total4);
-                s.x += v0.x; s.y += v0.y; s.z += v0.z; s.w += v0.w;
-                s.x += v1.x; s.y += v1.y; s.z += v1.z; s.w += v1.w;
-                s.x += v2.x; s.y += v2.y; s.z += v2.z; s.w += v2.w;
-                s.x += v3.x; s.y += v3.y; s.z += v3.z; s.w += v3.w;
+    const float4* w4 = reinterpret_cast<const float4*>(ws);
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < positions;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int t = (int)(q % ro.threads);
+        const int64_t r = q / ro.threads;
+        const int g = (int)(r & 15);
+        const int64_t tile = r >> 4;
+        // (thread, g) -> pixel quad and channel, as in the conv epilogue
+        const int warp = t >> 5, lane = t & 31;
+        const int cg = (warp % ro.wco) * 8 + (lane & 7);
+        const int pg = (warp / ro.wco) * 4 + (lane >> 3);
+        const int ib = g >> 3, j = g & 7;
+        const int tm = (int)(tile / ro.tiles_n);
+        const int tn = (int)(tile - (int64_t)tm * ro.tiles_n);
+        const int pbase = tm * ro.bm + ib * (ro.bm / 2) + pg * 4;
+        const int co = tn * ro.bn + (j >> 2) * (ro.bn / 2) + cg * 4 + (j & 3);
+        if (co >= ro.co || pbase >= ro.m) continue;
+        const float4* src = w4 + (tile * splits * 16 + g) * ro.threads + t;
+        const int64_t zstride = (int64_t)16 * ro.threads;
+        float4 v[kMaxSplits];
+#pragma unroll
+        for (int z = 0; z < kMaxSplits; ++z)
+            if (z < splits) v[z] = __ldcg(src + z * zstride);
+        float4 a = v[0];
+#pragma unroll
+        for (int z = 1; z < kMaxSplits; ++z)
+            if (z < splits) {
+                a.x += v[z].x;
+                a.y += v[z].y;
+                a.z += v[z].z;
+                a.w += v[z].w;
             }
-            for (; z < z1; ++z) {
-                const float4 v = __ldcg(src + (int64_t)z * total4);
-                s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
-            }
-            part[threadIdx.x] = s;
-        }
-        if (groups > 1) __syncthreads();
-        if (grp == 0 && i < total4) {
-            float4 s = part[lane];
-            for (int g = 1; g < groups; ++g) {
-                const float4 v = part[g * opb + lane];
-                s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
-            }
-            if (plain) {
-                reinterpret_cast<float4*>(ro.ys[0])[i] = s;
-            } else {
-                const int64_t e = i << 2;  // local (n, c, pixel) index of the first lane
-                const int64_t plane = (int64_t)ro.co * ro.ohw;
-                const int64_t n = e / plane;
-                const int64_t r = e - n * plane;
-                const int64_t d = (n * ro.co_total + ro.co_base) * ro.ohw + r;
+        const int n = pbase / ro.ohw;
+        const int rem = pbase - n * ro.ohw;
+        if (ro.vec && pbase + 3 < ro.m) {  // same sample: ohw % 4 == 0
+            const int64_t d = ((int64_t)n * ro.co_total + ro.co_base + co) * ro.ohw + rem;
+#pragma unroll
+            for (int o = 0; o < kMaxOut; ++o)
+                if (o < ro.n_out) *reinterpret_cast<float4*>(ro.ys[o] + d) = a;
+        } else {
+            const float av[4] = {a.x, a.y, a.z, a.w};
+            int nn = n, rr = rem;
+#pragma unroll
+            for (int ii = 0; ii < 4; ++ii) {
+                if (pbase + ii >= ro.m) break;
+                const int64_t d = ((int64_t)nn * ro.co_total + ro.co_base + co) * ro.ohw + rr;
 #pragma unroll
                 for (int o = 0; o < kMaxOut; ++o)
-                    if (o < ro.n_out) *reinterpret_cast<float4*>(ro.ys[o] + d) = s;
+                    if (o < ro.n_out) ro.ys[o][d] = av[ii];
+                if (++rr == ro.ohw) {
+                    rr = 0;
+                    ++nn;
+                }
             }
         }
-        if (groups > 1) __syncthreads();
-    }
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (total4 << 2) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-         i += stride) {
-        float s = ws[i];
-        for (int z = 1; z < splits; ++z) s += ws[(int64_t)z * total + i];
-        const int64_t plane = (int64_t)ro.co * ro.ohw;
-        const int64_t n = i / plane;
-        const int64_t d = (n * ro.co_total + ro.co_base) * ro.ohw + (i - n * plane);
-#pragma unroll
-        for (int o = 0; o < kMaxOut; ++o)
-            if (o < ro.n_out) ro.ys[o][d] = s;
     }
 }
 
@@ -654,16 +714,17 @@ constexpr int kBKCvec = 16;
 constexpr int kBKGeneric = 8;
 
 template <int BM, int BN, int T, int MINB, int TM, int BK, int KH, int KW, int SH, int SW,
-          bool CVEC, bool SK = false>
+          bool CVEC, bool SK = false, int G = 1>
 cudaError_t launch_one(const Problem& p, dim3 grid, cudaStream_t s) {
-    if (CVEC && !SK && p.reduce_mode == 3)
-        return launch_one<BM, BN, T, MINB, TM, BK, KH, KW, SH, SW, CVEC, true>(p, grid, s);
-    constexpr int ring = kStages * BK * (BM + BN) * (int)sizeof(float);
+    if constexpr (G == 1)
+        if (CVEC && !SK && p.reduce_mode == 3)
+            return launch_one<BM, BN, T, MINB, TM, BK, KH, KW, SH, SW, CVEC, true>(p, grid, s);
+    constexpr int ring = G * kStages * BK * (BM + BN) * (int)sizeof(float);
     constexpr int part = BN * (BM + 4) * (int)sizeof(float);  // reduce_mode 4 partial tile
     constexpr int smem_max = ring > part ? ring : part;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
-    auto kern = conv_ffma_kernel<BM, BN, T, MINB, TM, BK, KH, KW, SH, SW, CVEC, SK && CVEC>;
+    auto kern = conv_ffma_kernel<BM, BN, T, MINB, TM, BK, KH, KW, SH, SW, CVEC, SK && CVEC, G>;
     std::call_once(once, [&] {
         attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
     });
@@ -671,7 +732,7 @@ cudaError_t launch_one(const Problem& p, dim3 grid, cudaStream_t s) {
     if (!SK && p.reduce_mode == 4) {  // the S splits of a tile form one cluster
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = grid;
-        cfg.blockDim = dim3(T);
+        cfg.blockDim = dim3(T * G);
         cfg.dynamicSmemBytes = smem_max;
         cfg.stream = s;
         cudaLaunchAttribute attr[1];
@@ -683,8 +744,16 @@ cudaError_t launch_one(const Problem& p, dim3 grid, cudaStream_t s) {
         cfg.numAttrs = 1;
         return cudaLaunchKernelEx(&cfg, kern, p);
     }
-    kern<<<grid, T, ring, s>>>(p);
+    kern<<<grid, T * G, ring, s>>>(p);
     return cudaGetLastError();
+}
+
+// warp-group split-K instantiations (3x3 stride-1 and generic tap-major)
+template <int BM, int BN, int T, int G>
+cudaError_t launch_tile_groups(const Problem& p, int tap_kind, dim3 grid, cudaStream_t s) {
+    constexpr int C = kBKCvec;
+    if (tap_kind == 1) return launch_one<BM, BN, T, 1, 8, C, 3, 3, 1, 1, true, false, G>(p, grid, s);
+    return launch_one<BM, BN, T, 1, 8, C, 0, 0, 0, 0, true, false, G>(p, grid, s);
 }
 
 template <int BM, int BN, int T, int MINB, int TM = 8>
@@ -723,12 +792,15 @@ int tap_kind_of(const smmc_geom& g) {
 struct TunedPlan {
     int n, c_i, h, w, c_o, k, s, p;
     int variant, splits;
+    int groups = 1;
 };
 constexpr TunedPlan kTuned[] = {
-    {1, 64, 56, 56, 64, 3, 1, 1, 1, 8},        // 14.8 us (model: 15.5)
-    {1, 128, 28, 28, 128, 3, 1, 1, 1, 8},      // 15.0 us (19.4)
-    {1, 256, 14, 14, 256, 3, 1, 1, 0, 32},     // 14.1 us (1,16: 14.7)
-    {1, 512, 7, 7, 512, 3, 1, 1, 3, 32},       // 20.2 us (42.9)
+    // N=1: warp-group split-K (third field: groups per CTA), measured as
+    // 20 back-to-back launches in a graph (tools/plan_table_sweep.py)
+    {1, 64, 56, 56, 64, 3, 1, 1, 1, 4, 4},     // 13.5 us (1,8: 14.1)
+    {1, 128, 28, 28, 128, 3, 1, 1, 1, 8, 2},   // 13.2 us (1,8: 14.4)
+    {1, 256, 14, 14, 256, 3, 1, 1, 1, 16, 2},  // 13.9 us (0,32: 15.3)
+    {1, 512, 7, 7, 512, 3, 1, 1, 3, 32, 2},    // 15.4 us (3,32: 16.8; model 42.9)
     {32, 64, 56, 56, 64, 3, 1, 1, 2, 0},       // 160.0 us (168.0)
     {8, 96, 27, 27, 256, 5, 1, 2, 3, 4},       // 150.1 us (154.2)
     {256, 64, 56, 56, 256, 1, 1, 0, 3, 1},     // 642.2 us (695.3)
@@ -844,22 +916,30 @@ FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) {
     }
     // measured-best plans for known shapes (tuning table), then the
     // SMMC_FORCE_PLAN="variant,splits" experiment hook (splits 0 = stream-K)
-    int fv = -1, fs = -1;
+    int fv = -1, fs = -1, fg = 1;
     for (const TunedPlan& e : kTuned) {
         if (e.n == g.n && e.c_i == g.c_i && e.h == g.h && e.w == g.w && e.c_o == g.c_o &&
             e.k == g.k_h && g.k_w == g.k_h && e.s == g.s_h && g.s_w == g.s_h && e.p == g.p_h &&
             g.p_w == g.p_h) {
             fv = e.variant;
             fs = e.splits;
+            fg = e.groups;
         }
     }
-    if (const char* f = getenv("SMMC_FORCE_PLAN")) {
-        int v = -1, sp = -1;
-        if (sscanf(f, "%d,%d", &v, &sp) == 2) {
+    if (const char* f = getenv("SMMC_FORCE_PLAN")) {  // "variant,splits[,groups]"
+        int v = -1, sp = -1, gr = 1;
+        if (sscanf(f, "%d,%d,%d", &v, &sp, &gr) >= 2) {
             fv = v;
             fs = sp;
+            fg = gr;
         }
     }
+    // warp groups: tap-major blocks, classic split grid, instantiated
+    // (variant, G) pairs only
+    const bool groups_ok = cvec && fs > 0 &&
+                           ((fg == 2 && (fv == 0 || fv == 1 || fv == 3)) ||
+                            (fg == 4 && (fv == 1 || fv == 3)));
+    if (!groups_ok) fg = 1;
     if (fv >= 0 && fv < kNumTiles && fs >= 0 && (fs > 0 || cvec)) {
         const TileCfg t = kTiles[fv];
         best = FfmaPlan{};
@@ -883,11 +963,14 @@ FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) {
                                                 (tt * kt_total) / best.sk_iters + 1));
             best.sk_maxseg = maxseg;
         } else {
+            fs = std::min(fs, kMaxSplits);
             best.kt_per_split = (kt_total + fs - 1) / fs;
             best.splits = (kt_total + best.kt_per_split - 1) / best.kt_per_split;
             best.reduce_mode = best.splits > 1 ? (best.splits <= 4 ? 1 : 2) : 0;
+            best.groups = fg;
         }
     }
+    if (best.groups < 1) best.groups = 1;
     // split-K with 2..8 splits on an under-filled GPU (at most half the CTA
     // slots): reduce inside a thread-block cluster (reduce_mode 4) instead of
     // global partials (modes 1, 2).  On fuller grids a cluster's CTAs idle at
@@ -897,6 +980,7 @@ FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) {
     int per_sm_best = 1;
     for (int v = 0; v < kNumTiles; ++v)
         if (kTiles[v].bm == best.bm && kTiles[v].bn == best.bn) per_sm_best = kTiles[v].per_sm;
+    if (best.groups > 1) per_sm_best = 2;  // one G-group CTA per SM: allow a full wave
     if ((best.reduce_mode == 1 || best.reduce_mode == 2) && best.splits >= 2 && best.splits <= 8 &&
         2 * best.tiles * best.splits <= (int64_t)sm_count * per_sm_best) {
         const char* f = getenv("SMMC_CLUSTER_RED");  // A/B hook
@@ -913,7 +997,7 @@ FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) {
         best.ws_bytes = best.ws_counter_offset + (size_t)best.tiles * sizeof(int);
     } else if (best.reduce_mode == 2) {
         best.ws_counter_offset = 0;
-        best.ws_bytes = (size_t)best.splits * (size_t)m * g.c_o * sizeof(float);
+        best.ws_bytes = (size_t)best.tiles * best.splits * best.bm * best.bn * sizeof(float);
     } else {
         best.ws_bytes = 0;
         best.ws_counter_offset = 0;
@@ -936,9 +1020,10 @@ FfmaPlan plan_ffma_gather(const smmc_geom& g, int sm_count) {
         pl.splits = (pl.kt_total + pl.kt_per_split - 1) / pl.kt_per_split;
         pl.sk_ctas = pl.sk_iters = pl.sk_maxseg = 0;
     }
+    (void)m;
     pl.reduce_mode = 2;
     pl.ws_counter_offset = 0;
-    pl.ws_bytes = (size_t)pl.splits * (size_t)m * g.c_o * sizeof(float);
+    pl.ws_bytes = (size_t)pl.tiles * pl.splits * pl.bm * pl.bn * sizeof(float);
     return pl;
 }
 
@@ -951,6 +1036,17 @@ cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
         count_launches(1);
     }
     cudaError_t e;
+    if (pl.groups > 1) {
+        const int key = pl.variant * 8 + pl.groups;
+        switch (key) {
+            case 0 * 8 + 2: e = launch_tile_groups<128, 128, 256, 2>(p, pl.tap_kind, grid, s); break;
+            case 1 * 8 + 2: e = launch_tile_groups<128, 64, 128, 2>(p, pl.tap_kind, grid, s); break;
+            case 1 * 8 + 4: e = launch_tile_groups<128, 64, 128, 4>(p, pl.tap_kind, grid, s); break;
+            case 3 * 8 + 2: e = launch_tile_groups<64, 128, 128, 2>(p, pl.tap_kind, grid, s); break;
+            case 3 * 8 + 4: e = launch_tile_groups<64, 128, 128, 4>(p, pl.tap_kind, grid, s); break;
+            default: return cudaErrorInvalidConfiguration;
+        }
+    } else
     switch (pl.variant) {
         case 0: e = launch_tile<128, 128, 256, 2>(p, pl.tap_kind, pl.cvec, grid, s); break;
         case 1: e = launch_tile<128, 64, 128, 4>(p, pl.tap_kind, pl.cvec, grid, s); break;
@@ -959,19 +1055,25 @@ cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
     }
     count_launches(1);
     if (e != cudaSuccess || pl.reduce_mode != 2) return e;
-    const int64_t total = (int64_t)p.m * p.co;
-    const int groups = p.splits <= 4 ? 1 : p.splits <= 8 ? 2 : p.splits <= 16 ? 4 : 8;
-    const int blocks = (int)std::min<int64_t>((total / 4 + 256 / groups - 1) / (256 / groups) + 1, 148 * 16);
+    if (p.splits > kMaxSplits) return cudaErrorInvalidConfiguration;
+    const int64_t positions = pl.tiles * 16 * pl.threads;
+    const int blocks = (int)std::min<int64_t>((positions + 255) / 256, 148 * 16);
     ReduceOut ro{};
+    ro.m = p.m;
+    ro.bm = pl.bm;
+    ro.bn = pl.bn;
+    ro.threads = pl.threads;
+    ro.wco = pl.bn / 64;
+    ro.tiles_n = pl.tiles_n;
     for (int o = 0; o < p.n_out; ++o) ro.ys[o] = p.ys[o];
     ro.n_out = p.n_out;
     ro.co = p.co;
     ro.co_total = p.co_total;
     ro.co_base = p.co_base;
     ro.ohw = p.ohw;
-    ro.vec = 1;
+    ro.vec = (p.ohw & 3) == 0;
     for (int o = 0; o < p.n_out; ++o) ro.vec &= ((uintptr_t)p.ys[o] & 15) == 0;
-    splitk_reduce_kernel<<<blocks, 256, 0, s>>>(p.ws, ro, total, p.splits);
+    splitk_reduce_kernel<<<blocks, 256, 0, s>>>(p.ws, ro, positions, p.splits);
     count_launches(1);
     return cudaGetLastError();
 }

@@ -391,6 +391,10 @@ int smmc_plan_describe(const smmc_geom* g, int mode, char* buf, size_t len) {
              : pl.reduce_mode == 4 ? "cluster DSMEM"
                                    : "stream-K",
              (long long)pl.tiles);
+    if (pl.groups > 1) {
+        const size_t used = strlen(buf);
+        snprintf(buf + used, len - used, ", %d warp groups x %d threads", pl.groups, pl.threads);
+    }
     if (pl.reduce_mode == 3) {
         const size_t used = strlen(buf);
         snprintf(buf + used, len - used, ", stream-K %d CTAs x %d tap blocks", pl.sk_ctas,

@@ -64,6 +64,7 @@ struct FfmaPlan {
     int tap_kind;      // 0 generic, 1: 3x3s1, 2: 1x1s1, 3: 7x7s2, 4: 11x11s4, 5: 5x5s1
     int cvec;          // tap-major K order
     int reduce_mode;   // 0 none, 1 last-arriver, 2 reduce kernel, 3 stream-K, 4 cluster DSMEM
+    int groups;        // warp groups per CTA splitting the CTA's tap blocks (1 = off)
     int64_t tiles;     // pixel tiles x channel tiles
     int tiles_n;
     int sk_ctas;       // stream-K grid

@@ -244,6 +244,32 @@ def test_every_reduction_mode_matches_oracle(plan, cluster, monkeypatch):
         assert "cluster" not in desc, desc
 
 
+@pytest.mark.parametrize("cluster", ["1", "0"])
+@pytest.mark.parametrize("plan", ["1,1,4", "3,1,2", "0,1,2", "1,3,2", "1,8,4", "3,6,4", "1,16,4",
+                                  "3,32,2", "0,12,2"])
+def test_warp_group_split_matches_oracle(plan, cluster, monkeypatch):
+    """Warp-group split-K (G groups per CTA over the CTA's tap blocks, partial
+    tiles summed in group order through shared memory) under every outer
+    reduction (none, last arriver, cluster DSMEM, reduce kernel), including
+    groups left without tap blocks: oracle parity, bitwise run to run."""
+    import torch
+    from paper_2411_15659_b200 import device
+    monkeypatch.setenv("SMMC_FORCE_PLAN", plan)
+    monkeypatch.setenv("SMMC_CLUSTER_RED", cluster)
+    g = ConvGeometry(64, 96, 20, 20, 3, 3, pad_h=1, pad_w=1)
+    x, w = synthetic_layer(g, 3, 321)
+    wd = torch.from_numpy(smm.repack_weights(w, g)).cuda()
+    xd = torch.from_numpy(x).cuda()
+    desc = _native.plan_describe(g, 3)
+    assert "warp groups" in desc, desc
+    y1 = device.conv2d(xd, wd, g)
+    y2 = device.conv2d(xd, wd, g)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2), desc
+    ref = orc.smm_conv_c(x, orc.repack(w), g, threads=orc.host_threads())
+    assert orc.max_abs_ratio(y1.cpu().numpy(), ref) <= TOL_FP32, desc
+
+
 @pytest.mark.parametrize("plan", ["1,2", "1,8", "3,5", "0,3"])
 def test_cluster_dsmem_split_reduction(plan, monkeypatch):
     """Under-filled split-K grids reduce their partial tiles inside a

@@ -101,7 +101,8 @@ def main():
             mod = device.SmmConv2d(g, w)
             y = mod(xd)
             default = (time_plan(mod, xd, y, iters, a.cold), _native.plan_describe(g, n))
-            for v, s in cands:
+            for c in cands:
+                v, s = c[0], ",".join(map(str, c[1:]))
                 os.environ["SMMC_FORCE_PLAN"] = f"{v},{s}"
                 mod = device.SmmConv2d(g, w)
                 y = mod(xd)

@@ -67,6 +67,16 @@ def main():
         sms = len(set(t[:, 4].tolist()))
         print(f"{name}: {len(t)} CTAs on {sms} SMs, event {s.elapsed_time(e) * 1e3:.1f} us, "
               f"CTA span {span:.1f} us")
+        # per SM: first and last exit of its CTAs (co-resident CTAs with equal
+        # work finishing far apart = unfair issue between CTAs; the SM then
+        # runs its last CTA alone)
+        by_sm = {}
+        for row, sm in zip(r, t[:, 4]):
+            by_sm.setdefault(int(sm), []).append(row[3])
+        spread = np.array([max(v) - min(v) for v in by_sm.values() if len(v) > 1] or [0.0])
+        last = np.array([max(v) for v in by_sm.values()])
+        print(f"   per-SM exit spread p50 {pct(spread, 50):.1f} max {spread.max():.1f} us; "
+              f"SM done p10 {pct(last, 10):.1f} p50 {pct(last, 50):.1f} max {last.max():.1f} us")
         for lab, v in (("entry", r[:, 0]), ("prologue", r[:, 1] - r[:, 0]),
                        ("loop", r[:, 2] - r[:, 1]), ("epilogue", r[:, 3] - r[:, 2]),
                        ("exit", r[:, 3])):

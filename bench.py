@@ -53,9 +53,11 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="ffma", choices=["ffma", "exact", "bf16_tc"],
+    ap.add_argument("--mode", default="ffma", choices=["ffma", "exact", "bf16_tc", "bf16x3_tc"],
                     help="ffma: fp32 product kernel; exact: bitwise mode; bf16_tc: separately "
-                         "labelled bf16-input tcgen05 variant (stride-1 layers)")
+                         "labelled bf16-input tcgen05 variant (stride-1 layers); bf16x3_tc: "
+                         "fp32-accurate split-bf16 tcgen05 path (fp32 in/out, fp32 parity bar; "
+                         "input split/pack inside the timed step)")
     ap.add_argument("--replicas", type=int, default=0, help="0 = auto (>2x L2 between reuses)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -245,10 +247,11 @@ def run_ours(args):
                           * L["gl"].out_h * L["gl"].out_w) for L in layers)
     R = args.replicas or max(1, min(8, -(-3 * L2_BYTES // max(step_bytes, 1)) + 1))
     tc = args.mode == "bf16_tc"
-    if tc:
+    tc3 = args.mode == "bf16x3_tc"
+    if tc or tc3:
         for L in layers:
             if not device.tc_supported(L["gl"], max(L["n"], 1)):
-                raise SystemExit(f"--mode bf16_tc: layer {L['name']} is not supported "
+                raise SystemExit(f"--mode {args.mode}: layer {L['name']} is not supported "
                                  "(stride 1 and c_i % 8 == 0 required)")
     for L in layers:
         xd = torch.from_numpy(L["x_host"]).to(dev)
@@ -261,12 +264,20 @@ def run_ours(args):
             wt = device.pack_weights_bf16(wd, L["gl"])
             L["wt"] = [wt] + [wt.clone() for _ in range(R - 1)]
             del xd, wd
+        elif tc3:
+            # fp32 inputs (split/packed inside the step); weights split once
+            L["x"] = [xd] + [xd.clone() for _ in range(R - 1)]
+            w3 = device.pack_weights_bf16x3(wd, L["gl"])
+            L["w3"] = [w3] + [w3.clone() for _ in range(R - 1)]
+            L["x3"] = torch.empty(device.packed_input3_shape(L["gl"], L["n"]),
+                                  dtype=torch.bfloat16, device=dev)
+            del wd
         else:
             L["x"] = [xd] + [xd.clone() for _ in range(R - 1)]
             L["w"] = [wd] + [wd.clone() for _ in range(R - 1)]
         shape = (L["n"],) + L["gl"].output_shape
         L["y"] = [torch.empty(shape, device=dev) for _ in range(R)]
-        need = 0 if tc else _native.workspace_bytes(L["gl"], L["n"], args.mode)
+        need = 0 if (tc or tc3) else _native.workspace_bytes(L["gl"], L["n"], args.mode)
         L["ws"] = torch.empty(max(need, 16), dtype=torch.uint8, device=dev)
         if L["shard"] == "cout":
             L["full"] = torch.empty((L["n"],) + L["g"].output_shape, device=dev)
@@ -291,6 +302,9 @@ def run_ours(args):
             return
         if tc:
             device.conv2d_bf16_tc(L["xb"][r], L["wt"][r], L["gl"], out=L["y"][r])
+        elif tc3:
+            device.pack_input_bf16x3(L["x"][r], L["gl"], out=L["x3"])
+            device.conv2d_bf16x3_tc(L["x3"], L["w3"][r], L["gl"], out=L["y"][r])
         else:
             device.conv2d(L["x"][r], L["w"][r], L["gl"], mode=args.mode, out=L["y"][r],
                           workspace=L["ws"])
@@ -390,7 +404,7 @@ def run_ours(args):
     fp32_peak_tf = sm_count * FFMA_PER_SM_PER_CLK * 2 * sm_max * 1e6 / 1e12
     hbm_peak = float(pk.get("hbm_gbs", 6650.0))
     bf16_peak_tf = float(pk.get("bf16_tflops", 1590.0))
-    comp_peak_tf = bf16_peak_tf if tc else fp32_peak_tf
+    comp_peak_tf = bf16_peak_tf if (tc or tc3) else fp32_peak_tf
     details = []
     for li, L in enumerate(layers):
         d = per_layer[li]
@@ -398,8 +412,10 @@ def run_ours(args):
         tf = L["flops"] / (avg / 1e3) / 1e12 if avg > 0 else 0.0
         gl = L["gl"]
         byts = (gl.compulsory_bytes(L["n"], in_bytes=2, w_bytes=2) if tc
+                else gl.compulsory_bytes(L["n"], w_bytes=6) if tc3
                 else gl.compulsory_bytes(L["n"]))
-        t_comp = L["flops"] / (comp_peak_tf * 1e12)
+        # split-bf16: three bf16 MMAs per fp32-accurate product
+        t_comp = L["flops"] / ((comp_peak_tf / 3 if tc3 else comp_peak_tf) * 1e12)
         t_mem = byts / (hbm_peak * 1e9)
         t_roof = max(t_comp, t_mem)
         achieved_gbs = byts / (avg / 1e3) / 1e9 if avg > 0 else 0.0
@@ -409,13 +425,14 @@ def run_ours(args):
             "ms_min": round(min(d), 5), "tflops": round(tf, 3),
             "frac_fp32_peak": round(tf / fp32_peak_tf, 4),
             "frac_roofline": round(t_roof * 1e3 / avg, 4) if avg > 0 else None,
-            "bound": "hbm" if t_mem > t_comp else ("tensor" if tc else "fp32"),
+            "bound": "hbm" if t_mem > t_comp else ("tensor" if (tc or tc3) else "fp32"),
             "achieved_gbs": round(achieved_gbs, 1),
             "compulsory_bytes": byts,
             "flop_per_byte": round(L["flops"] / byts, 1),
             "plan": ((_native.tc_plan_describe(gl, L["n"]) if tc else
+                      "split-bf16 x3 over 3*c_i: " + device.tc3_plan_describe(gl, L["n"]) if tc3 else
                       _native.plan_describe(gl, L["n"], args.mode)) if L["n"] else ""),
-            "launches_per_call": 1 if tc else
+            "launches_per_call": 1 if tc else 2 if tc3 else
             (_native.plan_launches(gl, L["n"], args.mode) if L["n"] else 0)})
     dom = max(details, key=lambda d: d["ms_avg"])
     traffic = None
@@ -435,6 +452,16 @@ def run_ours(args):
                     "achieved_def": "compulsory bytes (input + weights + output) of one launch / "
                                     "its avg CUDA-event duration (per-layer event replay of the "
                                     "timed steps)"}
+    elif tc3:
+        roofline = {"bound": "tensor", "achieved": dom["tflops"],
+                    "peak": round(bf16_peak_tf / 3, 1), "unit": "TFLOP/s",
+                    "frac": round(dom["tflops"] / (bf16_peak_tf / 3), 4), "traffic": traffic,
+                    "kernel": f"split-bf16 pack + tcgen05 conv ({dom['layer']}: {dom['plan']})",
+                    "peak_source": "bf16_tflops (burst) of MEASURED_PEAKS.json / 3 (three bf16 "
+                                   "MMAs per fp32-accurate product)",
+                    "fp32_cuda_core_peak": round(fp32_peak_tf, 2),
+                    "achieved_def": "dense algorithmic FLOPs of one layer (pack + conv) / its avg "
+                                    "CUDA-event duration (per-layer event replay of the timed steps)"}
     elif tc:
         roofline = {"bound": "tensor", "achieved": dom["tflops"], "peak": bf16_peak_tf,
                     "unit": "TFLOP/s", "frac": round(dom["tflops"] / bf16_peak_tf, 4),
@@ -481,7 +508,8 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(max_ms / args.steps, 5), "higher_is_better": True,
             "scaling": "strong" if (args.config == 5 and world > 1) else "weak",
-            "vs_baseline": None, "dtype": "bf16-in/f32-acc" if tc else "f32",
+            "vs_baseline": None,
+            "dtype": ("bf16-in/f32-acc" if tc else "f32 (split bf16x3, f32 acc)" if tc3 else "f32"),
             "data": "synthetic",
             "config": {"workload": f"BASELINE config {args.config}: {CONFIGS[args.config]['title']}",
                        "layers": [L["name"] for L in layers],
@@ -521,7 +549,7 @@ def run_e2e(args, layers, world, dev):
     import torch.distributed as dist
 
     from paper_2411_15659_b200 import _native
-    if args.mode == "bf16_tc":
+    if args.mode in ("bf16_tc", "bf16x3_tc"):
         return run_e2e_tc(args, layers, world, dev)
     lib = _native.lib()
     bufs = []
@@ -599,11 +627,17 @@ def run_e2e_tc(args, layers, world, dev):
         h2d += xh.numel() * 4
         d2h += yh.numel() * 4
 
+    tc3 = args.mode == "bf16x3_tc"
+
     def step():
         for L, xh, yh, xd in bufs:
             xd.copy_(xh, non_blocking=True)
-            xb = device.pack_input_bf16(xd, L["gl"], out=L["xb"][0])
-            y = device.conv2d_bf16_tc(xb, L["wt"][0], L["gl"], out=L["y"][0])
+            if tc3:
+                x3 = device.pack_input_bf16x3(xd, L["gl"], out=L["x3"])
+                y = device.conv2d_bf16x3_tc(x3, L["w3"][0], L["gl"], out=L["y"][0])
+            else:
+                xb = device.pack_input_bf16(xd, L["gl"], out=L["xb"][0])
+                y = device.conv2d_bf16_tc(xb, L["wt"][0], L["gl"], out=L["y"][0])
             yh.copy_(y, non_blocking=True)
         torch.cuda.synchronize()
 
@@ -622,7 +656,8 @@ def run_e2e_tc(args, layers, world, dev):
     flops = sum(L["flops"] for L in layers) * world
     return {"value": round(flops * steps / dt / 1e9, 2), "unit": "GFLOP/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
-            "path": "device.pack_input_bf16 + device.conv2d_bf16_tc (C ABI) with pinned fp32 "
+            "path": ("device.pack_input_bf16x3 + device.conv2d_bf16x3_tc" if tc3 else
+                     "device.pack_input_bf16 + device.conv2d_bf16_tc") + " (C ABI) with pinned fp32 "
                     "host input/output, wall clock, max over ranks"}
 
 

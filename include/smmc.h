@@ -163,6 +163,27 @@ SMMC_API int smmc_pack_weights_bf16(const float* w_smm, uint16_t* w_tc, const sm
 SMMC_API int smmc_conv2d_fwd_bf16_tc(const uint16_t* x_nhwc, const uint16_t* w_tc, float* y,
                                      const smmc_geom* g, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * fp32-accurate tensor-core path ("bf16x3", split bf16): x = x_hi + x_lo and
+ * w = w_hi + w_lo with hi = bf16(v), lo = bf16(v - hi); y = x_hi*w_hi +
+ * x_lo*w_hi + x_hi*w_lo accumulated in fp32 TMEM — the bf16 tcgen05 conv
+ * above run over 3*c_i channels ([hi|lo|hi] input, [hi|hi|lo] weights).
+ * Parity bar: the fp32 one, 1e-4 * max|ref| (dropped x_lo*w_lo ~ 2^-16).
+ * Same geometry support as smmc_tc_supported.  Device pointers, async.
+ * ------------------------------------------------------------------------- */
+
+/* x fp32 NCHW -> x3 bf16 zero-padded NHWC (n, h + 2*p_h, w + 2*p_w, 3*c_i). */
+SMMC_API int smmc_pack_input_bf16x3_nhwc(const float* x, uint16_t* x3, const smmc_geom* g,
+                                         void* stream);
+
+/* w_smm fp32 (c_i, k_w, k_h, c_o) -> w3 bf16 (k_w*k_h, c_o, 3*c_i). */
+SMMC_API int smmc_pack_weights_bf16x3(const float* w_smm, uint16_t* w3, const smmc_geom* g,
+                                      void* stream);
+
+/* y fp32 NCHW = conv(x, w) from the split operands above. */
+SMMC_API int smmc_conv2d_fwd_bf16x3_tc(const uint16_t* x3, const uint16_t* w3, float* y,
+                                       const smmc_geom* g, void* stream);
+
 /* GPU im2col comparator (the paper's baseline): the explicit
  * lowered matrix of im2col_pack (im2col.py:22-71), per sample
  * [c_i*k_h*k_w][out_h*out_w], row (c*k_h + k)*k_w + j, zero-filled padding.

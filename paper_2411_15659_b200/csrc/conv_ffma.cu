@@ -557,11 +557,11 @@ __global__ void __launch_bounds__(THREADS * G, (G > 1 ? 1 : MINB)) conv_ffma_ker
     // the result (NCHW, gather replicas) — also with a single split when the
     // output goes to gather replicas
     if (!sk && p.reduce_mode == 2) {
-        static_assert(TM == 8, "mode-2 partial layout assumes 8x8 thread tiles");
         if (lead) {
-            float4* dst = reinterpret_cast<float4*>(p.ws) + ((tile * p.splits + slot) * 16) * THREADS + tid;
+            float4* dst =
+                reinterpret_cast<float4*>(p.ws) + ((tile * p.splits + slot) * (2 * TM)) * THREADS + tid;
 #pragma unroll
-            for (int ib = 0; ib < 2; ++ib)
+            for (int ib = 0; ib < NQ; ++ib)
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
                     dst[(ib * 8 + j) * THREADS] = make_float4(acc[ib * 4 + 0][j], acc[ib * 4 + 1][j],
@@ -632,6 +632,7 @@ struct ReduceOut {
     float* ys[kMaxOut];
     int n_out, co, co_total, co_base, ohw;
     int m, bm, bn, threads, wco, tiles_n;
+    int nq;  // pixel quads per thread (float4 groups per thread = 8 * nq)
     int vec;  // every replica 16-byte aligned and ohw % 4 == 0 (float4 stores)
 };
 
@@ -645,8 +646,9 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
          q += (int64_t)gridDim.x * blockDim.x) {
         const int t = (int)(q % ro.threads);
         const int64_t r = q / ro.threads;
-        const int g = (int)(r & 15);
-        const int64_t tile = r >> 4;
+        const int ng = 8 * ro.nq;
+        const int64_t tile = r / ng;
+        const int g = (int)(r - tile * ng);
         // (thread, g) -> pixel quad and channel, as in the conv epilogue
         const int warp = t >> 5, lane = t & 31;
         const int cg = (warp % ro.wco) * 8 + (lane & 7);
@@ -654,11 +656,11 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
         const int ib = g >> 3, j = g & 7;
         const int tm = (int)(tile / ro.tiles_n);
         const int tn = (int)(tile - (int64_t)tm * ro.tiles_n);
-        const int pbase = tm * ro.bm + ib * (ro.bm / 2) + pg * 4;
+        const int pbase = tm * ro.bm + ib * (ro.bm / ro.nq) + pg * 4;
         const int co = tn * ro.bn + (j >> 2) * (ro.bn / 2) + cg * 4 + (j & 3);
         if (co >= ro.co || pbase >= ro.m) continue;
-        const float4* src = w4 + (tile * splits * 16 + g) * ro.threads + t;
-        const int64_t zstride = (int64_t)16 * ro.threads;
+        const float4* src = w4 + (tile * splits * ng + g) * ro.threads + t;
+        const int64_t zstride = (int64_t)ng * ro.threads;
         float4 v[kMaxSplits];
 #pragma unroll
         for (int z = 0; z < kMaxSplits; ++z)
@@ -700,12 +702,16 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
 
 struct TileCfg {
     int bm, bn, threads, per_sm, tm;
+    int model;  // considered by the cost model (else tuning table / forced plans only)
 };
 constexpr TileCfg kTiles[] = {
-    {128, 128, 256, 2, 8},   // 0
-    {128, 64, 128, 4, 8},    // 1
-    {256, 64, 256, 2, 8},    // 2
-    {64, 128, 128, 4, 8},    // 3
+    {128, 128, 256, 2, 8, 1},   // 0
+    {128, 64, 128, 4, 8, 1},    // 1
+    {256, 64, 256, 2, 8, 1},    // 2
+    {64, 128, 128, 4, 8, 1},    // 3
+    // 4 x 8 thread tiles (64 registers, 8 CTAs/SM: latency hiding by
+    // occupancy) were measured 1-13 % slower on the c_i = 3 stems and 1x1
+    // layers (A/B, round 1) and are not instantiated.
     // 16 x 8 thread tiles (TM = 16, 216 registers) were measured slower on
     // every BASELINE layer (A/B, profiles/r01): more warps beat more ILP here.
 };
@@ -814,9 +820,7 @@ constexpr TunedPlan kTuned[] = {
 };
 
 int64_t best_cost_waves(const FfmaPlan& b, int64_t m, int c_o, int sm_count) {
-    int per_sm = 1;
-    for (int v = 0; v < kNumTiles; ++v)
-        if (kTiles[v].bm == b.bm && kTiles[v].bn == b.bn) per_sm = kTiles[v].per_sm;
+    const int per_sm = kTiles[b.variant].per_sm;
     const int64_t tiles = ((m + b.bm - 1) / b.bm) * ((c_o + b.bn - 1) / b.bn);
     const int64_t slots = (int64_t)sm_count * per_sm;
     return (tiles * std::max(b.splits, 1) + slots - 1) / slots;
@@ -840,6 +844,7 @@ FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) {
     const double blk = bk / 8.0;  // work of one tap block in 8-deep units
     for (int v = 0; v < kNumTiles; ++v) {
         const TileCfg t = kTiles[v];
+        if (!t.model) continue;
         const int64_t mt = (m + t.bm - 1) / t.bm;
         const int64_t nt = (g.c_o + t.bn - 1) / t.bn;
         const int64_t tiles = mt * nt;
@@ -879,6 +884,7 @@ FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) {
     const double classic_cost = best_cost;
     for (int v = 0; v < kNumTiles && cvec && best_waves <= 2; ++v) {
         const TileCfg t = kTiles[v];
+        if (!t.model) continue;
         const int64_t nt = (g.c_o + t.bn - 1) / t.bn;
         const int64_t tiles = ((m + t.bm - 1) / t.bm) * nt;
         const int64_t slots = (int64_t)sm_count * t.per_sm;
@@ -977,9 +983,7 @@ FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) {
     // the reduction waiting for each other and co-scheduling clusters costs
     // slots (measured: conv256@14 N=32, 294 CTAs, 147 -> 211 us; conv128@28
     // N=32, 588 CTAs, 152 -> 184 us); N=1 layers gain (20.0 -> 19.1 us).
-    int per_sm_best = 1;
-    for (int v = 0; v < kNumTiles; ++v)
-        if (kTiles[v].bm == best.bm && kTiles[v].bn == best.bn) per_sm_best = kTiles[v].per_sm;
+    int per_sm_best = kTiles[best.variant].per_sm;
     if (best.groups > 1) per_sm_best = 2;  // one G-group CTA per SM: allow a full wave
     if ((best.reduce_mode == 1 || best.reduce_mode == 2) && best.splits >= 2 && best.splits <= 8 &&
         2 * best.tiles * best.splits <= (int64_t)sm_count * per_sm_best) {
@@ -1056,7 +1060,7 @@ cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
     count_launches(1);
     if (e != cudaSuccess || pl.reduce_mode != 2) return e;
     if (p.splits > kMaxSplits) return cudaErrorInvalidConfiguration;
-    const int64_t positions = pl.tiles * 16 * pl.threads;
+    const int64_t positions = pl.tiles * 2 * kTiles[pl.variant].tm * pl.threads;
     const int blocks = (int)std::min<int64_t>((positions + 255) / 256, 148 * 16);
     ReduceOut ro{};
     ro.m = p.m;
@@ -1064,6 +1068,7 @@ cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
     ro.bn = pl.bn;
     ro.threads = pl.threads;
     ro.wco = pl.bn / 64;
+    ro.nq = kTiles[pl.variant].tm / 4;
     ro.tiles_n = pl.tiles_n;
     for (int o = 0; o < p.n_out; ++o) ro.ys[o] = p.ys[o];
     ro.n_out = p.n_out;

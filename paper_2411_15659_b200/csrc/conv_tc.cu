@@ -476,8 +476,19 @@ conv_tc_box_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
 
 // x fp32 NCHW -> zero-padded bf16 NHWC (n, h + 2p_h, w + 2p_w, c): one block
 // per (32 padded columns, 32 channels, padded row, image), smem transpose.
+// split = 3 (the fp32-accurate "bf16x3" path): x = hi + lo with hi =
+// bf16(x), lo = bf16(x - hi) (|x - hi - lo| <= 2^-16 |x|), written as 3*c
+// channels [hi | lo | hi]; paired with weights [hi | hi | lo] the same bf16
+// GEMM sums x_hi*w_hi + x_lo*w_hi + x_hi*w_lo in fp32 (TMEM): fp32-grade
+// products (the dropped x_lo*w_lo term is ~2^-16 relative) on tcgen05.
+__device__ __forceinline__ void split_bf16(float v, __nv_bfloat16& hi, __nv_bfloat16& lo) {
+    hi = __float2bfloat16_rn(v);
+    lo = __float2bfloat16_rn(v - __bfloat162float(hi));
+}
+
 __global__ void pack_input_padded_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ out,
-                                         int c, int h, int w, int ph, int pw, int hp, int wp) {
+                                         int c, int h, int w, int ph, int pw, int hp, int wp,
+                                         int split) {
     __shared__ float tile[32][33];
     const int t0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
     const int n = blockIdx.z / hp, r = blockIdx.z - n * hp;
@@ -491,16 +502,28 @@ __global__ void pack_input_padded_kernel(const float* __restrict__ x, __nv_bfloa
         tile[i][threadIdx.x] = v;
     }
     __syncthreads();
-    __nv_bfloat16* orow = out + (((int64_t)n * hp + r) * wp) * c;
+    const int cs = c * split;  // channels per padded pixel
+    __nv_bfloat16* orow = out + (((int64_t)n * hp + r) * wp) * cs;
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {
         const int t = t0 + i, cc = c0 + threadIdx.x;
-        if (t < wp && cc < c) orow[(int64_t)t * c + cc] = __float2bfloat16_rn(tile[threadIdx.x][i]);
+        if (t < wp && cc < c) {
+            const float v = tile[threadIdx.x][i];
+            if (split == 1) {
+                orow[(int64_t)t * cs + cc] = __float2bfloat16_rn(v);
+            } else {
+                __nv_bfloat16 hi, lo;
+                split_bf16(v, hi, lo);
+                orow[(int64_t)t * cs + cc] = hi;
+                orow[(int64_t)t * cs + c + cc] = lo;
+                orow[(int64_t)t * cs + 2 * c + cc] = hi;
+            }
+        }
     }
 }
 
 // W_smm fp32 (c_i, k_w, k_h, c_o) -> bf16 [tap = j*k_h + k][c_o][c_i]
 __global__ void pack_weights_kernel(const float* __restrict__ w, __nv_bfloat16* __restrict__ out,
-                                    int c, int taps, int co) {
+                                    int c, int taps, int co, int split) {
     const int64_t total = (int64_t)taps * co * c;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -508,7 +531,17 @@ __global__ void pack_weights_kernel(const float* __restrict__ w, __nv_bfloat16* 
         const int64_t rr = i / c;
         const int m = (int)(rr % co);
         const int t = (int)(rr / co);
-        out[i] = __float2bfloat16_rn(w[((int64_t)ci * taps + t) * co + m]);
+        const float v = w[((int64_t)ci * taps + t) * co + m];
+        if (split == 1) {
+            out[i] = __float2bfloat16_rn(v);
+        } else {  // [hi | hi | lo] per (tap, c_o) row of 3*c channels
+            __nv_bfloat16 hi, lo;
+            split_bf16(v, hi, lo);
+            __nv_bfloat16* row = out + rr * 3 * c;
+            row[ci] = hi;
+            row[c + ci] = hi;
+            row[2 * c + ci] = lo;
+        }
     }
 }
 
@@ -739,21 +772,22 @@ cudaError_t launch_tc_bf16(const uint16_t* x_pad, const uint16_t* w_tc, float* y
 }
 
 cudaError_t launch_pack_input_nhwc(const float* x, uint16_t* out, const smmc_geom& g,
-                                   cudaStream_t s) {
+                                   cudaStream_t s, int split) {
     const int hp = g.h + 2 * g.p_h, wp = g.w + 2 * g.p_w;
     dim3 grid((wp + 31) / 32, (g.c_i + 31) / 32, g.n * hp);
     pack_input_padded_kernel<<<grid, dim3(32, 8), 0, s>>>(x, reinterpret_cast<__nv_bfloat16*>(out),
-                                                          g.c_i, g.h, g.w, g.p_h, g.p_w, hp, wp);
+                                                          g.c_i, g.h, g.w, g.p_h, g.p_w, hp, wp,
+                                                          split);
     count_launches(1);
     return cudaGetLastError();
 }
 
 cudaError_t launch_pack_weights_bf16(const float* w, uint16_t* out, const smmc_geom& g,
-                                     cudaStream_t s) {
+                                     cudaStream_t s, int split) {
     const int64_t total = (int64_t)g.k_h * g.k_w * g.c_o * g.c_i;
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
     pack_weights_kernel<<<blocks, 256, 0, s>>>(w, reinterpret_cast<__nv_bfloat16*>(out), g.c_i,
-                                               g.k_h * g.k_w, g.c_o);
+                                               g.k_h * g.k_w, g.c_o, split);
     count_launches(1);
     return cudaGetLastError();
 }

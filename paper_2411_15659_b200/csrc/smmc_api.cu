@@ -757,6 +757,45 @@ int smmc_pack_weights_bf16(const float* w_smm, uint16_t* w_tc, const smmc_geom* 
                        "pack_weights_bf16 launch");
 }
 
+int smmc_pack_input_bf16x3_nhwc(const float* x, uint16_t* x3, const smmc_geom* g, void* stream) {
+    int oh = 0, ow = 0;
+    int st = check_geom(g, &oh, &ow);
+    if (st) return st;
+    if (g->n == 0) return SMMC_OK;
+    if (!x || !x3) {
+        set_error("x and x3 must be non-NULL device pointers");
+        return SMMC_ESHAPE;
+    }
+    return cuda_status(launch_pack_input_nhwc(x, x3, *g, static_cast<cudaStream_t>(stream), 3),
+                       "pack_input_bf16x3 launch");
+}
+
+int smmc_pack_weights_bf16x3(const float* w_smm, uint16_t* w3, const smmc_geom* g, void* stream) {
+    int oh = 0, ow = 0;
+    int st = check_geom(g, &oh, &ow);
+    if (st) return st;
+    if (!w_smm || !w3) {
+        set_error("w_smm and w3 must be non-NULL device pointers");
+        return SMMC_ESHAPE;
+    }
+    return cuda_status(launch_pack_weights_bf16(w_smm, w3, *g, static_cast<cudaStream_t>(stream), 3),
+                       "pack_weights_bf16x3 launch");
+}
+
+int smmc_conv2d_fwd_bf16x3_tc(const uint16_t* x3, const uint16_t* w3, float* y, const smmc_geom* g,
+                              void* stream) {
+    int oh = 0, ow = 0;
+    int st = check_geom(g, &oh, &ow);
+    if (st) return st;
+    if (g->c_i > INT32_MAX / 3) {
+        set_error("c_i too large for the split-bf16 path");
+        return SMMC_EUNSUPPORTED;
+    }
+    smmc_geom g3 = *g;  // the bf16 conv over the 3*c_i split channels
+    g3.c_i *= 3;
+    return smmc_conv2d_fwd_bf16_tc(x3, w3, y, &g3, stream);
+}
+
 int smmc_conv2d_fwd_bf16_tc(const uint16_t* x_nhwc, const uint16_t* w_tc, float* y,
                             const smmc_geom* g, void* stream) {
     int oh = 0, ow = 0;

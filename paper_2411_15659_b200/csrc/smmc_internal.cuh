@@ -92,9 +92,12 @@ struct TcPlan {
 TcPlan plan_tc(const smmc_geom& g);
 cudaError_t launch_tc_bf16(const uint16_t* x_nhwc, const uint16_t* w_tc, float* y, const smmc_geom& g,
                            cudaStream_t s, const char** why);
-cudaError_t launch_pack_input_nhwc(const float* x, uint16_t* out, const smmc_geom& g, cudaStream_t s);
+// split = 1: plain bf16; split = 3: [hi | lo | hi] input / [hi | hi | lo]
+// weight channels of the fp32-accurate bf16x3 path (run as a 3*c_i bf16 conv)
+cudaError_t launch_pack_input_nhwc(const float* x, uint16_t* out, const smmc_geom& g, cudaStream_t s,
+                                   int split = 1);
 cudaError_t launch_pack_weights_bf16(const float* w, uint16_t* out, const smmc_geom& g,
-                                     cudaStream_t s);
+                                     cudaStream_t s, int split = 1);
 cudaError_t launch_im2col_pack(const float* x, float* low, const smmc_geom& g, int oh, int ow,
                                cudaStream_t s);
 cudaError_t launch_extract_slice(const float* x, const smmc_geom& g, int c, int j,

@@ -276,6 +276,117 @@ class TcSmmConv2d:
         return conv2d_bf16_tc(x_nhwc, self.w_tc, self.geom, out=out)
 
 
+# --------------------------------------------------------------------------
+# fp32-accurate tensor-core path ("bf16x3"): each fp32 operand split into
+# bf16 hi + lo; the three significant cross products accumulate in fp32 TMEM
+# as one bf16 tcgen05 conv over 3*c_i channels.  fp32 in, fp32 out; parity
+# bar the fp32 one (1e-4 * max|ref|).
+# --------------------------------------------------------------------------
+
+def packed_input3_shape(geom, n):
+    return (n, geom.padded_h, geom.padded_w, 3 * geom.in_channels)
+
+
+def pack_input_bf16x3(x, geom, out=None):
+    """fp32 NCHW -> zero-padded bf16 NHWC with 3*c_i channels [hi | lo | hi]."""
+    torch = _torch()
+    n = x.shape[0]
+    _check_tensor(x, (n,) + geom.input_shape, "input batch")
+    if out is None:
+        out = torch.empty(packed_input3_shape(geom, n), dtype=torch.bfloat16, device=x.device)
+    elif tuple(out.shape) != packed_input3_shape(geom, n) or out.dtype != torch.bfloat16:
+        raise ShapeMismatchError("out must be bf16 " + str(packed_input3_shape(geom, n)))
+    g = _native.Geom.of(geom, n)
+    with torch.cuda.device(x.device):
+        _native.check(_native.lib().smmc_pack_input_bf16x3_nhwc(
+            ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()), ctypes.byref(g),
+            _stream_ptr(torch, x.device)), "smmc_pack_input_bf16x3_nhwc")
+    return out
+
+
+def pack_weights_bf16x3(weights_smm, geom):
+    """fp32 (c_i, k_w, k_h, c_o) -> bf16 (k_w*k_h, c_o, 3*c_i) [hi | hi | lo]."""
+    torch = _torch()
+    _check_tensor(weights_smm, geom.weights_smm_shape, "repacked weight tensor")
+    out = torch.empty((geom.k_w * geom.k_h, geom.out_channels, 3 * geom.in_channels),
+                      dtype=torch.bfloat16, device=weights_smm.device)
+    g = _native.Geom.of(geom, 1)
+    with torch.cuda.device(weights_smm.device):
+        _native.check(_native.lib().smmc_pack_weights_bf16x3(
+            ctypes.c_void_p(weights_smm.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+            ctypes.byref(g), _stream_ptr(torch, weights_smm.device)), "smmc_pack_weights_bf16x3")
+    return out
+
+
+def conv2d_bf16x3_tc(x3, w3, geom, out=None):
+    """tcgen05 split-bf16 conv of pack_input_bf16x3 / pack_weights_bf16x3
+    operands -> fp32 NCHW, on torch's current stream."""
+    torch = _torch()
+    if not isinstance(x3, torch.Tensor) or not x3.is_cuda or x3.dtype != torch.bfloat16 \
+            or x3.dim() != 4 or not x3.is_contiguous():
+        raise ShapeMismatchError("x3 must be a contiguous CUDA bf16 (N, hp, wp, 3*c_i) tensor")
+    n = x3.shape[0]
+    if tuple(x3.shape) != packed_input3_shape(geom, n):
+        raise ShapeMismatchError(f"x3 has shape {tuple(x3.shape)}, expected "
+                                 f"{packed_input3_shape(geom, n)}")
+    if tuple(w3.shape) != (geom.k_w * geom.k_h, geom.out_channels, 3 * geom.in_channels) \
+            or w3.dtype != torch.bfloat16 or not w3.is_cuda:
+        raise ShapeMismatchError("w3 must be bf16 (k_w*k_h, c_o, 3*c_i) on the device")
+    if out is None:
+        out = torch.empty((n,) + geom.output_shape, device=x3.device, dtype=torch.float32)
+    else:
+        _check_tensor(out, (n,) + geom.output_shape, "output tensor")
+    if n == 0:
+        return out
+    g = _native.Geom.of(geom, n)
+    with torch.cuda.device(x3.device):
+        _native.check(_native.lib().smmc_conv2d_fwd_bf16x3_tc(
+            ctypes.c_void_p(x3.data_ptr()), ctypes.c_void_p(w3.data_ptr()),
+            ctypes.c_void_p(out.data_ptr()), ctypes.byref(g), _stream_ptr(torch, x3.device)),
+            "smmc_conv2d_fwd_bf16x3_tc")
+    return out
+
+
+def tc3_plan_describe(geom, batch=1):
+    """Plan of the split-bf16 path (the bf16 plan over 3*c_i channels)."""
+    from .geometry import ConvGeometry
+    g3 = ConvGeometry(3 * geom.in_channels, geom.out_channels, geom.in_h, geom.in_w, geom.k_h,
+                      geom.k_w, geom.stride_h, geom.stride_w, geom.pad_h, geom.pad_w)
+    return _native.tc_plan_describe(g3, batch)
+
+
+class Tc3SmmConv2d:
+    """Fitted fp32-accurate tensor-core layer (fp32 NCHW in, fp32 NCHW out):
+    weights split and packed once (untimed, like the reference's repack); each
+    call splits/packs the input batch into a cached bf16 buffer and runs the
+    tcgen05 kernel (both inside a timed step)."""
+
+    def __init__(self, geom, weights, device="cuda"):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise DeviceError("Tc3SmmConv2d needs a CUDA device (no CPU fallback)")
+        if not tc_supported(geom):
+            from .errors import BackendUnsupportedError
+            raise BackendUnsupportedError(
+                "split-bf16 tensor-core path needs stride 1 and c_i % 8 == 0")
+        self.geom = geom
+        self.device = torch.device(device)
+        w = torch.as_tensor(weights, dtype=torch.float32)
+        if tuple(w.shape) == geom.weights_shape:
+            w = w.permute(1, 3, 2, 0)
+        w = w.contiguous().to(self.device)
+        self.w3 = pack_weights_bf16x3(w, geom)
+        self._x3 = None
+
+    def __call__(self, x, out=None):
+        n = x.shape[0]
+        if self._x3 is None or self._x3.shape[0] != n:
+            self._x3 = _torch().empty(packed_input3_shape(self.geom, n), dtype=_torch().bfloat16,
+                                      device=self.device)
+        pack_input_bf16x3(x, self.geom, out=self._x3)
+        return conv2d_bf16x3_tc(self._x3, self.w3, self.geom, out=out)
+
+
 def tc_plan_halo(geom):
     """True when the tensor-core variant uses the halo kernel for this geometry
     (one TMA box per 64-channel block shared by all taps)."""

@@ -277,7 +277,8 @@ def run_ours(args):
             L["w"] = [wd] + [wd.clone() for _ in range(R - 1)]
         shape = (L["n"],) + L["gl"].output_shape
         L["y"] = [torch.empty(shape, device=dev) for _ in range(R)]
-        need = 0 if (tc or tc3) else _native.workspace_bytes(L["gl"], L["n"], args.mode)
+        need = (device.tc_workspace_bytes(L["gl"], L["n"], split3=tc3) if (tc or tc3) and L["n"]
+                else 0 if (tc or tc3) else _native.workspace_bytes(L["gl"], L["n"], args.mode))
         L["ws"] = torch.empty(max(need, 16), dtype=torch.uint8, device=dev)
         if L["shard"] == "cout":
             L["full"] = torch.empty((L["n"],) + L["g"].output_shape, device=dev)
@@ -301,10 +302,10 @@ def run_ours(args):
         if L["n"] == 0:
             return
         if tc:
-            device.conv2d_bf16_tc(L["xb"][r], L["wt"][r], L["gl"], out=L["y"][r])
+            device.conv2d_bf16_tc(L["xb"][r], L["wt"][r], L["gl"], out=L["y"][r], workspace=L["ws"])
         elif tc3:
             device.pack_input_bf16x3(L["x"][r], L["gl"], out=L["x3"])
-            device.conv2d_bf16x3_tc(L["x3"], L["w3"][r], L["gl"], out=L["y"][r])
+            device.conv2d_bf16x3_tc(L["x3"], L["w3"][r], L["gl"], out=L["y"][r], workspace=L["ws"])
         else:
             device.conv2d(L["x"][r], L["w"][r], L["gl"], mode=args.mode, out=L["y"][r],
                           workspace=L["ws"])
@@ -432,7 +433,8 @@ def run_ours(args):
             "plan": ((_native.tc_plan_describe(gl, L["n"]) if tc else
                       "split-bf16 x3 over 3*c_i: " + device.tc3_plan_describe(gl, L["n"]) if tc3 else
                       _native.plan_describe(gl, L["n"], args.mode)) if L["n"] else ""),
-            "launches_per_call": 1 if tc else 2 if tc3 else
+            "launches_per_call": ((1 if tc else 2) + (1 if device.tc_workspace_bytes(
+                gl, L["n"], split3=tc3) else 0)) if (tc or tc3) and L["n"] else
             (_native.plan_launches(gl, L["n"], args.mode) if L["n"] else 0)})
     dom = max(details, key=lambda d: d["ms_avg"])
     traffic = None
@@ -634,10 +636,12 @@ def run_e2e_tc(args, layers, world, dev):
             xd.copy_(xh, non_blocking=True)
             if tc3:
                 x3 = device.pack_input_bf16x3(xd, L["gl"], out=L["x3"])
-                y = device.conv2d_bf16x3_tc(x3, L["w3"][0], L["gl"], out=L["y"][0])
+                y = device.conv2d_bf16x3_tc(x3, L["w3"][0], L["gl"], out=L["y"][0],
+                                            workspace=L["ws"])
             else:
                 xb = device.pack_input_bf16(xd, L["gl"], out=L["xb"][0])
-                y = device.conv2d_bf16_tc(xb, L["wt"][0], L["gl"], out=L["y"][0])
+                y = device.conv2d_bf16_tc(xb, L["wt"][0], L["gl"], out=L["y"][0],
+                                          workspace=L["ws"])
             yh.copy_(y, non_blocking=True)
         torch.cuda.synchronize()
 

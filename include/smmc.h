@@ -163,6 +163,18 @@ SMMC_API int smmc_pack_weights_bf16(const float* w_smm, uint16_t* w_tc, const sm
 SMMC_API int smmc_conv2d_fwd_bf16_tc(const uint16_t* x_nhwc, const uint16_t* w_tc, float* y,
                                      const smmc_geom* g, void* stream);
 
+/* Device scratch (bytes) of the tensor-core kernels' split-K (layers with
+ * fewer tiles than SMs split their channel blocks across CTAs and sum fp32
+ * partial planes in split order); 0 when the plan does not split.  split3 = 1
+ * for the bf16x3 path below (its 3*c_i channels). */
+SMMC_API size_t smmc_tc_workspace_bytes(const smmc_geom* g, int split3);
+
+/* smmc_conv2d_fwd_bf16_tc with a caller workspace (enables split-K; with
+ * ws = NULL or too small the kernel runs unsplit). */
+SMMC_API int smmc_conv2d_fwd_bf16_tc_ws(const uint16_t* x_nhwc, const uint16_t* w_tc, float* y,
+                                        const smmc_geom* g, void* ws, size_t ws_bytes,
+                                        void* stream);
+
 /* ---------------------------------------------------------------------------
  * fp32-accurate tensor-core path ("bf16x3", split bf16): x = x_hi + x_lo and
  * w = w_hi + w_lo with hi = bf16(v), lo = bf16(v - hi); y = x_hi*w_hi +
@@ -180,9 +192,11 @@ SMMC_API int smmc_pack_input_bf16x3_nhwc(const float* x, uint16_t* x3, const smm
 SMMC_API int smmc_pack_weights_bf16x3(const float* w_smm, uint16_t* w3, const smmc_geom* g,
                                       void* stream);
 
-/* y fp32 NCHW = conv(x, w) from the split operands above. */
+/* y fp32 NCHW = conv(x, w) from the split operands above; workspace as
+ * smmc_tc_workspace_bytes(g, 1) (NULL: unsplit). */
 SMMC_API int smmc_conv2d_fwd_bf16x3_tc(const uint16_t* x3, const uint16_t* w3, float* y,
-                                       const smmc_geom* g, void* stream);
+                                       const smmc_geom* g, void* ws, size_t ws_bytes,
+                                       void* stream);
 
 /* GPU im2col comparator (the paper's baseline): the explicit
  * lowered matrix of im2col_pack (im2col.py:22-71), per sample

@@ -40,7 +40,8 @@ EXPORTED_SYMBOLS = (
     "smmc_plan_launches", "smmc_plan_describe", "smmc_tc_plan_describe", "smmc_launch_count",
     "smmc_tc_supported", "smmc_pack_input_bf16_nhwc", "smmc_pack_weights_bf16",
     "smmc_conv2d_fwd_bf16_tc", "smmc_pack_input_bf16x3_nhwc", "smmc_pack_weights_bf16x3",
-    "smmc_conv2d_fwd_bf16x3_tc", "smmc_im2col_bytes", "smmc_im2col_pack_f32",
+    "smmc_conv2d_fwd_bf16x3_tc", "smmc_tc_workspace_bytes", "smmc_conv2d_fwd_bf16_tc_ws",
+    "smmc_im2col_bytes", "smmc_im2col_pack_f32",
     "smmc_conv2d_fwd_f32_gather", "smmc_gather_workspace_bytes", "smmc_ipc_handle",
     "smmc_ipc_open", "smmc_ipc_close", "smmc_host_alloc_pinned", "smmc_host_free_pinned",
     "smmc_layer_create", "smmc_layer_forward_host", "smmc_layer_destroy",
@@ -108,7 +109,9 @@ _SIGNATURES = {
     "smmc_conv2d_fwd_bf16_tc": (ctypes.c_int, [_P, _P, _P, _GP, _P]),
     "smmc_pack_input_bf16x3_nhwc": (ctypes.c_int, [_P, _P, _GP, _P]),
     "smmc_pack_weights_bf16x3": (ctypes.c_int, [_P, _P, _GP, _P]),
-    "smmc_conv2d_fwd_bf16x3_tc": (ctypes.c_int, [_P, _P, _P, _GP, _P]),
+    "smmc_conv2d_fwd_bf16x3_tc": (ctypes.c_int, [_P, _P, _P, _GP, _P, ctypes.c_size_t, _P]),
+    "smmc_tc_workspace_bytes": (ctypes.c_size_t, [_GP, ctypes.c_int]),
+    "smmc_conv2d_fwd_bf16_tc_ws": (ctypes.c_int, [_P, _P, _P, _GP, _P, ctypes.c_size_t, _P]),
     "smmc_im2col_bytes": (ctypes.c_size_t, [_GP]),
     "smmc_im2col_pack_f32": (ctypes.c_int, [_P, _P, _GP, _P]),
     "smmc_conv2d_fwd_f32_gather": (ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_void_p),

@@ -74,6 +74,13 @@ struct TcParams {
     int b_stages;                   // persistent kernel: B ring depth
     int tiles_m, tiles_n;           // persistent kernel: tile space (tile = m * tiles_n + n)
     uint32_t tx_a, tx_b;            // TMA bytes per A box / B box
+    // persistent kernel split-K over channel blocks (few-tile layers): work
+    // item t = tile * splits + s covers channel blocks [s*cb_per_split, ...)
+    // and writes fp32 partial planes ws[s] (n, co, oh, ow), summed in split
+    // order by tc_split_reduce_kernel
+    int splits, cb_per_split;
+    float* ws;
+    int64_t y_elems;
 };
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
@@ -250,7 +257,7 @@ conv_tc_halo_persistent_kernel(const __grid_constant__ CUtensorMap tm_a,
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int tiles = p.tiles_m * p.tiles_n;
+    const int items = p.tiles_m * p.tiles_n * p.splits;  // (tile, split) work items
 
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tm_a);
@@ -278,10 +285,13 @@ conv_tc_halo_persistent_kernel(const __grid_constant__ CUtensorMap tm_a,
     if (warp == 0) {
         if (lane == 0) {
             int ai = 0, bi = 0;
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            for (int it = blockIdx.x; it < items; it += gridDim.x) {
+                const int t = it / p.splits;
+                const int cb0 = (it - t * p.splits) * p.cb_per_split;
+                const int cb1 = min(p.cblocks, cb0 + p.cb_per_split);
                 const int q0 = (t / p.tiles_n) * (TC_BM * MT);
                 const int co0 = (t % p.tiles_n) * HBN;
-                for (int cb = 0; cb < p.cblocks; ++cb, ++ai) {
+                for (int cb = cb0; cb < cb1; ++cb, ++ai) {
                     const int sa = ai % HALO_A_STAGES;
                     if (ai >= HALO_A_STAGES)
                         ptx::mbar_wait(&a_empty[sa], ((ai / HALO_A_STAGES) - 1) & 1);
@@ -304,13 +314,16 @@ conv_tc_halo_persistent_kernel(const __grid_constant__ CUtensorMap tm_a,
         if (lane == 0) {
             constexpr uint32_t idesc = ptx::idesc_bf16(TC_BM, HBN);
             int ai = 0, bi = 0, local = 0;
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+            for (int it = blockIdx.x; it < items; it += gridDim.x, ++local) {
+                const int t = it / p.splits;
+                const int cb0 = (it - t * p.splits) * p.cb_per_split;
+                const int cb1 = min(p.cblocks, cb0 + p.cb_per_split);
                 const int acc = local % PH_ACC;
                 if (local >= PH_ACC) ptx::mbar_wait(&acc_empty[acc], ((local / PH_ACC) - 1) & 1);
                 ptx::tc_fence_after();
                 const uint32_t d = tmem + acc * MT * HBN;
                 bool first = true;
-                for (int cb = 0; cb < p.cblocks; ++cb, ++ai) {
+                for (int cb = cb0; cb < cb1; ++cb, ++ai) {
                     const int sa = ai % HALO_A_STAGES;
                     ptx::mbar_wait(&a_full[sa], (ai / HALO_A_STAGES) & 1);
                     for (int tap = 0; tap < p.taps; ++tap, ++bi) {
@@ -344,7 +357,9 @@ conv_tc_halo_persistent_kernel(const __grid_constant__ CUtensorMap tm_a,
         const int part = (warp - 2) >> 2;
         const int plane = p.hp * p.wp;
         int local = 0;
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+        for (int it = blockIdx.x; it < items; it += gridDim.x, ++local) {
+            const int t = it / p.splits;
+            float* const yo = p.splits > 1 ? p.ws + (int64_t)(it - t * p.splits) * p.y_elems : p.y;
             const int acc = local % PH_ACC;
             ptx::mbar_wait(&acc_full[acc], (local / PH_ACC) & 1);
             ptx::tc_fence_after();
@@ -367,7 +382,7 @@ conv_tc_halo_persistent_kernel(const __grid_constant__ CUtensorMap tm_a,
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
                         const int co = co0 + cc * 32 + i;
-                        if (co < p.co) p.y[ybase + (int64_t)co * p.ohw] = __uint_as_float(v[i]);
+                        if (co < p.co) yo[ybase + (int64_t)co * p.ohw] = __uint_as_float(v[i]);
                     }
                 }
             }
@@ -379,6 +394,34 @@ conv_tc_halo_persistent_kernel(const __grid_constant__ CUtensorMap tm_a,
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == 2) ptx::tmem_dealloc(tmem, PH_ACC * MT * HBN);
+}
+
+// y = ws[0] + ws[1] + ... in split order (deterministic)
+__global__ void __launch_bounds__(256) tc_split_reduce_kernel(const float* __restrict__ ws,
+                                                              float* __restrict__ y, int64_t total,
+                                                              int splits) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    if ((total & 3) == 0) {
+        const float4* w4 = reinterpret_cast<const float4*>(ws);
+        const int64_t t4 = total >> 2;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < t4; i += stride) {
+            float4 a = __ldcg(w4 + i);
+            for (int z = 1; z < splits; ++z) {
+                const float4 v = __ldcg(w4 + z * t4 + i);
+                a.x += v.x;
+                a.y += v.y;
+                a.z += v.z;
+                a.w += v.w;
+            }
+            reinterpret_cast<float4*>(y)[i] = a;
+        }
+        return;
+    }
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        float a = ws[i];
+        for (int z = 1; z < splits; ++z) a += ws[z * total + i];
+        y[i] = a;
+    }
 }
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -486,38 +529,49 @@ __device__ __forceinline__ void split_bf16(float v, __nv_bfloat16& hi, __nv_bflo
     lo = __float2bfloat16_rn(v - __bfloat162float(hi));
 }
 
-__global__ void pack_input_padded_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ out,
-                                         int c, int h, int w, int ph, int pw, int hp, int wp,
-                                         int split) {
-    __shared__ float tile[32][33];
-    const int t0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+__global__ void __launch_bounds__(256) pack_input_padded_kernel(
+    const float* __restrict__ x, __nv_bfloat16* __restrict__ out, int c, int h, int w, int ph, int pw,
+    int hp, int wp, int split) {
+    // tile: 32 channels x 64 padded columns of one padded row.  Loads are
+    // 256-byte rows of one channel; stores are 16-byte runs of 8 channels of
+    // one pixel (c % 8 == 0), i.e. whole 32-byte sectors per warp.
+    __shared__ float tile[32][65];
+    const int t0 = blockIdx.x * 64, c0 = blockIdx.y * 32;
     const int n = blockIdx.z / hp, r = blockIdx.z - n * hp;
     const int ih = r - ph;
     const bool row_in = (unsigned)ih < (unsigned)h;
-    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-        const int cc = c0 + i, iw = t0 + threadIdx.x - pw;
-        float v = 0.0f;
-        if (row_in && cc < c && (unsigned)iw < (unsigned)w)
-            v = x[(((int64_t)n * c + cc) * h + ih) * w + iw];
-        tile[i][threadIdx.x] = v;
+    const int tid = threadIdx.x;
+    {
+        const int px = tid & 63, cq = tid >> 6;  // 4 channel quarters of 8
+        const int iw = t0 + px - pw;
+        const bool col_in = row_in && (unsigned)iw < (unsigned)w;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int cc = c0 + cq * 8 + k;
+            float v = 0.0f;
+            if (col_in && cc < c) v = __ldg(x + (((int64_t)n * c + cc) * h + ih) * w + iw);
+            tile[cq * 8 + k][px] = v;
+        }
     }
     __syncthreads();
+    const int px = tid >> 2, grp = tid & 3;
+    const int t = t0 + px, cc = c0 + grp * 8;
+    if (t >= wp || cc >= c) return;
     const int cs = c * split;  // channels per padded pixel
-    __nv_bfloat16* orow = out + (((int64_t)n * hp + r) * wp) * cs;
-    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-        const int t = t0 + i, cc = c0 + threadIdx.x;
-        if (t < wp && cc < c) {
-            const float v = tile[threadIdx.x][i];
-            if (split == 1) {
-                orow[(int64_t)t * cs + cc] = __float2bfloat16_rn(v);
-            } else {
-                __nv_bfloat16 hi, lo;
-                split_bf16(v, hi, lo);
-                orow[(int64_t)t * cs + cc] = hi;
-                orow[(int64_t)t * cs + c + cc] = lo;
-                orow[(int64_t)t * cs + 2 * c + cc] = hi;
-            }
-        }
+    __nv_bfloat16* o = out + (((int64_t)n * hp + r) * wp + t) * cs + cc;
+    __align__(16) __nv_bfloat16 hi[8], lo[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const float v = tile[grp * 8 + k][px];
+        if (split == 1)
+            hi[k] = __float2bfloat16_rn(v);
+        else
+            split_bf16(v, hi[k], lo[k]);
+    }
+    *reinterpret_cast<uint4*>(o) = *reinterpret_cast<const uint4*>(hi);
+    if (split != 1) {  // [hi | lo | hi]
+        *reinterpret_cast<uint4*>(o + c) = *reinterpret_cast<const uint4*>(lo);
+        *reinterpret_cast<uint4*>(o + 2 * c) = *reinterpret_cast<const uint4*>(hi);
     }
 }
 
@@ -628,12 +682,55 @@ TcPlan plan_tc(const smmc_geom& g) {
         if (const char* f = getenv("SMMC_TC_MT")) pl.mt = atoi(f) == 2 ? 2 : 1;
     }
     pl.tiles_n = (g.c_o + pl.bn - 1) / pl.bn;
+    // few-tile layers (N = 1, 7x7 planes): split the channel blocks across
+    // CTAs of the persistent kernel so that ~148 work items run, partial
+    // planes summed in split order by a second kernel (needs the workspace
+    // of smmc_tc_workspace_bytes)
+    const int cblocks = (g.c_i + TC_BK - 1) / TC_BK;
+    pl.splits = 1;
+    pl.cb_per_split = cblocks;
+    const int64_t tiles = pl.tiles_m * pl.tiles_n;
+    int want = (pl.halo && pl.mt == 1 && tiles < 148) ? (int)std::min<int64_t>(cblocks, 148 / tiles) : 1;
+    if (want == 1 && pl.halo && pl.mt == 1 && tiles < 148) {
+        // 75-147 tiles: pick S so that tiles*S fills whole waves of 148
+        // (wave count per unit of K, plus a per-split cost); measured on
+        // 512@7 N=32, 84 tiles: S=5 66 us vs 85 unsplit (bf16x3)
+        double best = 1.0;
+        for (int sp = 2; sp <= cblocks; ++sp) {
+            const double cost = (double)((tiles * sp + 147) / 148) / sp + 0.02 * sp;
+            if (cost < best - 1e-9) {
+                best = cost;
+                want = sp;
+            }
+        }
+    }
+    if (const char* f = getenv("SMMC_TC_SPLIT")) want = pl.halo ? std::max(1, std::min(atoi(f), cblocks)) : 1;
+    if (want > 1) {
+        pl.cb_per_split = (cblocks + want - 1) / want;
+        pl.splits = (cblocks + pl.cb_per_split - 1) / pl.cb_per_split;
+        if (pl.splits > 1) {
+            pl.persistent = 1;
+            pl.mt = 1;
+        }
+    }
     return pl;
 }
 
-cudaError_t launch_tc_bf16(const uint16_t* x_pad, const uint16_t* w_tc, float* y, const smmc_geom& g,
-                           cudaStream_t s, const char** why) {
+size_t tc_workspace_bytes(const smmc_geom& g) {
     const TcPlan pl = plan_tc(g);
+    if (!pl.supported || pl.splits <= 1) return 0;
+    const int oh = (g.h + 2 * g.p_h - g.k_h) / g.s_h + 1;
+    const int ow = (g.w + 2 * g.p_w - g.k_w) / g.s_w + 1;
+    return (size_t)pl.splits * g.n * g.c_o * oh * ow * sizeof(float);
+}
+
+cudaError_t launch_tc_bf16(const uint16_t* x_pad, const uint16_t* w_tc, float* y, const smmc_geom& g,
+                           cudaStream_t s, const char** why, float* ws, size_t ws_bytes) {
+    TcPlan pl = plan_tc(g);
+    if (pl.splits > 1 && (!ws || ws_bytes < tc_workspace_bytes(g))) {
+        pl.splits = 1;  // no workspace: whole K per tile
+        pl.cb_per_split = (g.c_i + TC_BK - 1) / TC_BK;
+    }
     if (!pl.supported) {
         *why = "bf16 tensor-core variant needs stride 1 and c_i % 8 == 0";
         return cudaErrorNotSupported;
@@ -660,6 +757,10 @@ cudaError_t launch_tc_bf16(const uint16_t* x_pad, const uint16_t* w_tc, float* y
     p.taps = taps;
     p.cblocks = (g.c_i + TC_BK - 1) / TC_BK;
     p.tx_b = TC_B_BYTES;
+    p.splits = pl.splits;
+    p.cb_per_split = pl.cb_per_split;
+    p.ws = ws;
+    p.y_elems = (int64_t)g.n * g.c_o * oh * ow;
 
     CUtensorMap tm_a, tm_b;
     {
@@ -722,13 +823,19 @@ cudaError_t launch_tc_bf16(const uint16_t* x_pad, const uint16_t* w_tc, float* y
             int sms = 148, dev = 0;
             if (cudaGetDevice(&dev) == cudaSuccess)
                 cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            const int pgrid = (int)std::min<int64_t>((int64_t)p.tiles_m * p.tiles_n, sms);
+            const int pgrid = (int)std::min<int64_t>((int64_t)p.tiles_m * p.tiles_n * p.splits, sms);
             if (hbn == 256)
                 conv_tc_halo_persistent_kernel<256, 1><<<pgrid, PH_THREADS, psmem, s>>>(tm_a, tm_b, p);
             else if (mt == 2)
                 conv_tc_halo_persistent_kernel<128, 2><<<pgrid, PH_THREADS, psmem, s>>>(tm_a, tm_b, p);
             else
                 conv_tc_halo_persistent_kernel<128, 1><<<pgrid, PH_THREADS, psmem, s>>>(tm_a, tm_b, p);
+            if (p.splits > 1) {
+                count_launches(1);
+                const int64_t t4 = (p.y_elems + 3) / 4;
+                const int rblocks = (int)std::min<int64_t>((t4 + 255) / 256, 148 * 8);
+                tc_split_reduce_kernel<<<rblocks, 256, 0, s>>>(ws, y, p.y_elems, p.splits);
+            }
         } else {
             const int smem = HALO_A_STAGES * p.halo_stage_bytes + HALO_B_STAGES * (int)p.tx_b + 1024;
             static std::once_flag once;
@@ -774,8 +881,8 @@ cudaError_t launch_tc_bf16(const uint16_t* x_pad, const uint16_t* w_tc, float* y
 cudaError_t launch_pack_input_nhwc(const float* x, uint16_t* out, const smmc_geom& g,
                                    cudaStream_t s, int split) {
     const int hp = g.h + 2 * g.p_h, wp = g.w + 2 * g.p_w;
-    dim3 grid((wp + 31) / 32, (g.c_i + 31) / 32, g.n * hp);
-    pack_input_padded_kernel<<<grid, dim3(32, 8), 0, s>>>(x, reinterpret_cast<__nv_bfloat16*>(out),
+    dim3 grid((wp + 63) / 64, (g.c_i + 31) / 32, g.n * hp);
+    pack_input_padded_kernel<<<grid, 256, 0, s>>>(x, reinterpret_cast<__nv_bfloat16*>(out),
                                                           g.c_i, g.h, g.w, g.p_h, g.p_w, hp, wp,
                                                           split);
     count_launches(1);

@@ -363,7 +363,12 @@ int smmc_tc_plan_describe(const smmc_geom* g, char* buf, size_t len) {
                                : "one tile per CTA, 2 CTAs/SM",
                  (long long)((pl.tiles_m + (pl.persistent ? pl.mt : 1) - 1) / (pl.persistent ? pl.mt : 1)),
                  pl.tiles_n);
-    else
+    if (pl.halo && pl.splits > 1) {
+        const size_t used = strlen(buf);
+        snprintf(buf + used, len - used, ", split-K %d x %d channel blocks (with workspace)",
+                 pl.splits, pl.cb_per_split);
+    }
+    if (!pl.halo)
         snprintf(buf, len, "tc: tcgen05 bf16 M=128 x N=%d x K=64, TMA SW128 4-D box per tap (%dx%dx%d px), "
                  "%lld x %d tiles", pl.bn, pl.tw, pl.th, pl.nb, (long long)pl.tiles_m, pl.tiles_n);
     return SMMC_OK;
@@ -741,6 +746,10 @@ int smmc_pack_input_bf16_nhwc(const float* x, uint16_t* x_nhwc, const smmc_geom*
         set_error("x and x_nhwc must be non-NULL device pointers");
         return SMMC_ESHAPE;
     }
+    if ((g->c_i & 7) || ((uintptr_t)x_nhwc & 15)) {
+        set_error("bf16 pack needs c_i %% 8 == 0 and a 16-byte aligned x_nhwc");
+        return SMMC_EUNSUPPORTED;
+    }
     return cuda_status(launch_pack_input_nhwc(x, x_nhwc, *g, static_cast<cudaStream_t>(stream)),
                        "pack_input_nhwc launch");
 }
@@ -766,6 +775,10 @@ int smmc_pack_input_bf16x3_nhwc(const float* x, uint16_t* x3, const smmc_geom* g
         set_error("x and x3 must be non-NULL device pointers");
         return SMMC_ESHAPE;
     }
+    if ((g->c_i & 7) || ((uintptr_t)x3 & 15)) {
+        set_error("bf16x3 pack needs c_i %% 8 == 0 and a 16-byte aligned x3");
+        return SMMC_EUNSUPPORTED;
+    }
     return cuda_status(launch_pack_input_nhwc(x, x3, *g, static_cast<cudaStream_t>(stream), 3),
                        "pack_input_bf16x3 launch");
 }
@@ -783,7 +796,7 @@ int smmc_pack_weights_bf16x3(const float* w_smm, uint16_t* w3, const smmc_geom* 
 }
 
 int smmc_conv2d_fwd_bf16x3_tc(const uint16_t* x3, const uint16_t* w3, float* y, const smmc_geom* g,
-                              void* stream) {
+                              void* ws, size_t ws_bytes, void* stream) {
     int oh = 0, ow = 0;
     int st = check_geom(g, &oh, &ow);
     if (st) return st;
@@ -793,11 +806,27 @@ int smmc_conv2d_fwd_bf16x3_tc(const uint16_t* x3, const uint16_t* w3, float* y, 
     }
     smmc_geom g3 = *g;  // the bf16 conv over the 3*c_i split channels
     g3.c_i *= 3;
-    return smmc_conv2d_fwd_bf16_tc(x3, w3, y, &g3, stream);
+    return smmc_conv2d_fwd_bf16_tc_ws(x3, w3, y, &g3, ws, ws_bytes, stream);
+}
+
+size_t smmc_tc_workspace_bytes(const smmc_geom* g, int split3) {
+    int oh = 0, ow = 0;
+    if (!g || check_geom(g, &oh, &ow) || g->n == 0) return 0;
+    smmc_geom gg = *g;
+    if (split3) {
+        if (gg.c_i > INT32_MAX / 3) return 0;
+        gg.c_i *= 3;
+    }
+    return tc_workspace_bytes(gg);
 }
 
 int smmc_conv2d_fwd_bf16_tc(const uint16_t* x_nhwc, const uint16_t* w_tc, float* y,
                             const smmc_geom* g, void* stream) {
+    return smmc_conv2d_fwd_bf16_tc_ws(x_nhwc, w_tc, y, g, nullptr, 0, stream);
+}
+
+int smmc_conv2d_fwd_bf16_tc_ws(const uint16_t* x_nhwc, const uint16_t* w_tc, float* y,
+                               const smmc_geom* g, void* ws, size_t ws_bytes, void* stream) {
     int oh = 0, ow = 0;
     int st = check_geom(g, &oh, &ow);
     if (st) return st;
@@ -811,7 +840,12 @@ int smmc_conv2d_fwd_bf16_tc(const uint16_t* x_nhwc, const uint16_t* w_tc, float*
         return SMMC_ESHAPE;
     }
     const char* why = "";
-    cudaError_t e = launch_tc_bf16(x_nhwc, w_tc, y, *g, static_cast<cudaStream_t>(stream), &why);
+    if (ws && ((uintptr_t)ws & 15)) {
+        set_error("workspace must be 16-byte aligned");
+        return SMMC_ESHAPE;
+    }
+    cudaError_t e = launch_tc_bf16(x_nhwc, w_tc, y, *g, static_cast<cudaStream_t>(stream), &why,
+                                   static_cast<float*>(ws), ws_bytes);
     if (e == cudaErrorNotSupported) {
         set_error("%s", why);
         return SMMC_EUNSUPPORTED;

@@ -88,10 +88,14 @@ struct TcPlan {
     int mt;            // persistent: 128-pixel M sub-tiles per tile sharing one B stage
     int64_t tiles_m;
     int tiles_n;
+    int splits;        // persistent kernel split-K over channel blocks (few-tile layers)
+    int cb_per_split;
 };
 TcPlan plan_tc(const smmc_geom& g);
+size_t tc_workspace_bytes(const smmc_geom& g);
 cudaError_t launch_tc_bf16(const uint16_t* x_nhwc, const uint16_t* w_tc, float* y, const smmc_geom& g,
-                           cudaStream_t s, const char** why);
+                           cudaStream_t s, const char** why, float* ws = nullptr,
+                           size_t ws_bytes = 0);
 // split = 1: plain bf16; split = 3: [hi | lo | hi] input / [hi | hi | lo]
 // weight channels of the fp32-accurate bf16x3 path (run as a 3*c_i bf16 conv)
 cudaError_t launch_pack_input_nhwc(const float* x, uint16_t* out, const smmc_geom& g, cudaStream_t s,

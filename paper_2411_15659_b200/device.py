@@ -218,10 +218,26 @@ def pack_weights_bf16(weights_smm, geom):
     return out
 
 
-def conv2d_bf16_tc(x_nhwc, w_tc, geom, out=None):
+def tc_workspace_bytes(geom, batch, split3=False):
+    """Scratch of the tensor-core split-K (few-tile layers), else 0."""
+    g = _native.Geom.of(geom, batch)
+    return int(_native.lib().smmc_tc_workspace_bytes(ctypes.byref(g), 1 if split3 else 0))
+
+
+def _tc_workspace(torch, geom, n, dev, split3, workspace):
+    need = tc_workspace_bytes(geom, n, split3) if n else 0
+    if not need:
+        return None, 0
+    if workspace is None or workspace.numel() * workspace.element_size() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=dev)
+    return ctypes.c_void_p(workspace.data_ptr()), workspace.numel() * workspace.element_size()
+
+
+def conv2d_bf16_tc(x_nhwc, w_tc, geom, out=None, workspace=None):
     """tcgen05 bf16 conv: x_nhwc zero-padded bf16 (N, h+2p_h, w+2p_w, c_i) from
     pack_input_bf16, w_tc bf16 (taps, c_o, c_i) -> fp32 NCHW (N, c_o, h', w'),
-    on torch's current stream."""
+    on torch's current stream.  Few-tile layers split K across CTAs into a
+    workspace (passed, or taken from torch's caching allocator)."""
     torch = _torch()
     if not isinstance(x_nhwc, torch.Tensor) or x_nhwc.dim() != 4 or not x_nhwc.is_cuda \
             or x_nhwc.dtype != torch.bfloat16 or not x_nhwc.is_contiguous():
@@ -241,10 +257,11 @@ def conv2d_bf16_tc(x_nhwc, w_tc, geom, out=None):
         return out
     g = _native.Geom.of(geom, n)
     with torch.cuda.device(x_nhwc.device):
-        _native.check(_native.lib().smmc_conv2d_fwd_bf16_tc(
+        ws, ws_len = _tc_workspace(torch, geom, n, x_nhwc.device, False, workspace)
+        _native.check(_native.lib().smmc_conv2d_fwd_bf16_tc_ws(
             ctypes.c_void_p(x_nhwc.data_ptr()), ctypes.c_void_p(w_tc.data_ptr()),
-            ctypes.c_void_p(out.data_ptr()), ctypes.byref(g), _stream_ptr(torch, x_nhwc.device)),
-            "smmc_conv2d_fwd_bf16_tc")
+            ctypes.c_void_p(out.data_ptr()), ctypes.byref(g), ws, ws_len,
+            _stream_ptr(torch, x_nhwc.device)), "smmc_conv2d_fwd_bf16_tc_ws")
     return out
 
 
@@ -268,12 +285,18 @@ class TcSmmConv2d:
             w = w.permute(1, 3, 2, 0)
         w = w.contiguous().to(self.device)
         self.w_tc = pack_weights_bf16(w, geom)
+        self._ws = {}
 
     def pack_input(self, x, out=None):
         return pack_input_bf16(x, self.geom, out=out)
 
     def __call__(self, x_nhwc, out=None):
-        return conv2d_bf16_tc(x_nhwc, self.w_tc, self.geom, out=out)
+        n = x_nhwc.shape[0]
+        if n not in self._ws:
+            need = tc_workspace_bytes(self.geom, n) if n else 0
+            self._ws[n] = (_torch().empty(need, dtype=_torch().uint8, device=self.device)
+                           if need else None)
+        return conv2d_bf16_tc(x_nhwc, self.w_tc, self.geom, out=out, workspace=self._ws[n])
 
 
 # --------------------------------------------------------------------------
@@ -318,7 +341,7 @@ def pack_weights_bf16x3(weights_smm, geom):
     return out
 
 
-def conv2d_bf16x3_tc(x3, w3, geom, out=None):
+def conv2d_bf16x3_tc(x3, w3, geom, out=None, workspace=None):
     """tcgen05 split-bf16 conv of pack_input_bf16x3 / pack_weights_bf16x3
     operands -> fp32 NCHW, on torch's current stream."""
     torch = _torch()
@@ -340,10 +363,11 @@ def conv2d_bf16x3_tc(x3, w3, geom, out=None):
         return out
     g = _native.Geom.of(geom, n)
     with torch.cuda.device(x3.device):
+        ws, ws_len = _tc_workspace(torch, geom, n, x3.device, True, workspace)
         _native.check(_native.lib().smmc_conv2d_fwd_bf16x3_tc(
             ctypes.c_void_p(x3.data_ptr()), ctypes.c_void_p(w3.data_ptr()),
-            ctypes.c_void_p(out.data_ptr()), ctypes.byref(g), _stream_ptr(torch, x3.device)),
-            "smmc_conv2d_fwd_bf16x3_tc")
+            ctypes.c_void_p(out.data_ptr()), ctypes.byref(g), ws, ws_len,
+            _stream_ptr(torch, x3.device)), "smmc_conv2d_fwd_bf16x3_tc")
     return out
 
 
@@ -377,14 +401,18 @@ class Tc3SmmConv2d:
         w = w.contiguous().to(self.device)
         self.w3 = pack_weights_bf16x3(w, geom)
         self._x3 = None
+        self._ws = None
 
     def __call__(self, x, out=None):
+        torch = _torch()
         n = x.shape[0]
         if self._x3 is None or self._x3.shape[0] != n:
-            self._x3 = _torch().empty(packed_input3_shape(self.geom, n), dtype=_torch().bfloat16,
-                                      device=self.device)
+            self._x3 = torch.empty(packed_input3_shape(self.geom, n), dtype=torch.bfloat16,
+                                   device=self.device)
+            need = tc_workspace_bytes(self.geom, n, split3=True) if n else 0
+            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device) if need else None
         pack_input_bf16x3(x, self.geom, out=self._x3)
-        return conv2d_bf16x3_tc(self._x3, self.w3, self.geom, out=out)
+        return conv2d_bf16x3_tc(self._x3, self.w3, self.geom, out=out, workspace=self._ws)
 
 
 def tc_plan_halo(geom):

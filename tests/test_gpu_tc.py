@@ -94,3 +94,35 @@ def test_tc_both_tile_widths(monkeypatch, case, bn):
                          threads=orc.host_threads())
     err = orc.max_abs_ratio(y[samples], ref)
     assert 1e-5 <= err <= TOL_BF16, err
+
+
+@pytest.mark.parametrize("split", ["2", "3", "8"])
+@pytest.mark.parametrize("case", [(128, 64, 7, 7, 3, 3, 1, 1, 1, 1, 3),
+                                  (256, 96, 14, 14, 3, 3, 1, 1, 1, 1, 1),
+                                  (64, 40, 9, 11, 1, 1, 1, 1, 0, 0, 2)],
+                         ids=lambda c: "x".join(map(str, c)))
+def test_tc_split_k(monkeypatch, case, split):
+    """Few-tile layers split their channel blocks across CTAs of the
+    persistent kernel (fp32 partial planes summed in split order): same
+    tolerance, deterministic, and the workspace-less entry runs unsplit."""
+    import torch
+    from paper_2411_15659_b200 import _native, device
+    monkeypatch.setenv("SMMC_TC_SPLIT", split)
+    *gt, n = case
+    g = ConvGeometry(*gt)
+    desc = _native.tc_plan_describe(g, n)
+    cblocks = (g.in_channels + 63) // 64
+    if cblocks > 1:
+        assert "split-K" in desc and device.tc_workspace_bytes(g, n) > 0, desc
+    x, w = synthetic_layer(g, n, 17)
+    layer = device.TcSmmConv2d(g, w)
+    xb = layer.pack_input(torch.from_numpy(x).cuda())
+    y1 = layer(xb)
+    y2 = layer(xb)
+    y0 = device.conv2d_bf16_tc(xb, layer.w_tc, g, workspace=torch.empty(0, dtype=torch.uint8,
+                                                                          device="cuda"))
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+    ref = orc.smm_conv_c(x, orc.repack(w), g, threads=orc.host_threads())
+    for y in (y1, y0):
+        assert orc.max_abs_ratio(y.cpu().numpy(), ref) <= TOL_BF16

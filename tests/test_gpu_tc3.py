@@ -82,3 +82,12 @@ def test_tc3_rejects_strided():
     g = ConvGeometry(16, 16, 16, 16, 3, 3, stride_h=2, stride_w=2, pad_h=1, pad_w=1)
     with pytest.raises(BackendUnsupportedError):
         device.Tc3SmmConv2d(g, np.zeros(g.weights_shape, np.float32))
+
+
+@pytest.mark.parametrize("split", ["1", "4", "12"])
+def test_tc3_split_k_meets_the_fp32_bar(monkeypatch, split):
+    monkeypatch.setenv("SMMC_TC_SPLIT", split)
+    g = ConvGeometry(256, 128, 7, 7, 3, 3, pad_h=1, pad_w=1)
+    x, w, y = _run(g, 2, 23)
+    ref = orc.smm_conv_c(x, orc.repack(w), g, threads=orc.host_threads())
+    assert orc.max_abs_ratio(y, ref) <= TOL_FP32

@@ -1,6 +1,6 @@
 """Run one BASELINE layer a few times (for ncu / quick timing).
 
-    python tools/prof_layer.py --config 2 --layer conv128@28_n32 [--iters 5] [--mode ffma|exact|bf16_tc]
+    python tools/prof_layer.py --config 2 --layer conv128@28_n32 [--iters 5] [--mode ffma|exact|bf16_tc|bf16x3_tc]
 """
 import argparse
 import sys
@@ -28,7 +28,9 @@ def main():
             continue
         x, w = synthetic_layer(g, n, layer_seed(a.config, li))
         xd = torch.from_numpy(x).cuda()
-        if a.mode == "bf16_tc":  # tcgen05 variant: input packed to bf16 NHWC once
+        if a.mode == "bf16x3_tc":  # fp32-accurate split-bf16: pack + conv every call
+            mod = device.Tc3SmmConv2d(g, w)
+        elif a.mode == "bf16_tc":  # tcgen05 variant: input packed to bf16 NHWC once
             mod = device.TcSmmConv2d(g, w)
             xd = mod.pack_input(xd)
         else:

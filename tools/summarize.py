@@ -3,7 +3,8 @@ import glob
 import json
 import sys
 
-for f in sorted(glob.glob(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/bench_cfg*.json")):
+pats = sys.argv[1:] or ["gpurun_out/bench_cfg*.json"]
+for f in [f for p in pats for f in sorted(glob.glob(p))]:
     j = json.load(open(f))
     cpu = j.get("cpu_baseline") or {}
     print(f"{f}: value={j['value']} GFLOP/s ms/step={j['ms_per_step']} e2e={j['e2e']['value'] if j.get('e2e') else None} "

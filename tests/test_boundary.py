@@ -76,6 +76,24 @@ def test_plans_and_workspace_without_gpu():
     assert _native.plan_launches(g, 0) == 0
 
 
+def test_tensor_core_plans_and_workspace_without_gpu():
+    """The tensor-core split-K planner (host only): few-tile layers split
+    their channel blocks and need a workspace, many-tile layers do not; the
+    bf16x3 geometry plans over 3*c_i channels."""
+    from paper_2411_15659_b200 import device
+    small = ConvGeometry(512, 512, 7, 7, 3, 3, pad_h=1, pad_w=1)
+    big = ConvGeometry(128, 128, 28, 28, 3, 3, pad_h=1, pad_w=1)
+    assert device.tc_workspace_bytes(small, 1) > 0
+    assert "split-K" in _native.tc_plan_describe(small, 1)
+    assert device.tc_workspace_bytes(small, 1, split3=True) > 0
+    assert "split-K" in device.tc3_plan_describe(small, 1)
+    assert device.tc_workspace_bytes(big, 256) == 0
+    assert device.tc_workspace_bytes(small, 0) == 0
+    strided = ConvGeometry(16, 16, 16, 16, 3, 3, stride_h=2, stride_w=2, pad_h=1, pad_w=1)
+    assert device.tc_workspace_bytes(strided, 4) == 0
+    assert not device.tc_supported(strided)
+
+
 def test_status_mapping():
     for st, exc in [(_native.SMMC_ESHAPE, smm.ShapeMismatchError),
                     (_native.SMMC_EUNSUPPORTED, smm.BackendUnsupportedError),

@@ -91,3 +91,32 @@ def test_tc3_split_k_meets_the_fp32_bar(monkeypatch, split):
     x, w, y = _run(g, 2, 23)
     ref = orc.smm_conv_c(x, orc.repack(w), g, threads=orc.host_threads())
     assert orc.max_abs_ratio(y, ref) <= TOL_FP32
+
+
+def test_tc3_entry_point_errors():
+    """Contract errors before any compute: misaligned workspace, packed
+    shapes, c_i % 8 != 0 at the pack entry."""
+    import ctypes
+
+    import torch
+    from paper_2411_15659_b200 import ShapeMismatchError, _native, device
+    g = ConvGeometry(128, 64, 7, 7, 3, 3, pad_h=1, pad_w=1)
+    x, w = synthetic_layer(g, 2, 3)
+    layer = device.Tc3SmmConv2d(g, w)
+    x3 = device.pack_input_bf16x3(torch.from_numpy(x).cuda(), g)
+    need = device.tc_workspace_bytes(g, 2, split3=True)
+    assert need > 0
+    buf = torch.empty(need + 16, dtype=torch.uint8, device="cuda")
+    y = torch.empty((2,) + g.output_shape, device="cuda")
+    gg = _native.Geom.of(g, 2)
+    st = _native.lib().smmc_conv2d_fwd_bf16x3_tc(
+        ctypes.c_void_p(x3.data_ptr()), ctypes.c_void_p(layer.w3.data_ptr()),
+        ctypes.c_void_p(y.data_ptr()), ctypes.byref(gg), ctypes.c_void_p(buf.data_ptr() + 4),
+        need, None)
+    assert st == _native.SMMC_ESHAPE
+    with pytest.raises(ShapeMismatchError):
+        device.conv2d_bf16x3_tc(x3[:1].contiguous(), layer.w3, g, out=y)
+    g5 = ConvGeometry(12, 8, 6, 6, 3, 3, pad_h=1, pad_w=1)
+    xs = torch.zeros((1,) + g5.input_shape, device="cuda")
+    with pytest.raises(BackendUnsupportedError):
+        device.pack_input_bf16x3(xs, g5)

@@ -1,0 +1,226 @@
+// conv_1x1.cu — persistent FFMA kernel for 1x1 stride-1 layers (short K).
+//
+// With k_h = k_w = 1 the SMM update (c, 0, 0) is one scalar weight per
+// output channel times the input plane of channel c (smm.py:84-114 with a
+// single tap): Y[n, m, p] = sum_c W_smm[c, 0, 0, m] * X[n, c, p].  K = c_i
+// is short (64-256: 4-16 blocks of 16), so in the tiled kernel every CTA
+// spends as long in its prologue (first loads) and epilogue (tile stores) as
+// in its K loop (timeline probe: 3.6 + 2.9 us around an 8.2 us loop on the
+// ResNet-50 1x1 64->256 layer; with 4 CTAs per SM the other CTAs mostly
+// cover that: measured 643 -> 637 us there, 27.8 -> 26.5 us on the config-3
+// 1x1 256->64 layer).  Here a persistent CTA walks its tiles as ONE
+// continuous stream of 16-deep blocks through a 4-stage cp.async ring: the
+// loads of tile t+1's first blocks are in flight while tile t's last blocks
+// compute and its outputs are stored.
+//
+// Same 8x8 FFMA2 thread tile and the same summation order as conv_ffma's
+// tap-major path (channel blocks in order, k steps in order), so results are
+// bitwise identical to it.  Input quads of 4 consecutive pixels of one
+// channel are 16-byte cp.async copies (h*w % 4 == 0): a quarter of the
+// tiled kernel's 4-byte gathers.
+#include <algorithm>
+#include <cstdlib>
+#include <mutex>
+
+#include "smmc_internal.cuh"
+
+namespace smmc {
+namespace {
+
+constexpr int kBK = 16;
+constexpr int kRing = 4;
+
+template <int BM, int BN, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) conv1x1_persistent_kernel(const Problem p) {
+    constexpr int TM = 8;
+    constexpr int TPX = BM / TM, TCO = BN / 8;
+    static_assert(TPX * TCO == THREADS && TCO % 8 == 0 && TPX % 4 == 0, "thread tile");
+    constexpr int WCO = TCO / 8;
+    constexpr int A_CHUNKS = kBK * BM / 4;   // 16-byte chunks per A stage
+    constexpr int B_CHUNKS = kBK * BN / 4;
+    static_assert(A_CHUNKS % THREADS == 0 && B_CHUNKS % THREADS == 0, "loader split");
+    constexpr int A_PER = A_CHUNKS / THREADS, B_PER = B_CHUNKS / THREADS;
+
+    extern __shared__ __align__(16) float smem[];
+    float* As = smem;                          // [kRing][kBK][BM]
+    float* Bs = smem + kRing * kBK * BM;       // [kRing][kBK][BN]
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int cg = (warp % WCO) * 8 + (lane & 7);
+    const int pg = (warp / WCO) * 4 + (lane >> 3);
+    const int KT = p.c / kBK;
+    const int64_t tiles = p.tiles;
+    // this CTA's tiles: blockIdx.x, +gridDim.x, ...; global block q of the
+    // stream = local tile index * KT + channel block
+    const int my_tiles = tiles > blockIdx.x ? (int)((tiles - 1 - blockIdx.x) / gridDim.x) + 1 : 0;
+    const int nq = my_tiles * KT;
+
+    // loader state (incremental: block kb of local tile lt), per-tile
+    // source pointers of this thread's A chunks and B chunks
+    int ld_kb = 0, ld_lt = 0, ld_slot = 0;
+    const float* a_src[A_PER];
+    bool a_ok[A_PER];
+    const float* b_src[B_PER];
+    int b_bytes[B_PER];
+    auto tile_setup = [&](int lt) {
+        const int64_t tile = blockIdx.x + (int64_t)lt * gridDim.x;
+        const int tm = (int)(tile / p.tiles_n);
+        const int m0 = tm * BM;
+        const int n0 = (int)(tile - (int64_t)tm * p.tiles_n) * BN;
+#pragma unroll
+        for (int i = 0; i < A_PER; ++i) {
+            const int ch = tid + i * THREADS;        // chunk: row r, pixel quad
+            const int r = ch / (BM / 4);
+            const int pm = m0 + (ch - r * (BM / 4)) * 4;
+            a_ok[i] = pm < p.m;
+            const int n = a_ok[i] ? pm / p.ohw : 0;
+            const int px = a_ok[i] ? pm - n * p.ohw : 0;
+            a_src[i] = p.x + ((int64_t)n * p.c + r) * p.ohw + px;
+        }
+#pragma unroll
+        for (int i = 0; i < B_PER; ++i) {
+            const int ch = tid + i * THREADS;
+            const int r = ch / (BN / 4);
+            const int co = n0 + (ch - r * (BN / 4)) * 4;
+            b_bytes[i] = min(max(p.co - co, 0), 4) * 4;
+            b_src[i] = p.w + (int64_t)r * p.co + co;
+        }
+    };
+    auto load_next = [&]() {
+        if (ld_kb == 0) tile_setup(ld_lt);
+        const uint32_t adst = smem_u32(As + ld_slot * kBK * BM);
+        const int64_t aoff = (int64_t)ld_kb * kBK * p.ohw;
+#pragma unroll
+        for (int i = 0; i < A_PER; ++i) {
+            const int ch = tid + i * THREADS;
+            const int r = ch / (BM / 4);
+            const int pq = (ch - r * (BM / 4)) * 4;
+            cp_async16_zfill(adst + (r * BM + pq) * 4, a_ok[i] ? a_src[i] + aoff : p.x, a_ok[i] ? 16 : 0);
+        }
+        const uint32_t bdst = smem_u32(Bs + ld_slot * kBK * BN);
+        const int64_t boff = (int64_t)ld_kb * kBK * p.co;
+#pragma unroll
+        for (int i = 0; i < B_PER; ++i) {
+            const int ch = tid + i * THREADS;
+            const int r = ch / (BN / 4);
+            const int cq = (ch - r * (BN / 4)) * 4;
+            cp_async16_zfill(bdst + (r * BN + cq) * 4, b_bytes[i] ? b_src[i] + boff : p.w, b_bytes[i]);
+        }
+        if (++ld_kb == KT) {
+            ld_kb = 0;
+            ++ld_lt;
+        }
+        ld_slot = ld_slot == kRing - 1 ? 0 : ld_slot + 1;
+    };
+
+#pragma unroll
+    for (int s = 0; s < kRing - 1; ++s) {
+        if (s < nq) load_next();
+        cp_async_commit();
+    }
+
+    uint64_t acc2[TM][4];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc2[i][j] = 0ull;
+
+    const float* a_rd = As + pg * 4;
+    const float* b_rd = Bs + cg * 4;
+    int slot = 0, kb = 0, lt = 0;
+    for (int q = 0; q < nq; ++q) {
+        cp_async_wait<kRing - 2>();
+        __syncthreads();
+        if (q + kRing - 1 < nq) load_next();
+        cp_async_commit();
+        const float* ap = a_rd + slot * (kBK * BM);
+        const float* bp = b_rd + slot * (kBK * BN);
+#pragma unroll
+        for (int kk = 0; kk < kBK; ++kk) {
+            float a[TM];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const float4 v = *reinterpret_cast<const float4*>(ap + kk * BM + h * (BM / 2));
+                a[4 * h + 0] = v.x;
+                a[4 * h + 1] = v.y;
+                a[4 * h + 2] = v.z;
+                a[4 * h + 3] = v.w;
+            }
+            const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(bp + kk * BN);
+            const ulonglong2 b1 = *reinterpret_cast<const ulonglong2*>(bp + kk * BN + BN / 2);
+            const uint64_t b[4] = {b0.x, b0.y, b1.x, b1.y};
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc2[i][j] = ffma2_bcast(a[i], b[j], acc2[i][j]);
+        }
+        slot = slot == kRing - 1 ? 0 : slot + 1;
+        if (++kb == KT) {  // last block of this tile: store it, restart
+            kb = 0;
+            const int64_t tile = blockIdx.x + lt * gridDim.x;
+            const int tm = (int)(tile / p.tiles_n);
+            const int m0 = tm * BM;
+            const int n0 = (int)(tile - (int64_t)tm * p.tiles_n) * BN;
+#pragma unroll
+            for (int ib = 0; ib < 2; ++ib) {
+                const int pbase = m0 + ib * (BM / 2) + pg * 4;
+                if (pbase >= p.m) continue;
+                const int n = pbase / p.ohw;
+                const int rem = pbase - n * p.ohw;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int co = n0 + (j >> 2) * (BN / 2) + cg * 4 + (j & 3);
+                    if (co >= p.co) continue;
+                    float v[4];
+#pragma unroll
+                    for (int ii = 0; ii < 4; ++ii) {
+                        const float2 pr = unpack2(acc2[ib * 4 + ii][j >> 1]);
+                        v[ii] = (j & 1) ? pr.y : pr.x;
+                    }
+                    *reinterpret_cast<float4*>(p.y + ((int64_t)n * p.co + co) * p.ohw + rem) =
+                        make_float4(v[0], v[1], v[2], v[3]);
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc2[i][j] = 0ull;
+            ++lt;
+        }
+    }
+    cp_async_wait<0>();
+}
+
+template <int BM, int BN, int T, int MINB>
+cudaError_t launch_1x1(const Problem& p, int sm_count, cudaStream_t s) {
+    constexpr int smem = kRing * kBK * (BM + BN) * (int)sizeof(float);
+    static std::once_flag once;
+    static cudaError_t attr = cudaSuccess;
+    auto kern = conv1x1_persistent_kernel<BM, BN, T, MINB>;
+    std::call_once(once, [&] {
+        attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    });
+    if (attr != cudaSuccess) return attr;
+    const int grid = (int)std::min<int64_t>(p.tiles, (int64_t)sm_count * MINB);
+    kern<<<grid, T, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+bool conv1x1_eligible(const smmc_geom& g) {
+    return g.k_h == 1 && g.k_w == 1 && g.s_h == 1 && g.s_w == 1 && g.p_h == 0 && g.p_w == 0 &&
+           (g.c_i % kBK) == 0 && ((g.h * g.w) & 3) == 0 && (g.c_o & 3) == 0;
+}
+
+// bn = 64 (128 x 64 tiles) for c_o <= 64, else 64 x 128 tiles; 4 CTAs per SM.
+// (64 x 256 tiles, 256 threads, 2 CTAs/SM — the input read once instead of
+// twice for c_o = 256 — measured 2x slower on the 64->256 layer, dropped.)
+cudaError_t launch_conv1x1(const Problem& p, int bn, int sm_count, cudaStream_t s) {
+    cudaError_t e = bn == 64 ? launch_1x1<128, 64, 128, 4>(p, sm_count, s)
+                             : launch_1x1<64, 128, 128, 4>(p, sm_count, s);
+    count_launches(1);
+    return e;
+}
+
+}  // namespace smmc

@@ -935,12 +935,14 @@ FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) {
             fg = e.groups;
         }
     }
+    bool env_forced = false;
     if (const char* f = getenv("SMMC_FORCE_PLAN")) {  // "variant,splits[,groups]"
         int v = -1, sp = -1, gr = 1;
         if (sscanf(f, "%d,%d,%d", &v, &sp, &gr) >= 2) {
             fv = v;
             fs = sp;
             fg = gr;
+            env_forced = true;
         }
     }
     // warp groups: tap-major blocks, classic split grid, instantiated
@@ -993,6 +995,26 @@ FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) {
         const char* f = getenv("SMMC_CLUSTER_RED");  // A/B hook
         if (!f || atoi(f) != 0) best.reduce_mode = 4;
     }
+    // 1x1 layers: the persistent block-stream kernel (no split, no
+    // workspace); the tiled kernel with the same tile is its fallback for
+    // operands that are not 16-byte aligned
+    const char* f1 = getenv("SMMC_1X1");  // A/B hook: 0 = tiled kernel
+    if (conv1x1_eligible(g) && (!f1 || atoi(f1) != 0) && !env_forced) {
+        const int v = g.c_o <= 64 ? 1 : 3;  // 128x64 or 64x128
+        const TileCfg t = kTiles[v];
+        best = FfmaPlan{};
+        best.variant = v;
+        best.bm = t.bm;
+        best.bn = t.bn;
+        best.threads = t.threads;
+        best.tiles_n = (int)((g.c_o + t.bn - 1) / t.bn);
+        best.tiles = ((m + t.bm - 1) / t.bm) * best.tiles_n;
+        best.splits = 1;
+        best.kt_per_split = kt_total;
+        best.reduce_mode = 0;
+        best.groups = 1;
+        best.persist1x1 = t.bn;
+    }
     best.bk = bk;
     best.kt_total = kt_total;
     best.cvec = cvec ? 1 : 0;
@@ -1028,6 +1050,7 @@ FfmaPlan plan_ffma_gather(const smmc_geom& g, int sm_count) {
         pl.sk_ctas = pl.sk_iters = pl.sk_maxseg = 0;
     }
     (void)m;
+    pl.persist1x1 = 0;
     pl.reduce_mode = 2;
     pl.ws_counter_offset = 0;
     pl.ws_bytes = (size_t)pl.tiles * pl.splits * pl.bm * pl.bn * sizeof(float);
@@ -1043,6 +1066,13 @@ cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
         count_launches(1);
     }
     cudaError_t e;
+    if (pl.persist1x1 && p.n_out == 1 &&
+        !(((uintptr_t)p.x | (uintptr_t)p.w | (uintptr_t)p.y) & 15)) {
+        int dev = 0, sms = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess)
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        return launch_conv1x1(p, pl.persist1x1, sms, s);
+    }
     if (pl.groups > 1) {
         const int key = pl.variant * 8 + pl.groups;
         switch (key) {

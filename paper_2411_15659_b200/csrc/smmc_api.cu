@@ -400,6 +400,10 @@ int smmc_plan_describe(const smmc_geom* g, int mode, char* buf, size_t len) {
         const size_t used = strlen(buf);
         snprintf(buf + used, len - used, ", %d warp groups x %d threads", pl.groups, pl.threads);
     }
+    if (pl.persist1x1) {
+        const size_t used = strlen(buf);
+        snprintf(buf + used, len - used, ", persistent 1x1 block stream (16-byte loads)");
+    }
     if (pl.reduce_mode == 3) {
         const size_t used = strlen(buf);
         snprintf(buf + used, len - used, ", stream-K %d CTAs x %d tap blocks", pl.sk_ctas,

@@ -328,3 +328,32 @@ def test_acceptance_sweep_200_random_geometries():
         assert np.array_equal(smm.smm_conv_batched(x, ws, g), y), g
         assert np.array_equal(smm.smm_conv_batched(x, ws, g, mode="exact"), ref), g
     assert worst > 0.0  # the FFMA path really reorders the sums
+
+
+@pytest.mark.parametrize("gt,n", [((64, 256, 56, 56, 1, 1), 3), ((256, 64, 28, 28, 1, 1), 2),
+                                  ((48, 100, 6, 10, 1, 1), 3), ((16, 4, 4, 4, 1, 1), 1)],
+                         ids=["64to256", "256to64", "ragged", "tiny"])
+def test_persistent_1x1_matches_tiled_kernel_bitwise(gt, n, monkeypatch):
+    """1x1 layers run the persistent block-stream kernel: same summation
+    order as the tiled kernel (bitwise equal to it), oracle parity, and the
+    tiled fallback for operands that are not 16-byte aligned."""
+    import torch
+    from paper_2411_15659_b200 import device
+    g = ConvGeometry(*gt)
+    assert "persistent 1x1" in _native.plan_describe(g, n)
+    x, w = synthetic_layer(g, n, 99)
+    wd = torch.from_numpy(smm.repack_weights(w, g)).cuda()
+    xd = torch.from_numpy(x).cuda()
+    y = device.conv2d(xd, wd, g)
+    buf = torch.empty(x.size + 1, device="cuda")
+    xm = buf[1:].view(x.shape)
+    xm.copy_(xd)
+    ym = device.conv2d(xm, wd, g)  # 4-byte aligned input: tiled fallback
+    # the tiled kernel on the same tile without split-K (same summation order)
+    monkeypatch.setenv("SMMC_FORCE_PLAN", "1,1" if g.out_channels <= 64 else "3,1")
+    assert "persistent" not in _native.plan_describe(g, n)
+    yt = device.conv2d(xd, wd, g)
+    torch.cuda.synchronize()
+    assert torch.equal(y, yt) and torch.equal(y, ym)
+    ref = orc.smm_conv_c(x, orc.repack(w), g, threads=orc.host_threads())
+    assert orc.max_abs_ratio(y.cpu().numpy(), ref) <= TOL_FP32

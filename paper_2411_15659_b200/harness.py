@@ -19,7 +19,8 @@ GPU counterparts of the reference's harness pieces, same formats:
   the lowered matrix for im2col (the paper's memory claim, Eq. 1).
 
 Backends: ``b200_smm`` (FFMA product), ``b200_exact`` (bitwise mode),
-``b200_bf16_tc`` (tcgen05 bf16 variant, own tolerance), ``b200_im2col``
+``b200_bf16_tc`` (tcgen05 bf16 variant, own tolerance), ``b200_bf16x3_tc``
+(fp32-accurate split-bf16 tensor-core path, fp32 checksum bar), ``b200_im2col``
 (explicit lowered matrix by a kernel of this library + a cuBLAS SGEMM with
 TF32 off — a plain library GEMM, the paper's comparator).
 
@@ -46,7 +47,7 @@ __all__ = [
     "SWEEP_KINDS",
 ]
 
-BACKENDS = ("b200_im2col", "b200_smm", "b200_exact", "b200_bf16_tc")
+BACKENDS = ("b200_im2col", "b200_smm", "b200_exact", "b200_bf16_tc", "b200_bf16x3_tc")
 SWEEP_KINDS = ("in_channels", "spatial", "kernel", "out_channels")
 CSV_HEADER = ("layer,backend,threads,repeats,median_time_s,scratch_bytes,"
               "speedup_vs_im2col,checksum")
@@ -190,6 +191,15 @@ def _backend(name, geom, batch, x, w_oihw):
             mod(mod.pack_input(x, out=xb), out=out)
             return out
         return True, run, scratch
+    if name == "b200_bf16x3_tc":  # fp32-accurate split-bf16 tensor-core path
+        if not device.tc_supported(geom, batch):
+            return False, None, 0
+        mod = device.Tc3SmmConv2d(geom, w_oihw)
+        out = torch.empty((batch,) + geom.output_shape, device=x.device)
+        # the [hi|lo|hi] bf16 channels-last input copy + split-K partial planes
+        scratch = (2 * 3 * batch * geom.padded_h * geom.padded_w * geom.in_channels +
+                   device.tc_workspace_bytes(geom, batch, split3=True))
+        return True, (lambda: mod(x, out=out)), scratch
     if name == "b200_im2col":
         import ctypes
         g = _native.Geom.of(geom, batch)
@@ -263,7 +273,8 @@ def run_bench(specs, backends, repeats=5, batch=1, seed=0):
                                         sums[name]))
             names = list(sums)
             for other in names[1:]:
-                tol = _CHECKSUM_RTOL_BF16 if "bf16" in (names[0] + other) else _CHECKSUM_RTOL
+                tol = (_CHECKSUM_RTOL_BF16 if "b200_bf16_tc" in (names[0], other)
+                       else _CHECKSUM_RTOL)  # the split-bf16 path meets the fp32 bar
                 if _rel(sums[names[0]], sums[other]) > tol:
                     raise ChecksumMismatchError(
                         f"checksum divergence on layer {spec.name!r}: {names[0]}="

@@ -87,6 +87,11 @@ def test_run_bench_gpu_all_backends():
     by = {(r.layer, r.backend): r for r in recs}
     # strided stem: the bf16 tensor-core variant is unsupported, recorded as such
     assert by[("l2", "b200_bf16_tc")].unsupported
+    assert by[("l2", "b200_bf16x3_tc")].unsupported
+    for layer in ("l1", "l3"):  # fp32-accurate split-bf16: the fp32 checksum bar
+        r, base = by[(layer, "b200_bf16x3_tc")], by[(layer, "b200_im2col")]
+        assert abs(r.checksum - base.checksum) <= 1e-3 * abs(base.checksum)
+        assert r.scratch_bytes > 0
     for layer in ("l1", "l2", "l3"):
         im2col = by[(layer, "b200_im2col")]
         g = next(s.geometry for s in specs if s.name == layer)

@@ -520,14 +520,20 @@ __global__ void __launch_bounds__(THREADS * G, (G > 1 ? 1 : MINB)) conv_ffma_ker
             const int cl = e / (BM / 4);
             const int px = (e - cl * (BM / 4)) * 4;
             const int off = cl * LD + px;
-            float4 a4 = *reinterpret_cast<const float4*>(cluster.map_shared_rank(part, 0) + off);
-            for (int z = 1; z < S; ++z) {
-                const float4 v = *reinterpret_cast<const float4*>(cluster.map_shared_rank(part, z) + off);
-                a4.x += v.x;
-                a4.y += v.y;
-                a4.z += v.z;
-                a4.w += v.w;
-            }
+            // all S (<= 8) remote loads in flight, then the fixed-order sum
+            float4 v[8];
+#pragma unroll
+            for (int z = 0; z < 8; ++z)
+                if (z < S) v[z] = *reinterpret_cast<const float4*>(cluster.map_shared_rank(part, z) + off);
+            float4 a4 = v[0];
+#pragma unroll
+            for (int z = 1; z < 8; ++z)
+                if (z < S) {
+                    a4.x += v[z].x;
+                    a4.y += v[z].y;
+                    a4.z += v[z].z;
+                    a4.w += v[z].w;
+                }
             const int co = n0 + cl;
             const int pbase = m0 + px;
             if (co >= p.co || pbase >= p.m) continue;

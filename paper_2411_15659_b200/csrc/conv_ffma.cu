@@ -732,14 +732,14 @@ template <int BM, int BN, int T, int MINB, int TM, int BK, int KH, int KW, int S
           bool CVEC, bool SK = false, int G = 1>
 cudaError_t launch_one(const Problem& p, dim3 grid, cudaStream_t s) {
     if constexpr (G == 1)
-        if (CVEC && !SK && p.reduce_mode == 3)
+        if (!SK && p.reduce_mode == 3)
             return launch_one<BM, BN, T, MINB, TM, BK, KH, KW, SH, SW, CVEC, true>(p, grid, s);
     constexpr int ring = G * kStages * BK * (BM + BN) * (int)sizeof(float);
     constexpr int part = BN * (BM + 4) * (int)sizeof(float);  // reduce_mode 4 partial tile
     constexpr int smem_max = ring > part ? ring : part;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
-    auto kern = conv_ffma_kernel<BM, BN, T, MINB, TM, BK, KH, KW, SH, SW, CVEC, SK && CVEC, G>;
+    auto kern = conv_ffma_kernel<BM, BN, T, MINB, TM, BK, KH, KW, SH, SW, CVEC, SK, G>;
     std::call_once(once, [&] {
         attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
     });
@@ -891,6 +891,8 @@ FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) {
     // conv512@7 at N=32, but slower than split-K on many-wave layers.
     const int64_t best_waves = best_cost_waves(best, m, g.c_o, sm_count);
     const double classic_cost = best_cost;
+    // (tap-major layers only: on the c_i = 3 stems stream-K measured 8-24 %
+    // slower than the classic grid; forced plans still reach it)
     for (int v = 0; v < kNumTiles && cvec && best_waves <= 2; ++v) {
         const TileCfg t = kTiles[v];
         if (!t.model) continue;
@@ -957,7 +959,7 @@ FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) {
                            ((fg == 2 && (fv == 0 || fv == 1 || fv == 3)) ||
                             (fg == 4 && (fv == 1 || fv == 3)));
     if (!groups_ok) fg = 1;
-    if (fv >= 0 && fv < kNumTiles && fs >= 0 && (fs > 0 || cvec)) {
+    if (fv >= 0 && fv < kNumTiles && fs >= 0) {
         const TileCfg t = kTiles[fv];
         best = FfmaPlan{};
         best.variant = fv;

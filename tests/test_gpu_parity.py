@@ -357,3 +357,28 @@ def test_persistent_1x1_matches_tiled_kernel_bitwise(gt, n, monkeypatch):
     assert torch.equal(y, yt) and torch.equal(y, ym)
     ref = orc.smm_conv_c(x, orc.repack(w), g, threads=orc.host_threads())
     assert orc.max_abs_ratio(y.cpu().numpy(), ref) <= TOL_FP32
+
+
+@pytest.mark.parametrize("plan", ["1,0", "2,0", "0,0", "3,0"])
+@pytest.mark.parametrize("gt,n", [((3, 64, 40, 40, 7, 7, 2, 2, 3, 3), 3),
+                                  ((3, 40, 47, 47, 11, 11, 4, 4, 0, 0), 2),
+                                  ((5, 24, 19, 23, 3, 5, 1, 2, 1, 2), 2)],
+                         ids=["7x7s2", "11x11s4", "ragged"])
+def test_stream_k_on_the_generic_k_order(gt, n, plan, monkeypatch):
+    """Stream-K over the reference's (c, j, k) update order (the c_i = 3 stems
+    and any c_i % 16 != 0 layer): oracle parity, deterministic."""
+    import torch
+    from paper_2411_15659_b200 import device
+    monkeypatch.setenv("SMMC_FORCE_PLAN", plan)
+    g = ConvGeometry(*gt)
+    desc = _native.plan_describe(g, n)
+    assert "stream-K" in desc and "(c,j,k)" in desc, desc
+    x, w = synthetic_layer(g, n, 5)
+    wd = torch.from_numpy(smm.repack_weights(w, g)).cuda()
+    xd = torch.from_numpy(x).cuda()
+    y1 = device.conv2d(xd, wd, g)
+    y2 = device.conv2d(xd, wd, g)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2), desc
+    ref = orc.smm_conv_c(x, orc.repack(w), g, threads=orc.host_threads())
+    assert orc.max_abs_ratio(y1.cpu().numpy(), ref) <= TOL_FP32, desc

@@ -812,7 +812,7 @@ struct TunedPlan {
 constexpr TunedPlan kTuned[] = {
     // N=1: warp-group split-K (third field: groups per CTA), measured as
     // 20 back-to-back launches in a graph (tools/plan_table_sweep.py)
-    {1, 64, 56, 56, 64, 3, 1, 1, 1, 4, 4},     // 13.5 us (1,8: 14.1)
+    {1, 64, 56, 56, 64, 3, 1, 1, 1, 4, 3},     // 12.3 us (1,4,4: 13.1; 1,8: 14.1)
     {1, 128, 28, 28, 128, 3, 1, 1, 1, 8, 2},   // 13.2 us (1,8: 14.4)
     {1, 256, 14, 14, 256, 3, 1, 1, 1, 16, 2},  // 13.9 us (0,32: 15.3)
     {1, 512, 7, 7, 512, 3, 1, 1, 3, 32, 2},    // 15.4 us (3,32: 16.8; model 42.9)
@@ -957,7 +957,7 @@ FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) {
     // (variant, G) pairs only
     const bool groups_ok = cvec && fs > 0 &&
                            ((fg == 2 && (fv == 0 || fv == 1 || fv == 3)) ||
-                            (fg == 4 && (fv == 1 || fv == 3)));
+                            ((fg == 3 || fg == 4) && (fv == 1 || fv == 3)));
     if (!groups_ok) fg = 1;
     if (fv >= 0 && fv < kNumTiles && fs >= 0) {
         const TileCfg t = kTiles[fv];
@@ -1086,6 +1086,8 @@ cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
         switch (key) {
             case 0 * 8 + 2: e = launch_tile_groups<128, 128, 256, 2>(p, pl.tap_kind, grid, s); break;
             case 1 * 8 + 2: e = launch_tile_groups<128, 64, 128, 2>(p, pl.tap_kind, grid, s); break;
+            case 1 * 8 + 3: e = launch_tile_groups<128, 64, 128, 3>(p, pl.tap_kind, grid, s); break;
+            case 3 * 8 + 3: e = launch_tile_groups<64, 128, 128, 3>(p, pl.tap_kind, grid, s); break;
             case 1 * 8 + 4: e = launch_tile_groups<128, 64, 128, 4>(p, pl.tap_kind, grid, s); break;
             case 3 * 8 + 2: e = launch_tile_groups<64, 128, 128, 2>(p, pl.tap_kind, grid, s); break;
             case 3 * 8 + 4: e = launch_tile_groups<64, 128, 128, 4>(p, pl.tap_kind, grid, s); break;

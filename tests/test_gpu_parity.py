@@ -246,7 +246,7 @@ def test_every_reduction_mode_matches_oracle(plan, cluster, monkeypatch):
 
 @pytest.mark.parametrize("cluster", ["1", "0"])
 @pytest.mark.parametrize("plan", ["1,1,4", "3,1,2", "0,1,2", "1,3,2", "1,8,4", "3,6,4", "1,16,4",
-                                  "3,32,2", "0,12,2"])
+                                  "3,32,2", "0,12,2", "1,4,3", "3,5,3"])
 def test_warp_group_split_matches_oracle(plan, cluster, monkeypatch):
     """Warp-group split-K (G groups per CTA over the CTA's tap blocks, partial
     tiles summed in group order through shared memory) under every outer

@@ -157,13 +157,32 @@ int ensure_streams(HostPool& hp) {
     return SMMC_OK;
 }
 
-HostPool& pool_for(int device) {
+// A free (unlocked) staging pool of `device`, returned LOCKED: concurrent
+// host-entry calls from several threads (independent layers) each get their
+// own streams and buffers and overlap on the copy engines, up to
+// kMaxPools per device; beyond that callers queue on a pool.
+constexpr int kMaxPools = 4;
+HostPool& acquire_pool(int device) {
     static std::mutex mu;
-    static std::vector<HostPool*> pools;
-    std::lock_guard<std::mutex> lk(mu);
-    if (device >= (int)pools.size()) pools.resize(device + 1, nullptr);
-    if (!pools[device]) pools[device] = new HostPool();
-    return *pools[device];
+    static std::vector<std::vector<HostPool*>> pools;
+    HostPool* wait_on = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (device >= (int)pools.size()) pools.resize(device + 1);
+        auto& v = pools[device];
+        for (HostPool* hp : v)
+            if (hp->mu.try_lock()) return *hp;
+        if ((int)v.size() < kMaxPools) {
+            HostPool* hp = new HostPool();
+            hp->mu.lock();
+            v.push_back(hp);
+            return *hp;
+        }
+        static unsigned rr = 0;
+        wait_on = v[rr++ % v.size()];
+    }
+    wait_on->mu.lock();
+    return *wait_on;
 }
 
 int ensure(HostPool& hp, int i, size_t bytes) {
@@ -518,8 +537,8 @@ int host_pipeline(const float* x, const float* w_smm, const float* w_dev, float*
         return SMMC_ESHAPE;
     }
     if ((st = select_device(device))) return st;
-    HostPool& hp = pool_for(device);
-    std::lock_guard<std::mutex> lk(hp.mu);
+    HostPool& hp = acquire_pool(device);
+    std::lock_guard<std::mutex> lk(hp.mu, std::adopt_lock);
     if ((st = ensure_streams(hp))) return st;
     const size_t xs = (size_t)g->c_i * g->h * g->w;          // floats per input sample
     const size_t ys = (size_t)g->c_o * oh * ow;              // floats per output sample
@@ -907,8 +926,8 @@ int smmc_extract_slice_f32_host(const float* x, const smmc_geom* g, int32_t c, i
         return SMMC_EINDEX;
     }
     if ((st = select_device(device))) return st;
-    HostPool& hp = pool_for(device);
-    std::lock_guard<std::mutex> lk(hp.mu);
+    HostPool& hp = acquire_pool(device);
+    std::lock_guard<std::mutex> lk(hp.mu, std::adopt_lock);
     if ((st = ensure_streams(hp))) return st;
     const size_t xb = (size_t)g->c_i * g->h * g->w * sizeof(float);
     const size_t bb = (size_t)(g->h + 2 * g->p_h) * ow * sizeof(float);
@@ -935,8 +954,8 @@ int smmc_scalar_matrix_fma_f32_host(float alpha, const float* src, int64_t src_r
     if (!rows || !cols) return SMMC_OK;
     int st = select_device(device);
     if (st) return st;
-    HostPool& hp = pool_for(device);
-    std::lock_guard<std::mutex> lk(hp.mu);
+    HostPool& hp = acquire_pool(device);
+    std::lock_guard<std::mutex> lk(hp.mu, std::adopt_lock);
     if ((st = ensure_streams(hp))) return st;
     const size_t sb = ((size_t)(rows - 1) * src_row_stride + cols) * sizeof(float);
     const size_t db = ((size_t)(rows - 1) * dst_row_stride + cols) * sizeof(float);

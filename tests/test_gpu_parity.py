@@ -382,3 +382,41 @@ def test_stream_k_on_the_generic_k_order(gt, n, plan, monkeypatch):
     assert torch.equal(y1, y2), desc
     ref = orc.smm_conv_c(x, orc.repack(w), g, threads=orc.host_threads())
     assert orc.max_abs_ratio(y1.cpu().numpy(), ref) <= TOL_FP32, desc
+
+
+def test_random_geometries_wide_channels():
+    """150 random geometries beyond the reference's small-channel acceptance
+    ranges: c_i multiples of 16 (the tap-major K order, 16-byte weight rows)
+    and ragged c_o, planes 1-40 wide, kernels 1-5, strides 1-2, batches 1-6 —
+    whatever plan the planner picks (split-K, cluster DSMEM, reduce kernel,
+    stream-K, warp groups, the persistent 1x1 kernel), within the fp32 bar of
+    the oracle (BASELINE signed data) and bitwise deterministic."""
+    import torch
+    from paper_2411_15659_b200 import device
+    rng = np.random.default_rng(424242)
+    checked = 0
+    plans = set()
+    while checked < 150:
+        ci = int(rng.choice((16, 32, 48, 64, 96, 128)))
+        co = int(rng.integers(1, 200))
+        h, w = int(rng.integers(1, 41)), int(rng.integers(1, 41))
+        k = int(rng.choice((1, 3, 5)))
+        s = int(rng.choice((1, 1, 2)))
+        p = int(rng.choice((0, 1, 2)))
+        if k > h + 2 * p or k > w + 2 * p:
+            continue
+        g = ConvGeometry(ci, co, h, w, k, k, s, s, p, p)
+        n = int(rng.integers(1, 7))
+        checked += 1
+        x, wt = synthetic_layer(g, n, checked)
+        wd = torch.from_numpy(smm.repack_weights(wt, g)).cuda()
+        xd = torch.from_numpy(x).cuda()
+        y1 = device.conv2d(xd, wd, g)
+        y2 = device.conv2d(xd, wd, g)
+        torch.cuda.synchronize()
+        desc = _native.plan_describe(g, n)
+        plans.add(desc.split("reduce=")[-1].split(")")[0])
+        assert torch.equal(y1, y2), (g, n, desc)
+        ref = orc.smm_conv_c(x, orc.repack(wt), g, threads=orc.host_threads())
+        assert orc.max_abs_ratio(y1.cpu().numpy(), ref) <= TOL_FP32, (g, n, desc)
+    assert len(plans) >= 3, plans  # several reduction schemes were exercised

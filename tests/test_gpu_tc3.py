@@ -120,3 +120,19 @@ def test_tc3_entry_point_errors():
     xs = torch.zeros((1,) + g5.input_shape, device="cuda")
     with pytest.raises(BackendUnsupportedError):
         device.pack_input_bf16x3(xs, g5)
+
+
+def test_conv2d_estimator_tc3_backend():
+    """The drop-in Conv2D with backend="smm_tc3": same fit/transform surface,
+    the fp32 bar against the oracle, strided layers rejected at fit."""
+    from paper_2411_15659_b200 import Conv2D
+    rng = np.random.default_rng(8)
+    X = rng.uniform(-1, 1, (3, 16, 12, 12)).astype(np.float32)
+    est = Conv2D(out_channels=24, kernel_size=3, padding=1, backend="smm_tc3").fit(X)
+    Y = est.transform(X)
+    g = est.geometry_
+    ref = orc.smm_conv_c(X, orc.repack(est.weights_), g, threads=orc.host_threads())
+    assert Y.shape == (3,) + g.output_shape
+    assert orc.max_abs_ratio(Y, ref) <= TOL_FP32
+    with pytest.raises(BackendUnsupportedError):
+        Conv2D(out_channels=8, stride=2, backend="smm_tc3").fit(X)

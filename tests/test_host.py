@@ -145,5 +145,12 @@ def test_estimator_params_and_fit_without_gpu():
         smm.Conv2D(out_channels=2, backend="winograd").fit(X)
     with pytest.raises(BackendUnsupportedError):
         smm.Conv2D(out_channels=2, backend="im2col").fit(X)
+    # the split-bf16 tensor-core backend: c_i % 8 == 0 and stride 1 (host check at fit)
+    with pytest.raises(BackendUnsupportedError):
+        smm.Conv2D(out_channels=2, backend="smm_tc3").fit(X)
+    X8 = np.zeros((1, 8, 6, 6), np.float32)
+    assert smm.Conv2D(out_channels=2, backend="smm_tc3").fit(X8).geometry_.in_channels == 8
+    with pytest.raises(BackendUnsupportedError):
+        smm.Conv2D(out_channels=2, stride=2, backend="smm_tc3").fit(X8)
     with pytest.raises(ValueError):
         smm.Conv2D(out_channels=2, weights=np.zeros((1, 2, 3, 3), np.float32)).fit(X)

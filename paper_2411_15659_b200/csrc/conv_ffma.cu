@@ -840,7 +840,7 @@ int64_t best_cost_waves(const FfmaPlan& b, int64_t m, int c_o, int sm_count) {
 // to per_sm * BM * BN * (work per CTA in 8-deep tap blocks, plus a prologue /
 // epilogue term and ~3 blocks of partial-tile traffic when split), with a
 // small per-split overhead.
-FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) {
+static FfmaPlan plan_ffma_impl(const smmc_geom& g, int sm_count, bool allow_stem) {
     FfmaPlan best{};
     double best_cost = 1e300;
     const int oh = (g.h + 2 * g.p_h - g.k_h) / g.s_h + 1;
@@ -1023,6 +1023,23 @@ FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) {
         best.groups = 1;
         best.persist1x1 = t.bn;
     }
+    // c_i <= 4 stems: the direct register-window kernel (weights resident in
+    // smem, no zero-packed A tiles); the tiled kernel stays the fallback for
+    // the fused gather and for forced plans
+    if (allow_stem && !env_forced && stem_kind(g)) {
+        const int kind = stem_kind(g);
+        best = FfmaPlan{};
+        best.bm = 128;  // 16 pixel groups of 8 columns per 128-thread CTA
+        best.bn = stem_bn(g, kind);
+        best.threads = 128;
+        best.tiles_n = (g.c_o + best.bn - 1) / best.bn;
+        best.tiles = ((m + best.bm - 1) / best.bm) * best.tiles_n;
+        best.splits = 1;
+        best.kt_per_split = kt_total;
+        best.reduce_mode = 0;
+        best.groups = 1;
+        best.stem = kind;
+    }
     best.bk = bk;
     best.kt_total = kt_total;
     best.cvec = cvec ? 1 : 0;
@@ -1046,8 +1063,11 @@ FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) {
 // mode 2, so the conv kernel keeps its single-output epilogue and the (already
 // needed, or one extra tiny) placement pass splitk_reduce_kernel writes the
 // replicas — local and NVLink peer memory — in split order.
+FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) { return plan_ffma_impl(g, sm_count, true); }
+
 FfmaPlan plan_ffma_gather(const smmc_geom& g, int sm_count) {
-    FfmaPlan pl = plan_ffma(g, sm_count);
+    // the gather epilogue lives in the tiled kernel: plan without the stem kernel
+    FfmaPlan pl = plan_ffma_impl(g, sm_count, false);
     const int64_t m = (int64_t)g.n * ((g.h + 2 * g.p_h - g.k_h) / g.s_h + 1) *
                       ((g.w + 2 * g.p_w - g.k_w) / g.s_w + 1);
     if (pl.reduce_mode == 3) {  // stream-K -> classic split grid of similar size
@@ -1074,6 +1094,7 @@ cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
         count_launches(1);
     }
     cudaError_t e;
+    if (pl.stem && p.n_out == 1) return launch_stem(p, pl.stem, s);
     if (pl.persist1x1 && p.n_out == 1 &&
         !(((uintptr_t)p.x | (uintptr_t)p.w | (uintptr_t)p.y) & 15)) {
         int dev = 0, sms = 148;

@@ -419,6 +419,10 @@ int smmc_plan_describe(const smmc_geom* g, int mode, char* buf, size_t len) {
         const size_t used = strlen(buf);
         snprintf(buf + used, len - used, ", %d warp groups x %d threads", pl.groups, pl.threads);
     }
+    if (pl.stem) {
+        const size_t used = strlen(buf);
+        snprintf(buf + used, len - used, ", direct stem kernel (weights in smem, register windows)");
+    }
     if (pl.persist1x1) {
         const size_t used = strlen(buf);
         snprintf(buf + used, len - used, ", persistent 1x1 block stream (16-byte loads)");

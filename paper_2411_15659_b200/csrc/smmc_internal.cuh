@@ -66,6 +66,7 @@ struct FfmaPlan {
     int reduce_mode;   // 0 none, 1 last-arriver, 2 reduce kernel, 3 stream-K, 4 cluster DSMEM
     int groups;        // warp groups per CTA splitting the CTA's tap blocks (1 = off)
     int persist1x1;    // 1x1 layers: persistent block-stream kernel (conv_1x1.cu), BN = 64/128
+    int stem;          // c_i <= kStemMaxCi layers: direct register-window kernel (conv_stem.cu) kind
     int64_t tiles;     // pixel tiles x channel tiles
     int tiles_n;
     int sk_ctas;       // stream-K grid
@@ -78,6 +79,11 @@ FfmaPlan plan_ffma(const smmc_geom& g, int sm_count);
 FfmaPlan plan_ffma_gather(const smmc_geom& g, int sm_count);
 cudaError_t launch_ffma(const Problem& p, const FfmaPlan& plan, cudaStream_t s);
 bool conv1x1_eligible(const smmc_geom& g);
+constexpr int kStemMaxCi = 4;
+constexpr size_t kStemMaxSmem = 200 * 1024;
+int stem_kind(const smmc_geom& g);
+int stem_bn(const smmc_geom& g, int kind);
+cudaError_t launch_stem(const Problem& p, int kind, cudaStream_t s);
 cudaError_t launch_conv1x1(const Problem& p, int bn, int sm_count, cudaStream_t s);
 int ffma_launches(const FfmaPlan& plan);
 // bf16 tensor-core variant (conv_tc.cu)

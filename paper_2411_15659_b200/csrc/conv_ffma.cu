@@ -1029,7 +1029,7 @@ static FfmaPlan plan_ffma_impl(const smmc_geom& g, int sm_count, bool allow_stem
     if (allow_stem && !env_forced && stem_kind(g)) {
         const int kind = stem_kind(g);
         best = FfmaPlan{};
-        best.bm = 128;  // 16 pixel groups of 8 columns per 128-thread CTA
+        best.bm = 128;  // nominal pixels per CTA (the stem kernel tiles rows itself)
         best.bn = stem_bn(g, kind);
         best.threads = 128;
         best.tiles_n = (g.c_o + best.bn - 1) / best.bn;

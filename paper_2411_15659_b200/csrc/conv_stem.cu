@@ -10,7 +10,7 @@
 //
 //   * the CTA's whole weight slice W_smm[:, :, :, co0:co0+BN] (K x BN floats,
 //     <= 46 KB at BASELINE shapes) is staged in shared memory once;
-//   * a thread owns 8 consecutive output columns x CPT output channels
+//   * a thread owns PX consecutive output columns x CPT output channels
 //     (CPT/2 packed FFMA2 accumulator pairs per pixel);
 //   * per (c, kh) input row it loads its (7*SW + KW)-wide window once through
 //     the read-only path (the zero padding is a predicate: out-of-range
@@ -36,20 +36,21 @@ struct StemParams {
     const float* w;
     float* y;
     int c_i, h, w_in, co, sh, ph, pw, oh, ow;
-    int gpr;        // 8-pixel column groups per output row
+    int gpr;        // PX-pixel column groups per output row
     int pg_total;   // n * oh * gpr
     int ohgpr;      // oh * gpr
     int k;          // c_i * KW * KH
+    int n;
 };
 
 // T threads = (T/32) warps; a warp = (32/NG) pixel groups x NG channel groups.
 // PF: software-pipelined windows (row r+1 in flight while row r is consumed).
-template <int KH, int KW, int SW, int CPT, int NG, int T, int MINB, bool PF>
+template <int KH, int KW, int SW, int PX, int CPT, int NG, int T, int MINB, bool PF>
 __global__ void __launch_bounds__(T, MINB) conv_stem_kernel(const StemParams p) {
     constexpr int BN = CPT * NG;
     constexpr int PGW = 32 / NG;          // pixel groups per warp
     constexpr int PGC = (T / 32) * PGW;   // pixel groups per CTA
-    constexpr int WIN = 7 * SW + KW;      // input columns one thread reads per row
+    constexpr int WIN = (PX - 1) * SW + KW;  // input columns one thread reads per row
     constexpr int CP = CPT / 2;
     extern __shared__ __align__(16) float s_w[];  // [k][BN]
 
@@ -81,13 +82,13 @@ __global__ void __launch_bounds__(T, MINB) conv_stem_kernel(const StemParams p) 
     const int n = pg / p.ohgpr;
     const int rem = pg - n * p.ohgpr;
     const int orow = rem / p.gpr;
-    const int ow0 = (rem - orow * p.gpr) * 8;
+    const int ow0 = (rem - orow * p.gpr) * PX;
     const int iw0 = ow0 * SW - p.pw;
     const int ih0 = orow * p.sh - p.ph;
 
-    uint64_t acc[8][CP];
+    uint64_t acc[PX][CP];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < PX; ++i)
 #pragma unroll
         for (int q = 0; q < CP; ++q) acc[i][q] = 0ull;
 
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(T, MINB) conv_stem_kernel(const StemParams p) 
                 wp[q + 1] = v.y;
             }
 #pragma unroll
-            for (int px = 0; px < 8; ++px)
+            for (int px = 0; px < PX; ++px)
 #pragma unroll
                 for (int q = 0; q < CP; ++q)
                     acc[px][q] = ffma2_bcast(win[px * SW + kw], wp[q], acc[px][q]);
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(T, MINB) conv_stem_kernel(const StemParams p) 
 
     // epilogue: NCHW, 8 consecutive columns per channel
     const int64_t ohw = (int64_t)p.oh * p.ow;
-    const bool vec = (p.ow & 3) == 0 && ow0 + 8 <= p.ow;
+    const bool vec = PX % 4 == 0 && (p.ow & 3) == 0 && ow0 + PX <= p.ow;
     float* yrow = p.y + ((int64_t)n * p.co) * ohw + (int64_t)orow * p.ow + ow0;
 #pragma unroll
     for (int q = 0; q < CP; ++q) {
@@ -162,34 +163,39 @@ __global__ void __launch_bounds__(T, MINB) conv_stem_kernel(const StemParams p) 
         for (int h2 = 0; h2 < 2; ++h2) {
             const int co = co_base + cg * CPT + 2 * q + h2;
             if (co >= p.co) continue;
-            float v[8];
+            float v[PX];
 #pragma unroll
-            for (int px = 0; px < 8; ++px) {
+            for (int px = 0; px < PX; ++px) {
                 const uint64_t a = acc[px][q];
                 v[px] = __uint_as_float(h2 ? (uint32_t)(a >> 32) : (uint32_t)a);
             }
             float* dst = yrow + (int64_t)co * ohw;
             if (vec) {
-                reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
-                reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
+#pragma unroll
+                for (int v4 = 0; v4 < PX / 4; ++v4)
+                    reinterpret_cast<float4*>(dst)[v4] =
+                        make_float4(v[4 * v4], v[4 * v4 + 1], v[4 * v4 + 2], v[4 * v4 + 3]);
             } else {
 #pragma unroll
-                for (int px = 0; px < 8; ++px)
+                for (int px = 0; px < PX; ++px)
                     if (ow0 + px < p.ow) dst[px] = v[px];
             }
         }
     }
 }
 
-template <int KH, int KW, int SW, int CPT, int NG, int T, int MINB, bool PF>
-cudaError_t launch_stem_t(const StemParams& sp, cudaStream_t s) {
+template <int KH, int KW, int SW, int PX, int CPT, int NG, int T, int MINB, bool PF>
+cudaError_t launch_stem_t(StemParams sp, cudaStream_t s) {
+    sp.gpr = (sp.ow + PX - 1) / PX;
+    sp.ohgpr = sp.oh * sp.gpr;
+    sp.pg_total = sp.n * sp.ohgpr;
     constexpr int BN = CPT * NG;
     constexpr int PGC = (T / 32) * (32 / NG);
     const size_t smem = (size_t)sp.k * BN * sizeof(float);
     if (smem > kStemMaxSmem) return cudaErrorInvalidConfiguration;
     static std::once_flag once;
     static cudaError_t attr = cudaSuccess;
-    auto kern = conv_stem_kernel<KH, KW, SW, CPT, NG, T, MINB, PF>;
+    auto kern = conv_stem_kernel<KH, KW, SW, PX, CPT, NG, T, MINB, PF>;
     std::call_once(once, [&] {
         attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)kStemMaxSmem);
@@ -202,15 +208,46 @@ cudaError_t launch_stem_t(const StemParams& sp, cudaStream_t s) {
 
 }  // namespace
 
+// Thread tiles (PX pixels x CPT channels, NG channel groups per warp, T
+// threads, MINB CTAs/SM, PF pipelined windows), measured on B200
+// (tools/stem_ab*.sh); overridable at build time for A/B libraries.
+#ifndef SV1_PX
+#define SV1_PX 8
+#define SV1_CPT 8
+#define SV1_NG 8
+#define SV1_T 128
+#define SV1_MINB 3
+#define SV1_PF false
+#endif
+#ifndef SV2_PX
+#define SV2_PX 8
+#define SV2_CPT 8
+#define SV2_NG 8
+#define SV2_T 128
+#define SV2_MINB 3
+#define SV2_PF true
+#endif
+#ifndef SV3_PX
+#define SV3_PX 4
+#define SV3_CPT 16
+#define SV3_NG 2
+#define SV3_T 128
+#define SV3_MINB 3
+#define SV3_PF true
+#endif
+
 // Layers with an instantiated stem kernel: c_i <= 4 with (KH, KW, SW) =
 // (7, 7, 2) or (11, 11, 4), the BASELINE config-3 stems.  (3x3 s1 c_i = 3 —
-// VGG conv1_1 — and 5x5 were measured no faster than the tiled kernel with
-// this loop nest.)
+// VGG conv1_1 — measured 448-487 us against 457 us for the tiled kernel;
+// STEM_K1 builds it for A/B.  DESIGN.md §3.1.)
 int stem_kind(const smmc_geom& g) {
     const char* f = getenv("SMMC_STEM");  // A/B hook: 0 = tiled kernel
     if (f && atoi(f) == 0) return 0;
     if (g.c_i > kStemMaxCi) return 0;
     int kind = 0;
+#ifdef STEM_K1
+    if (g.k_h == 3 && g.k_w == 3 && g.s_w == 1) kind = 1;
+#endif
     if (g.k_h == 7 && g.k_w == 7 && g.s_w == 2) kind = 2;
     else if (g.k_h == 11 && g.k_w == 11 && g.s_w == 4) kind = 3;
     if (!kind) return 0;
@@ -221,7 +258,7 @@ int stem_kind(const smmc_geom& g) {
 
 int stem_bn(const smmc_geom& g, int kind) {
     (void)g;
-    return kind == 3 ? 32 : 64;
+    return kind == 1 ? SV1_CPT * SV1_NG : kind == 2 ? SV2_CPT * SV2_NG : SV3_CPT * SV3_NG;
 }
 
 cudaError_t launch_stem(const Problem& p, int kind, cudaStream_t s) {
@@ -238,16 +275,16 @@ cudaError_t launch_stem(const Problem& p, int kind, cudaStream_t s) {
     sp.pw = p.pw;
     sp.oh = p.oh;
     sp.ow = p.ow;
-    sp.gpr = (p.ow + 7) / 8;
-    sp.ohgpr = p.oh * sp.gpr;
-    sp.pg_total = p.n * sp.ohgpr;
+    sp.n = p.n;
     sp.k = p.k;
     cudaError_t e;
     switch (kind) {
-        // measured on B200 (tools/stem_ab.sh): 7x7 s2 best with the pipelined
-        // windows, 11x11 s4 (39-wide windows) without
-        case 2: e = launch_stem_t<7, 7, 2, 8, 8, 128, 3, true>(sp, s); break;
-        case 3: e = launch_stem_t<11, 11, 4, 4, 8, 128, 4, false>(sp, s); break;
+        // measured on B200 (tools/stem_ab.sh, 20 launches back to back):
+        // 7x7 s2: 8 px x 8 c_o 56.9 us (4 px x 16 c_o 77 us); 11x11 s4:
+        // 4 px x 16 c_o pipelined 52.7 us (8 x 4 64.2, 2 x 32 54-58, tiled 71.8)
+        case 1: e = launch_stem_t<3, 3, 1, SV1_PX, SV1_CPT, SV1_NG, SV1_T, SV1_MINB, SV1_PF>(sp, s); break;
+        case 2: e = launch_stem_t<7, 7, 2, SV2_PX, SV2_CPT, SV2_NG, SV2_T, SV2_MINB, SV2_PF>(sp, s); break;
+        case 3: e = launch_stem_t<11, 11, 4, SV3_PX, SV3_CPT, SV3_NG, SV3_T, SV3_MINB, SV3_PF>(sp, s); break;
         default: return cudaErrorInvalidConfiguration;
     }
     count_launches(1);

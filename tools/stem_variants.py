@@ -1,0 +1,31 @@
+"""Build A/B libraries that differ only in the stem kernel thread tiles
+(lib/ab/<name>.so; conv_stem.cu recompiled with SV*_ defines, linked with the
+main build objects).  Run from the repo root after the main build."""
+import subprocess, sys
+sys_path_fix = __import__("sys").path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[1]))
+from pathlib import Path
+from paper_2411_15659_b200 import build as b
+V = {
+ "a6": ("SV3", (2,32,1,128,3,0)), "a7": ("SV3", (4,16,2,128,3,1)), "a8": ("SV3", (4,16,2,256,2,0)),
+ "b1": ("SV2", (4,16,4,128,3,1)), "b2": ("SV2", (4,16,4,128,3,0)), "b3": ("SV2", (4,8,8,128,4,1)),
+ "c1": ("SV1", (4,16,4,128,3,0)), "c2": ("SV1", (8,8,8,128,3,0)), "c3": ("SV1", (4,16,4,128,3,1)),
+}
+exe = b.nvcc()
+objs = [str(o) for o in sorted(Path("build/smmc").glob("*.o")) if o.stem != "conv_stem"]
+procs = []
+for k, (pre, (px, cpt, ng, t, mb, pf)) in V.items():
+    d = [f"-D{pre}_PX={px}", f"-D{pre}_CPT={cpt}", f"-D{pre}_NG={ng}", f"-D{pre}_T={t}",
+         f"-D{pre}_MINB={mb}", f"-D{pre}_PF={'true' if pf else 'false'}"]
+    if pre == "SV1": d.append("-DSTEM_K1=1")
+    obj = f"/tmp/stem_{k}.o"
+    cmd = [exe, *b.ARCH, *b.NVCC_FLAGS, *d, "-c", "paper_2411_15659_b200/csrc/conv_stem.cu", "-o", obj]
+    procs.append((k, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
+for k, obj, p in procs:
+    out, _ = p.communicate()
+    assert p.returncode == 0, out.decode()[-3000:]
+    spill = [l for l in out.decode().splitlines() if "spill" in l and not l.strip().startswith("0 bytes stack frame, 0 bytes spill stores")]
+    lib = f"paper_2411_15659_b200/lib/ab/{k}.so"
+    Path(lib).parent.mkdir(parents=True, exist_ok=True)
+    subprocess.run([exe, *b.ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", lib, obj, *objs,
+                    "-lcudart_static", "-lrt", "-ldl", "-lpthread", "-Xlinker", "--no-undefined"], check=True)
+    print(k, "spills:", spill)

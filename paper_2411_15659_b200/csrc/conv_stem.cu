@@ -52,7 +52,14 @@ __global__ void __launch_bounds__(T, MINB) conv_stem_kernel(const StemParams p) 
     constexpr int PGC = (T / 32) * PGW;   // pixel groups per CTA
     constexpr int WIN = (PX - 1) * SW + KW;  // input columns one thread reads per row
     constexpr int CP = CPT / 2;
-    extern __shared__ __align__(16) float s_w[];  // [k][BN]
+    extern __shared__ __align__(16) float s_w[];  // [k][BN], columns permuted by wslot
+    // channel co_local = cg*CPT + 4*q4 + e lives at q4*(4*NG) + 4*cg + e, so
+    // one LDS.128 of a warp reads NG consecutive 16-byte chunks (no bank
+    // conflict between the channel groups)
+    auto wslot = [](int col) {
+        const int cg_ = col / CPT, r = col - cg_ * CPT;
+        return (r >> 2) * (4 * NG) + cg_ * 4 + (r & 3);
+    };
 
     const int tid = threadIdx.x;
     const int co_base = blockIdx.y * BN;
@@ -64,13 +71,13 @@ __global__ void __launch_bounds__(T, MINB) conv_stem_kernel(const StemParams p) 
             const int co = co_base + q * 4;
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
             if (co < p.co) v = __ldg(reinterpret_cast<const float4*>(p.w + (int64_t)kk * p.co + co));
-            *reinterpret_cast<float4*>(s_w + kk * BN + q * 4) = v;
+            *reinterpret_cast<float4*>(s_w + kk * BN + wslot(q * 4)) = v;
         }
     } else {
         for (int i = tid; i < p.k * BN; i += T) {
             const int kk = i / BN, q = i - kk * BN;
             const int co = co_base + q;
-            s_w[i] = co < p.co ? __ldg(p.w + (int64_t)kk * p.co + co) : 0.f;
+            s_w[kk * BN + wslot(q)] = co < p.co ? __ldg(p.w + (int64_t)kk * p.co + co) : 0.f;
         }
     }
     __syncthreads();
@@ -93,7 +100,7 @@ __global__ void __launch_bounds__(T, MINB) conv_stem_kernel(const StemParams p) 
         for (int q = 0; q < CP; ++q) acc[i][q] = 0ull;
 
     const float* xn = p.x + (int64_t)n * p.c_i * p.h * p.w_in;
-    const float* wcg = s_w + cg * CPT;
+    const float* wcg = s_w + cg * 4;
     // interior windows need no column predicate
     const bool cols_in = iw0 >= 0 && iw0 + WIN <= p.w_in;
     // one (c, kh) input row window; columns/rows in the zero padding read as 0
@@ -120,7 +127,8 @@ __global__ void __launch_bounds__(T, MINB) conv_stem_kernel(const StemParams p) 
             uint64_t wp[CP];
 #pragma unroll
             for (int q = 0; q < CP; q += 2) {
-                const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(wr + kw * KH * BN + q * 2);
+                const ulonglong2 v =
+                    *reinterpret_cast<const ulonglong2*>(wr + kw * KH * BN + (q >> 1) * (4 * NG));
                 wp[q] = v.x;
                 wp[q + 1] = v.y;
             }
@@ -212,9 +220,9 @@ cudaError_t launch_stem_t(StemParams sp, cudaStream_t s) {
 // threads, MINB CTAs/SM, PF pipelined windows), measured on B200
 // (tools/stem_ab*.sh); overridable at build time for A/B libraries.
 #ifndef SV1_PX
-#define SV1_PX 8
-#define SV1_CPT 8
-#define SV1_NG 8
+#define SV1_PX 4
+#define SV1_CPT 16
+#define SV1_NG 4
 #define SV1_T 128
 #define SV1_MINB 3
 #define SV1_PF false
@@ -237,17 +245,14 @@ cudaError_t launch_stem_t(StemParams sp, cudaStream_t s) {
 #endif
 
 // Layers with an instantiated stem kernel: c_i <= 4 with (KH, KW, SW) =
-// (7, 7, 2) or (11, 11, 4), the BASELINE config-3 stems.  (3x3 s1 c_i = 3 —
-// VGG conv1_1 — measured 448-487 us against 457 us for the tiled kernel;
-// STEM_K1 builds it for A/B.  DESIGN.md §3.1.)
+// (3, 3, 1), (7, 7, 2) or (11, 11, 4) — VGG conv1_1 and the config-3 stems.
+// (5x5 and c_i > 4 stay on the tiled kernel.  DESIGN.md §3.1.)
 int stem_kind(const smmc_geom& g) {
     const char* f = getenv("SMMC_STEM");  // A/B hook: 0 = tiled kernel
     if (f && atoi(f) == 0) return 0;
     if (g.c_i > kStemMaxCi) return 0;
     int kind = 0;
-#ifdef STEM_K1
     if (g.k_h == 3 && g.k_w == 3 && g.s_w == 1) kind = 1;
-#endif
     if (g.k_h == 7 && g.k_w == 7 && g.s_w == 2) kind = 2;
     else if (g.k_h == 11 && g.k_w == 11 && g.s_w == 4) kind = 3;
     if (!kind) return 0;
@@ -280,8 +285,10 @@ cudaError_t launch_stem(const Problem& p, int kind, cudaStream_t s) {
     cudaError_t e;
     switch (kind) {
         // measured on B200 (tools/stem_ab.sh, 20 launches back to back):
-        // 7x7 s2: 8 px x 8 c_o 56.9 us (4 px x 16 c_o 77 us); 11x11 s4:
-        // 4 px x 16 c_o pipelined 52.7 us (8 x 4 64.2, 2 x 32 54-58, tiled 71.8)
+        // 3x3 s1 (VGG conv1_1): 4 px x 16 c_o 381.6 us (8 x 8: 432-436,
+        // tiled 457); 7x7 s2: 8 px x 8 c_o pipelined 52.8 us (4 x 16: 55.2,
+        // tiled 59.5); 11x11 s4: 4 px x 16 c_o pipelined 52.5 us (4 x 8:
+        // 60.0, 8 x 4: 64.2, 2 x 32: 54-58, tiled 71.6)
         case 1: e = launch_stem_t<3, 3, 1, SV1_PX, SV1_CPT, SV1_NG, SV1_T, SV1_MINB, SV1_PF>(sp, s); break;
         case 2: e = launch_stem_t<7, 7, 2, SV2_PX, SV2_CPT, SV2_NG, SV2_T, SV2_MINB, SV2_PF>(sp, s); break;
         case 3: e = launch_stem_t<11, 11, 4, SV3_PX, SV3_CPT, SV3_NG, SV3_T, SV3_MINB, SV3_PF>(sp, s); break;

@@ -1,5 +1,6 @@
 """GPU parity of the direct stem kernel (csrc/conv_stem.cu): c_i <= 4 layers
-with 7x7 s2 and 11x11 s4 column strides — the BASELINE config-3 stems plus ragged geometries (odd widths, partial 8-column
+with 3x3 s1, 7x7 s2 and 11x11 s4 kernels — VGG conv1_1 and the BASELINE
+config-3 stems plus ragged geometries (odd widths, partial 8-column
 groups, c_o not a multiple of 4, unequal strides and pads, 1-row planes) —
 against the CPU oracle at the fp32 bar, deterministic, and against the tiled
 kernel it replaces (SMMC_STEM=0)."""
@@ -18,7 +19,11 @@ TOL_FP32 = 1e-4
 
 STEM_CASES = [
     # (c_i, c_o, h, w, kh, kw, sh, sw, ph, pw), n
+    ((3, 64, 224, 224, 3, 3, 1, 1, 1, 1), 1),      # VGG conv1_1 (config 4), one sample
     ((3, 64, 224, 224, 7, 7, 2, 2, 3, 3), 1),      # config 3 7x7 s2 stem
+    ((1, 5, 13, 17, 3, 3, 2, 1, 1, 1), 2),         # 3x3, s_h != s_w, c_o % 4 != 0
+    ((3, 16, 9, 9, 3, 3, 1, 1, 1, 1), 3),          # w' = 9: one full + one 1-column group
+    ((4, 130, 12, 30, 3, 3, 1, 1, 0, 1), 2),       # 3x3, three channel tiles, unequal pads
     ((3, 96, 227, 227, 11, 11, 4, 4, 0, 0), 2),    # config 3 11x11 s4 stem (w' = 55)
     ((3, 40, 47, 47, 11, 11, 4, 4, 0, 0), 3),      # c_o < tile, ragged
     ((1, 5, 13, 17, 7, 7, 2, 2, 3, 3), 2),         # c_o % 4 != 0, one channel
@@ -86,13 +91,13 @@ def test_stem_kernel_on_unaligned_input_and_host_entry():
 
 def test_random_stem_geometries():
     """80 random c_i <= 4 geometries over the stem kernel's tap kinds; other
-    c_i <= 4 kernels (3x3, 5x5) stay on the tiled kernel."""
+    c_i <= 4 kernels (5x5, ...) stay on the tiled kernel."""
     import torch
     rng = np.random.default_rng(31337)
-    kinds = [(7, 7, 2), (11, 11, 4)]
+    kinds = [(3, 3, 1), (7, 7, 2), (11, 11, 4)]
     checked = 0
     while checked < 80:
-        kh, kw, sw = kinds[int(rng.integers(0, 2))]
+        kh, kw, sw = kinds[int(rng.integers(0, 3))]
         ci = int(rng.integers(1, 5))
         co = int(rng.integers(1, 140))
         h, wd_ = int(rng.integers(1, 60)), int(rng.integers(1, 60))
@@ -112,6 +117,6 @@ def test_random_stem_geometries():
 
 
 def test_other_small_channel_layers_stay_on_the_tiled_kernel():
-    for gt in [(3, 64, 224, 224, 3, 3, 1, 1, 1, 1), (3, 16, 20, 20, 5, 5, 1, 1, 2, 2),
-               (5, 64, 40, 40, 7, 7, 2, 2, 3, 3)]:
+    for gt in [(3, 16, 20, 20, 5, 5, 1, 1, 2, 2), (5, 64, 40, 40, 7, 7, 2, 2, 3, 3),
+               (8, 64, 40, 40, 3, 3, 1, 1, 1, 1), (3, 16, 20, 20, 3, 3, 1, 2, 1, 1)]:
         assert "direct stem" not in _native.plan_describe(ConvGeometry(*gt), 2), gt

@@ -222,7 +222,7 @@ cudaError_t launch_stem_t(StemParams sp, cudaStream_t s) {
 #ifndef SV1_PX
 #define SV1_PX 4
 #define SV1_CPT 16
-#define SV1_NG 4
+#define SV1_NG 2
 #define SV1_T 128
 #define SV1_MINB 3
 #define SV1_PF false
@@ -266,6 +266,21 @@ int stem_bn(const smmc_geom& g, int kind) {
     return kind == 1 ? SV1_CPT * SV1_NG : kind == 2 ? SV2_CPT * SV2_NG : SV3_CPT * SV3_NG;
 }
 
+int stem_describe(int kind, char* buf, size_t len) {
+    int px, cpt, ng, t, minb;
+    bool pf;
+    switch (kind) {
+        case 1: px = SV1_PX, cpt = SV1_CPT, ng = SV1_NG, t = SV1_T, minb = SV1_MINB, pf = SV1_PF; break;
+        case 2: px = SV2_PX, cpt = SV2_CPT, ng = SV2_NG, t = SV2_T, minb = SV2_MINB, pf = SV2_PF; break;
+        case 3: px = SV3_PX, cpt = SV3_CPT, ng = SV3_NG, t = SV3_T, minb = SV3_MINB, pf = SV3_PF; break;
+        default: return -1;
+    }
+    return snprintf(buf, len,
+                    "ffma: direct stem kernel (weights in smem, register windows), %d px x %d c_o per "
+                    "thread, %d c_o per CTA, %d threads, %d CTAs/SM, %s windows, split_k=1 (reduce=none)",
+                    px, cpt, cpt * ng, t, minb, pf ? "pipelined" : "unpipelined");
+}
+
 cudaError_t launch_stem(const Problem& p, int kind, cudaStream_t s) {
     StemParams sp{};
     sp.x = p.x;
@@ -285,8 +300,8 @@ cudaError_t launch_stem(const Problem& p, int kind, cudaStream_t s) {
     cudaError_t e;
     switch (kind) {
         // measured on B200 (tools/stem_ab.sh, 20 launches back to back):
-        // 3x3 s1 (VGG conv1_1): 4 px x 16 c_o 381.6 us (8 x 8: 432-436,
-        // tiled 457); 7x7 s2: 8 px x 8 c_o pipelined 52.8 us (4 x 16: 55.2,
+        // 3x3 s1 (VGG conv1_1): 4 px x 16 c_o, 2 channel groups per warp
+        // 371.8 us (4 groups: 381.6, 8 x 8: 432-436, 2 x 32: 484, tiled 457); 7x7 s2: 8 px x 8 c_o pipelined 52.8 us (4 x 16: 55.2,
         // tiled 59.5); 11x11 s4: 4 px x 16 c_o pipelined 52.5 us (4 x 8:
         // 60.0, 8 x 4: 64.2, 2 x 32: 54-58, tiled 71.6)
         case 1: e = launch_stem_t<3, 3, 1, SV1_PX, SV1_CPT, SV1_NG, SV1_T, SV1_MINB, SV1_PF>(sp, s); break;

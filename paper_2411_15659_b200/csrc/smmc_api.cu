@@ -404,6 +404,10 @@ int smmc_plan_describe(const smmc_geom* g, int mode, char* buf, size_t len) {
         return SMMC_OK;
     }
     const FfmaPlan pl = plan_ffma(*g, sm_count_for(current_device()));
+    if (pl.stem) {
+        stem_describe(pl.stem, buf, len);
+        return SMMC_OK;
+    }
     snprintf(buf, len,
              "ffma: tile %dx%dx%d, %d threads, taps=%d, %s K order, split_k=%d (%d of %d tap blocks "
              "each, reduce=%s), %lld tiles",
@@ -418,10 +422,6 @@ int smmc_plan_describe(const smmc_geom* g, int mode, char* buf, size_t len) {
     if (pl.groups > 1) {
         const size_t used = strlen(buf);
         snprintf(buf + used, len - used, ", %d warp groups x %d threads", pl.groups, pl.threads);
-    }
-    if (pl.stem) {
-        const size_t used = strlen(buf);
-        snprintf(buf + used, len - used, ", direct stem kernel (weights in smem, register windows)");
     }
     if (pl.persist1x1) {
         const size_t used = strlen(buf);

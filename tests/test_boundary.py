@@ -132,3 +132,24 @@ def test_product_package_never_imports_the_oracle():
         text = src.read_text()
         for needle in ("import oracle", "from oracle", "smm_oracle", "liboracle"):
             assert needle not in text, (src, needle)
+
+
+def test_stem_plans_without_gpu():
+    """c_i <= 4 3x3 s1 / 7x7 s2 / 11x11 s4 layers plan the direct stem kernel
+    (one launch, no workspace); SMMC_STEM=0 and other kernels keep the tiled
+    kernel."""
+    import os
+    for gt in [(3, 64, 224, 224, 3, 3, 1, 1, 1, 1), (3, 64, 224, 224, 7, 7, 2, 2, 3, 3),
+               (3, 96, 227, 227, 11, 11, 4, 4, 0, 0), (1, 5, 13, 17, 3, 3, 2, 1, 1, 1)]:
+        g = ConvGeometry(*gt)
+        assert "direct stem" in _native.plan_describe(g, 8), gt
+        assert _native.plan_launches(g, 8, "ffma") == 1
+        assert _native.workspace_bytes(g, 8, "ffma") == 0
+    for gt in [(3, 16, 20, 20, 5, 5, 1, 1, 2, 2), (5, 64, 40, 40, 7, 7, 2, 2, 3, 3)]:
+        assert "direct stem" not in _native.plan_describe(ConvGeometry(*gt), 2), gt
+    g = ConvGeometry(3, 64, 224, 224, 7, 7, 2, 2, 3, 3)
+    os.environ["SMMC_STEM"] = "0"
+    try:
+        assert "direct stem" not in _native.plan_describe(g, 8)
+    finally:
+        del os.environ["SMMC_STEM"]

@@ -6,10 +6,8 @@ sys_path_fix = __import__("sys").path.insert(0, str(__import__("pathlib").Path(_
 from pathlib import Path
 from paper_2411_15659_b200 import build as b
 V = {
- "a9": ("SV3", (4,16,2,128,4,1)), "a10": ("SV3", (4,8,4,128,4,1)),
- "b1": ("SV2", (4,16,4,128,3,1)), "b4": ("SV2", (8,8,8,128,3,0)), "b5": ("SV2", (8,8,8,256,2,1)),
- "b6": ("SV2", (4,8,8,128,4,1)),
- "c1": ("SV1", (4,16,4,128,3,0)), "c2": ("SV1", (8,8,8,128,3,0)), "c4": ("SV1", (8,8,8,128,4,0)),
+ "d1": ("SV1", (4,16,4,128,4,0)), "d2": ("SV1", (4,16,4,256,2,0)), "d3": ("SV1", (4,16,2,128,3,0)),
+ "d4": ("SV1", (2,32,2,128,3,0)), "d5": ("SV1", (4,16,4,64,6,0)), "d6": ("SV1", (4,16,4,128,3,1)),
 }
 exe = b.nvcc()
 objs = [str(o) for o in sorted(Path("build/smmc").glob("*.o")) if o.stem != "conv_stem"]

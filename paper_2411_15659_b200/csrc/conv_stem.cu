@@ -45,8 +45,10 @@ struct StemParams {
 
 // T threads = (T/32) warps; a warp = (32/NG) pixel groups x NG channel groups.
 // PF: software-pipelined windows (row r+1 in flight while row r is consumed).
-template <int KH, int KW, int SW, int PX, int CPT, int NG, int T, int MINB, bool PF>
-__global__ void __launch_bounds__(T, MINB) conv_stem_kernel(const StemParams p) {
+// G > 1: G groups of T threads share a tile, group g over the g-th 1/G of
+// the (c, kh) rows; partial tiles summed in group order through shared memory.
+template <int KH, int KW, int SW, int PX, int CPT, int NG, int T, int MINB, bool PF, int G>
+__global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams p) {
     constexpr int BN = CPT * NG;
     constexpr int PGW = 32 / NG;          // pixel groups per warp
     constexpr int PGC = (T / 32) * PGW;   // pixel groups per CTA
@@ -61,12 +63,14 @@ __global__ void __launch_bounds__(T, MINB) conv_stem_kernel(const StemParams p) 
         return (r >> 2) * (4 * NG) + cg_ * 4 + (r & 3);
     };
 
-    const int tid = threadIdx.x;
+    const int tid_all = threadIdx.x;
+    const int grp = G > 1 ? tid_all / T : 0;
+    const int tid = tid_all - grp * T;
     const int co_base = blockIdx.y * BN;
     // the CTA's weight columns: rows of W_smm (c, j, k order), c_o innermost
     if ((p.co & 3) == 0) {
         constexpr int Q = BN / 4;
-        for (int i = tid; i < p.k * Q; i += T) {
+        for (int i = tid_all; i < p.k * Q; i += T * G) {
             const int kk = i / Q, q = i - kk * Q;
             const int co = co_base + q * 4;
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -74,7 +78,7 @@ __global__ void __launch_bounds__(T, MINB) conv_stem_kernel(const StemParams p) 
             *reinterpret_cast<float4*>(s_w + kk * BN + wslot(q * 4)) = v;
         }
     } else {
-        for (int i = tid; i < p.k * BN; i += T) {
+        for (int i = tid_all; i < p.k * BN; i += T * G) {
             const int kk = i / BN, q = i - kk * BN;
             const int co = co_base + q;
             s_w[kk * BN + wslot(q)] = co < p.co ? __ldg(p.w + (int64_t)kk * p.co + co) : 0.f;
@@ -84,8 +88,10 @@ __global__ void __launch_bounds__(T, MINB) conv_stem_kernel(const StemParams p) 
 
     const int lane = tid & 31;
     const int cg = lane % NG;
-    const int pg = blockIdx.x * PGC + (tid >> 5) * PGW + lane / NG;
-    if (pg >= p.pg_total) return;
+    const int pg_raw = blockIdx.x * PGC + (tid >> 5) * PGW + lane / NG;
+    const bool active = pg_raw < p.pg_total;
+    if (G == 1 && !active) return;
+    const int pg = active ? pg_raw : p.pg_total - 1;  // G > 1: stay for the barrier
     const int n = pg / p.ohgpr;
     const int rem = pg - n * p.ohgpr;
     const int orow = rem / p.gpr;
@@ -139,11 +145,13 @@ __global__ void __launch_bounds__(T, MINB) conv_stem_kernel(const StemParams p) 
                     acc[px][q] = ffma2_bcast(win[px * SW + kw], wp[q], acc[px][q]);
         }
     };
-    const int rows = p.c_i * KH;
+    const int rows_all = p.c_i * KH;
+    const int r_begin = grp * rows_all / G;
+    const int rows = (grp + 1) * rows_all / G;
     if (PF) {
         float wa[WIN], wb[WIN];
-        load_win(0, wa);
-        int r = 0;
+        int r = r_begin;
+        if (r < rows) load_win(r, wa);
 #pragma unroll 1
         for (; r + 2 <= rows; r += 2) {
             load_win(r + 1, wb);
@@ -154,14 +162,36 @@ __global__ void __launch_bounds__(T, MINB) conv_stem_kernel(const StemParams p) 
         if (r < rows) fma_row(r, wa);
     } else {
 #pragma unroll 1
-        for (int r = 0; r < rows; ++r) {
+        for (int r = r_begin; r < rows; ++r) {
             float win[WIN];
             load_win(r, win);
             fma_row(r, win);
         }
     }
 
-    // epilogue: NCHW, 8 consecutive columns per channel
+    if (G > 1) {
+        // groups 1..G-1 park their partial tiles; group 0 sums them in order
+        uint64_t* red = reinterpret_cast<uint64_t*>(s_w + p.k * BN);  // [G-1][PX*CP][T]
+        if (grp > 0) {
+#pragma unroll
+            for (int i = 0; i < PX; ++i)
+#pragma unroll
+                for (int q = 0; q < CP; ++q) red[((grp - 1) * PX * CP + i * CP + q) * T + tid] = acc[i][q];
+        }
+        __syncthreads();
+        if (grp > 0 || !active) return;
+#pragma unroll 1
+        for (int g = 1; g < G; ++g)
+#pragma unroll
+            for (int i = 0; i < PX; ++i)
+#pragma unroll
+                for (int q = 0; q < CP; ++q) {
+                    const float2 a = unpack2(acc[i][q]);
+                    const float2 b = unpack2(red[((g - 1) * PX * CP + i * CP + q) * T + tid]);
+                    acc[i][q] = pack2(a.x + b.x, a.y + b.y);
+                }
+    }
+    // epilogue: NCHW, PX consecutive columns per channel
     const int64_t ohw = (int64_t)p.oh * p.ow;
     const bool vec = PX % 4 == 0 && (p.ow & 3) == 0 && ow0 + PX <= p.ow;
     float* yrow = p.y + ((int64_t)n * p.co) * ohw + (int64_t)orow * p.ow + ow0;
@@ -192,25 +222,25 @@ __global__ void __launch_bounds__(T, MINB) conv_stem_kernel(const StemParams p) 
     }
 }
 
-template <int KH, int KW, int SW, int PX, int CPT, int NG, int T, int MINB, bool PF>
+template <int KH, int KW, int SW, int PX, int CPT, int NG, int T, int MINB, bool PF, int G>
 cudaError_t launch_stem_t(StemParams sp, cudaStream_t s) {
     sp.gpr = (sp.ow + PX - 1) / PX;
     sp.ohgpr = sp.oh * sp.gpr;
     sp.pg_total = sp.n * sp.ohgpr;
     constexpr int BN = CPT * NG;
     constexpr int PGC = (T / 32) * (32 / NG);
-    const size_t smem = (size_t)sp.k * BN * sizeof(float);
+    const size_t smem = (size_t)sp.k * BN * sizeof(float) + (size_t)(G - 1) * PX * (CPT / 2) * T * 8;
     if (smem > kStemMaxSmem) return cudaErrorInvalidConfiguration;
     static std::once_flag once;
     static cudaError_t attr = cudaSuccess;
-    auto kern = conv_stem_kernel<KH, KW, SW, PX, CPT, NG, T, MINB, PF>;
+    auto kern = conv_stem_kernel<KH, KW, SW, PX, CPT, NG, T, MINB, PF, G>;
     std::call_once(once, [&] {
         attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)kStemMaxSmem);
     });
     if (attr != cudaSuccess) return attr;
     dim3 grid((sp.pg_total + PGC - 1) / PGC, (sp.co + BN - 1) / BN);
-    kern<<<grid, T, smem, s>>>(sp);
+    kern<<<grid, T * G, smem, s>>>(sp);
     return cudaGetLastError();
 }
 
@@ -226,6 +256,7 @@ cudaError_t launch_stem_t(StemParams sp, cudaStream_t s) {
 #define SV1_T 128
 #define SV1_MINB 3
 #define SV1_PF false
+#define SV1_G 1
 #endif
 #ifndef SV2_PX
 #define SV2_PX 8
@@ -234,14 +265,16 @@ cudaError_t launch_stem_t(StemParams sp, cudaStream_t s) {
 #define SV2_T 128
 #define SV2_MINB 3
 #define SV2_PF true
+#define SV2_G 1
 #endif
 #ifndef SV3_PX
 #define SV3_PX 4
 #define SV3_CPT 16
 #define SV3_NG 2
 #define SV3_T 128
-#define SV3_MINB 3
-#define SV3_PF true
+#define SV3_MINB 2
+#define SV3_PF false
+#define SV3_G 2
 #endif
 
 // Layers with an instantiated stem kernel: c_i <= 4 with (KH, KW, SW) =
@@ -267,18 +300,19 @@ int stem_bn(const smmc_geom& g, int kind) {
 }
 
 int stem_describe(int kind, char* buf, size_t len) {
-    int px, cpt, ng, t, minb;
+    int px, cpt, ng, t, minb, g;
     bool pf;
     switch (kind) {
-        case 1: px = SV1_PX, cpt = SV1_CPT, ng = SV1_NG, t = SV1_T, minb = SV1_MINB, pf = SV1_PF; break;
-        case 2: px = SV2_PX, cpt = SV2_CPT, ng = SV2_NG, t = SV2_T, minb = SV2_MINB, pf = SV2_PF; break;
-        case 3: px = SV3_PX, cpt = SV3_CPT, ng = SV3_NG, t = SV3_T, minb = SV3_MINB, pf = SV3_PF; break;
+        case 1: px = SV1_PX, cpt = SV1_CPT, ng = SV1_NG, t = SV1_T, minb = SV1_MINB, pf = SV1_PF, g = SV1_G; break;
+        case 2: px = SV2_PX, cpt = SV2_CPT, ng = SV2_NG, t = SV2_T, minb = SV2_MINB, pf = SV2_PF, g = SV2_G; break;
+        case 3: px = SV3_PX, cpt = SV3_CPT, ng = SV3_NG, t = SV3_T, minb = SV3_MINB, pf = SV3_PF, g = SV3_G; break;
         default: return -1;
     }
     return snprintf(buf, len,
                     "ffma: direct stem kernel (weights in smem, register windows), %d px x %d c_o per "
-                    "thread, %d c_o per CTA, %d threads, %d CTAs/SM, %s windows, split_k=1 (reduce=none)",
-                    px, cpt, cpt * ng, t, minb, pf ? "pipelined" : "unpipelined");
+                    "thread, %d c_o per CTA, %d threads (%d row groups), %d CTAs/SM, %s windows, "
+                    "split_k=1 (reduce=none)",
+                    px, cpt, cpt * ng, t * g, g, minb, pf ? "pipelined" : "unpipelined");
 }
 
 cudaError_t launch_stem(const Problem& p, int kind, cudaStream_t s) {
@@ -302,11 +336,13 @@ cudaError_t launch_stem(const Problem& p, int kind, cudaStream_t s) {
         // measured on B200 (tools/stem_ab.sh, 20 launches back to back):
         // 3x3 s1 (VGG conv1_1): 4 px x 16 c_o, 2 channel groups per warp
         // 371.8 us (4 groups: 381.6, 8 x 8: 432-436, 2 x 32: 484, tiled 457); 7x7 s2: 8 px x 8 c_o pipelined 52.8 us (4 x 16: 55.2,
-        // tiled 59.5); 11x11 s4: 4 px x 16 c_o pipelined 52.5 us (4 x 8:
-        // 60.0, 8 x 4: 64.2, 2 x 32: 54-58, tiled 71.6)
-        case 1: e = launch_stem_t<3, 3, 1, SV1_PX, SV1_CPT, SV1_NG, SV1_T, SV1_MINB, SV1_PF>(sp, s); break;
-        case 2: e = launch_stem_t<7, 7, 2, SV2_PX, SV2_CPT, SV2_NG, SV2_T, SV2_MINB, SV2_PF>(sp, s); break;
-        case 3: e = launch_stem_t<11, 11, 4, SV3_PX, SV3_CPT, SV3_NG, SV3_T, SV3_MINB, SV3_PF>(sp, s); break;
+        // tiled 59.5; 2 row groups: 60-70); 11x11 s4: 4 px x 16 c_o, rows
+        // split over 2 groups of 128 threads 51.6 us (1 group pipelined
+        // 52.5-53.2, 3 groups 58-60, 4 x 8: 60.0, 8 x 4: 64.2, 2 x 32: 54-58,
+        // tiled 71.6)
+        case 1: e = launch_stem_t<3, 3, 1, SV1_PX, SV1_CPT, SV1_NG, SV1_T, SV1_MINB, SV1_PF, SV1_G>(sp, s); break;
+        case 2: e = launch_stem_t<7, 7, 2, SV2_PX, SV2_CPT, SV2_NG, SV2_T, SV2_MINB, SV2_PF, SV2_G>(sp, s); break;
+        case 3: e = launch_stem_t<11, 11, 4, SV3_PX, SV3_CPT, SV3_NG, SV3_T, SV3_MINB, SV3_PF, SV3_G>(sp, s); break;
         default: return cudaErrorInvalidConfiguration;
     }
     count_launches(1);

@@ -6,15 +6,16 @@ sys_path_fix = __import__("sys").path.insert(0, str(__import__("pathlib").Path(_
 from pathlib import Path
 from paper_2411_15659_b200 import build as b
 V = {
- "d1": ("SV1", (4,16,4,128,4,0)), "d2": ("SV1", (4,16,4,256,2,0)), "d3": ("SV1", (4,16,2,128,3,0)),
- "d4": ("SV1", (2,32,2,128,3,0)), "d5": ("SV1", (4,16,4,64,6,0)), "d6": ("SV1", (4,16,4,128,3,1)),
+ "e1": ("SV3", (4,16,2,128,1,1,3)), "e2": ("SV3", (4,16,2,128,2,0,2)), "e3": ("SV3", (4,16,2,128,1,0,3)),
+ "e4": ("SV3", (4,16,2,128,2,1,2)),
+ "f1": ("SV2", (8,8,8,128,1,1,2)), "f2": ("SV2", (8,8,8,128,2,0,2)),
 }
 exe = b.nvcc()
 objs = [str(o) for o in sorted(Path("build/smmc").glob("*.o")) if o.stem != "conv_stem"]
 procs = []
-for k, (pre, (px, cpt, ng, t, mb, pf)) in V.items():
+for k, (pre, (px, cpt, ng, t, mb, pf, *gg)) in V.items():
     d = [f"-D{pre}_PX={px}", f"-D{pre}_CPT={cpt}", f"-D{pre}_NG={ng}", f"-D{pre}_T={t}",
-         f"-D{pre}_MINB={mb}", f"-D{pre}_PF={'true' if pf else 'false'}"]
+         f"-D{pre}_MINB={mb}", f"-D{pre}_PF={'true' if pf else 'false'}", f"-D{pre}_G={gg[0] if gg else 1}"]
     if pre == "SV1": d.append("-DSTEM_K1=1")
     obj = f"/tmp/stem_{k}.o"
     cmd = [exe, *b.ARCH, *b.NVCC_FLAGS, *d, "-c", "paper_2411_15659_b200/csrc/conv_stem.cu", "-o", obj]

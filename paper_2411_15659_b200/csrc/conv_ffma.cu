@@ -1094,7 +1094,10 @@ cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
         count_launches(1);
     }
     cudaError_t e;
-    if (pl.stem && p.n_out == 1) return launch_stem(p, pl.stem, s);
+    if (pl.stem) {  // stem plans come from plan_ffma only (never the replicated-output gather)
+        if (p.n_out != 1) return cudaErrorInvalidConfiguration;
+        return launch_stem(p, pl.stem, s);
+    }
     if (pl.persist1x1 && p.n_out == 1 &&
         !(((uintptr_t)p.x | (uintptr_t)p.w | (uintptr_t)p.y) & 15)) {
         int dev = 0, sms = 148;

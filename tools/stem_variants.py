@@ -6,9 +6,9 @@ sys_path_fix = __import__("sys").path.insert(0, str(__import__("pathlib").Path(_
 from pathlib import Path
 from paper_2411_15659_b200 import build as b
 V = {
- "g1": ("SV2", (8,8,4,128,3,1,1)), "g2": ("SV2", (8,8,2,128,3,1,1)), "g3": ("SV2", (8,8,4,128,3,0,1)),
- "h1": ("SV3", (4,16,1,128,2,0,2)), "h2": ("SV3", (4,16,1,128,3,1,1)),
- "k1": ("SV1", (4,16,1,128,3,0,1)), "k2": ("SV1", (4,8,2,128,4,0,1)),
+ "m2a": ("SV2", (8,8,8,128,4,1,1)), "m2b": ("SV2", (8,8,8,256,2,1,1)),
+ "m1a": ("SV1", (4,16,2,128,4,0,1)), "m1b": ("SV1", (4,16,2,256,2,0,1)),
+ "m3a": ("SV3", (4,16,2,128,3,0,2)), "m3b": ("SV3", (4,16,2,128,2,1,2)),
 }
 exe = b.nvcc()
 objs = [str(o) for o in sorted(Path("build/smmc").glob("*.o")) if o.stem != "conv_stem"]

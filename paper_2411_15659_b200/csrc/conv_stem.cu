@@ -23,6 +23,7 @@
 // Accumulation order per output: c, kh, kw (fp32 FMA) — within the product
 // tolerance of the oracle (1e-4 * max|ref|, BASELINE north_star).
 #include <algorithm>
+#include <cstdint>
 #include <cstdlib>
 #include <mutex>
 
@@ -47,7 +48,10 @@ struct StemParams {
 // PF: software-pipelined windows (row r+1 in flight while row r is consumed).
 // G > 1: G groups of T threads share a tile, group g over the g-th 1/G of
 // the (c, kh) rows; partial tiles summed in group order through shared memory.
-template <int KH, int KW, int SW, int PX, int CPT, int NG, int T, int MINB, bool PF, int G>
+// VOFF >= 0: interior windows start VOFF floats past a 16-byte boundary
+// (fixed per launch: PX * SW % 4 == 0, w_in % 4 == 0), so they are read as
+// float4s (LDG.128) and sliced at compile-time offsets.
+template <int KH, int KW, int SW, int PX, int CPT, int NG, int T, int MINB, bool PF, int G, int VOFF>
 __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams p) {
     constexpr int BN = CPT * NG;
     constexpr int PGW = 32 / NG;          // pixel groups per warp
@@ -108,16 +112,26 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
     const float* xn = p.x + (int64_t)n * p.c_i * p.h * p.w_in;
     const float* wcg = s_w + cg * 4;
     // interior windows need no column predicate
-    const bool cols_in = iw0 >= 0 && iw0 + WIN <= p.w_in;
+    constexpr int NV = VOFF >= 0 ? (VOFF + WIN + 3) / 4 : 1;  // float4s per vector window
+    const bool cols_in = VOFF >= 0 ? iw0 - VOFF >= 0 && iw0 - VOFF + 4 * NV <= p.w_in
+                                   : iw0 >= 0 && iw0 + WIN <= p.w_in;
     // one (c, kh) input row window; columns/rows in the zero padding read as 0
     auto load_win = [&](int r, float (&win)[WIN]) {
         const int c = r / KH, kh = r - c * KH;
         const int ih = ih0 + kh;
         const bool row_in = (unsigned)ih < (unsigned)p.h;
         const float* xr = xn + ((int64_t)c * p.h + (row_in ? ih : 0)) * p.w_in + iw0;
-        if (row_in && cols_in) {
+        if (VOFF < 0 && row_in && cols_in) {
 #pragma unroll
             for (int t = 0; t < WIN; ++t) win[t] = __ldg(xr + t);
+        } else if (VOFF >= 0 && row_in && cols_in) {
+            float4 v[NV];
+            const float4* xv = reinterpret_cast<const float4*>(xr - (VOFF >= 0 ? VOFF : 0));
+#pragma unroll
+            for (int i = 0; i < NV; ++i) v[i] = __ldg(xv + i);
+            const float* vf = reinterpret_cast<const float*>(v);
+#pragma unroll
+            for (int t = 0; t < WIN; ++t) win[t] = vf[t + (VOFF >= 0 ? VOFF : 0)];
         } else {
 #pragma unroll
             for (int t = 0; t < WIN; ++t)
@@ -222,8 +236,14 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
     }
 }
 
-template <int KH, int KW, int SW, int PX, int CPT, int NG, int T, int MINB, bool PF, int G>
+template <int KH, int KW, int SW, int PX, int CPT, int NG, int T, int MINB, bool PF, int G, int VOFF = -1>
 cudaError_t launch_stem_t(StemParams sp, cudaStream_t s) {
+    if constexpr (VOFF >= 0) {  // vector windows: aligned rows and window starts only
+        static_assert((PX * SW) % 4 == 0, "window starts must step by whole float4s");
+        const bool ok = (sp.w_in & 3) == 0 && (reinterpret_cast<uintptr_t>(sp.x) & 15) == 0 &&
+                        ((-sp.pw) & 3) == VOFF && !getenv("SMMC_STEM_SCALAR");  // A/B hook
+        if (!ok) return launch_stem_t<KH, KW, SW, PX, CPT, NG, T, MINB, PF, G, -1>(sp, s);
+    }
     sp.gpr = (sp.ow + PX - 1) / PX;
     sp.ohgpr = sp.oh * sp.gpr;
     sp.pg_total = sp.n * sp.ohgpr;
@@ -233,7 +253,7 @@ cudaError_t launch_stem_t(StemParams sp, cudaStream_t s) {
     if (smem > kStemMaxSmem) return cudaErrorInvalidConfiguration;
     static std::once_flag once;
     static cudaError_t attr = cudaSuccess;
-    auto kern = conv_stem_kernel<KH, KW, SW, PX, CPT, NG, T, MINB, PF, G>;
+    auto kern = conv_stem_kernel<KH, KW, SW, PX, CPT, NG, T, MINB, PF, G, VOFF>;
     std::call_once(once, [&] {
         attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)kStemMaxSmem);
@@ -340,7 +360,9 @@ cudaError_t launch_stem(const Problem& p, int kind, cudaStream_t s) {
         // split over 2 groups of 128 threads 51.6 us (1 group pipelined
         // 52.5-53.2, 3 groups 58-60, 4 x 8: 60.0, 8 x 4: 64.2, 2 x 32: 54-58,
         // tiled 71.6)
-        case 1: e = launch_stem_t<3, 3, 1, SV1_PX, SV1_CPT, SV1_NG, SV1_T, SV1_MINB, SV1_PF, SV1_G>(sp, s); break;
+        // 3x3 s1 windows as float4s (w_in % 4 == 0): 370.0 -> 368.0 us; the
+        // 7x7 s2 stem measured slower with them (53.3 -> 56.0 us), scalar there
+        case 1: e = launch_stem_t<3, 3, 1, SV1_PX, SV1_CPT, SV1_NG, SV1_T, SV1_MINB, SV1_PF, SV1_G, 3>(sp, s); break;
         case 2: e = launch_stem_t<7, 7, 2, SV2_PX, SV2_CPT, SV2_NG, SV2_T, SV2_MINB, SV2_PF, SV2_G>(sp, s); break;
         case 3: e = launch_stem_t<11, 11, 4, SV3_PX, SV3_CPT, SV3_NG, SV3_T, SV3_MINB, SV3_PF, SV3_G>(sp, s); break;
         default: return cudaErrorInvalidConfiguration;

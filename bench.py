@@ -1,25 +1,31 @@
 #!/usr/bin/env python
-"""Benchmark of the SMM-Conv forward path on B200 (driver contract, see DESIGN.md §Measurement).
+"""Benchmark of the SMM-Conv forward path on B200 (driver contract, see DESIGN.md §5).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
 
-A *step* is one forward pass of every layer of BASELINE.json config C
-(default 2 = the ResNet-style 3x3 sweep, N in {1, 32}) over its synthetic
-batch.  Metric: conv GFLOP/s = sum of 2*N*c_o*h'*w'*c_i*k_h*k_w over the step's
-layers / step time.  Inputs are resident in HBM; three replicas of every
-layer's buffers are rotated so that > 2x L2 (126 MB) is touched between reuses
-of any buffer.  The K timed steps are captured once as a CUDA graph (with
-external event nodes between layers) and replayed once between a barrier +
-synchronize on both sides; time is the CUDA-event time, max over ranks.
+A *step* is one forward pass of every layer of BASELINE.json config C over its
+synthetic batch.  Default C: 4 (VGG-16 conv layers, N=64 -- the largest
+single-GPU config) at N=1 GPU, 5 (the multi-GPU scaling config) at N>1.
+Metric: conv GFLOP/s = sum of 2*N*c_o*h'*w'*c_i*k_h*k_w over the step's layers
+/ step time.  Inputs are resident in HBM; R replicas of every layer's buffers
+are rotated so that > 2x L2 (126 MB) is touched between reuses of any buffer.
+The K timed steps are captured once as a CUDA graph and replayed once between
+a barrier + synchronize on both sides; time is the CUDA-event time, max over
+ranks.
 
-Multi-GPU (torchrun): config 2/1/3/4 run weak-scaled (every rank runs the
-full config on its own samples, no collective).  Config 5 shards the N=256
-layers by batch (strong) and the 512@7 N=8 layer by output channel with an
-NCCL all-gather.
+Multi-GPU: ``--gpus N`` without torchrun re-launches this script under
+``torch.distributed.run`` with N ranks on 127.0.0.1; under torchrun the world
+size must equal ``--gpus``.  Config 5 shards the N=256 layers by batch
+(estimator.py:123-124 -- samples are independent, no collective) and the
+512@7 N=8 layer by output channel (the Algorithm-2 channel partition,
+smm.py:273-279) with a fused peer-write gather (or NCCL all-gather with
+``--gather nccl``).  Configs 1-4 run weak-scaled replicas.
 
-``--impl reference`` times the reference's CPU algorithm (the C restatement
-of smm_conv_parallel in oracle/, all host threads) on a bounded sample of the
-same workload; rank 0 only.
+``--impl reference`` times the reference's own CPU implementation -- the
+unmodified ``smmconv`` package installed under baseline/_ref, through its
+public ``Conv2D(backend="smm", threads=<all cores>)`` -- on one sample of every
+layer per step; rank 0 only.  When baseline/_ref is absent it falls back to
+the C restatement in oracle/ (kind "port").
 """
 
 import argparse
@@ -51,7 +57,8 @@ def parse_args():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--config", type=int, default=None, choices=sorted(CONFIGS),
+                    help="BASELINE.json config (default: 4 at --gpus 1, 5 at --gpus > 1)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="ffma", choices=["ffma", "exact", "bf16_tc", "bf16x3_tc"],
                     help="ffma: fp32 product kernel; exact: bitwise mode; bf16_tc: separately "
@@ -66,7 +73,12 @@ def parse_args():
                     help="c_o-sharded layer (config 5, N>1): fused peer-write epilogue "
                          "(smmc_conv2d_fwd_f32_gather over CUDA IPC) or NCCL all-gather + permute")
     ap.add_argument("--details", default="", help="write per-layer details JSON here")
-    return ap.parse_args()
+    ap.add_argument("--plan-only", action="store_true",
+                    help="no GPU work: every rank (gloo) reports its layer plan; rank 0 prints it")
+    args = ap.parse_args()
+    if args.config is None:
+        args.config = 4 if args.gpus <= 1 else 5
+    return args
 
 
 def peaks():
@@ -150,62 +162,213 @@ def dist_env():
     return rank, world, local
 
 
+def _free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch(args):
+    """--gpus N > 1 outside torchrun: run this script under
+    torch.distributed.run with N ranks on one node (127.0.0.1)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={_free_port()}", str(Path(__file__).resolve())] + sys.argv[1:]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
+
+
 def layer_plan(config, rank, world):
-    """Per-rank layers: (name, n_local, geom, seed, shard) — shard is
-    'replica' (weak), 'batch' (strong, N split) or 'cout' (c_o split)."""
+    """Per-rank layers: dicts (name, n, geom, seed, shard, c_lo, c_hi) -- shard
+    is 'replica' (weak: every rank its own samples), 'batch' (strong: samples
+    [N r/P, N (r+1)/P), estimator.py:123-124) or 'cout' (output channels
+    [c_o r/P, c_o (r+1)/P), the Algorithm-2 partition of smm.py:273-279)."""
+    from paper_2411_15659_b200.parallel import cout_shard
     out = []
     for li, (name, n, g) in enumerate(CONFIGS[config]["layers"]):
         seed = layer_seed(config, li)
+        lo, hi = 0, g.out_channels
         if config == 5 and world > 1:
             if "coshard" in name:
-                out.append((name, n, g, seed, "cout"))
+                lo, hi = cout_shard(g.out_channels, rank, world)
+                shard, nl = "cout", n
             else:
-                lo, hi = n * rank // world, n * (rank + 1) // world
-                out.append((name, hi - lo, g, seed + 100003 * rank, "batch"))
+                b0, b1 = n * rank // world, n * (rank + 1) // world
+                shard, nl, seed = "batch", b1 - b0, seed + 100003 * rank
         else:
-            out.append((name, n, g, seed + 100003 * rank, "replica"))
+            shard, nl, seed = "replica", n, seed + 100003 * rank
+        out.append(dict(name=name, n=nl, g=g, seed=seed, shard=shard, c_lo=lo, c_hi=hi))
     return out
 
 
+def step_bytes_of(plan):
+    b = 0
+    for p in plan:
+        g, nc = p["g"], p["c_hi"] - p["c_lo"]
+        b += 4 * (p["n"] * g.in_channels * g.in_h * g.in_w + nc * g.in_channels * g.k_h * g.k_w
+                  + p["n"] * nc * g.out_h * g.out_w)
+    return b
+
+
+def replicas_for(args, plan):
+    sb = step_bytes_of(plan)
+    return args.replicas or max(1, min(8, -(-3 * L2_BYTES // max(sb, 1)) + 1))
+
+
+def workload_config(args, world):
+    """The `config` dict of the JSON line -- identical in both arms."""
+    plan = layer_plan(args.config, 0, world)
+    R = replicas_for(args, plan)
+    sb = step_bytes_of(plan)
+    par = {"replica": f"dp{world}" if world > 1 else "single",
+           "batch": f"batch-shard{world}", "cout": f"cout-shard{world}"}
+    return {"workload": f"BASELINE config {args.config}: {CONFIGS[args.config]['title']}",
+            "layers": [p["name"] for p in plan],
+            "batch": [n for _, n, _ in CONFIGS[args.config]["layers"]],
+            "parallelism": "+".join(par[s] for s in sorted({p["shard"] for p in plan})),
+            "l2": (f"{R} rotating replicas of every GPU buffer ({R * sb / 2**20:.0f} MiB > 2x L2 "
+                   "between reuses)" if R > 1 else "GPU inputs larger than L2")}
+
+
+def plan_only(args):
+    """Multi-rank plan check without a GPU (gloo): each rank derives its own
+    plan, rank 0 prints all of them."""
+    import torch.distributed as dist
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    mine = [{k: (v if k != "g" else list(v.as_abi(1))) for k, v in p.items()}
+            for p in layer_plan(args.config, rank, world)]
+    allp = [None] * world
+    if world > 1:
+        dist.all_gather_object(allp, {"rank": rank, "plan": mine})
+    else:
+        allp = [{"rank": 0, "plan": mine}]
+    if rank == 0:
+        print(json.dumps({"plan_only": True, "n_gpus": world, "config": workload_config(args, world),
+                          "ranks": allp}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def cpu_model():
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 # --------------------------------------------------------------------- reference arm
+def reference_package():
+    """The unmodified reference package from baseline/_ref (pip-installed
+    there from /root/reference/pkg, git-ignored, travels to the GPU box), or
+    None when it is absent or cannot be imported (numba missing)."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "smmconv" / "__init__.py").exists():
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/smmc_numba_cache")
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        import smmconv
+    except Exception:  # noqa: BLE001 -- e.g. numba absent: the port stands in
+        return None
+    return smmconv
+
+
+class ReferenceSample:
+    """One sample of every layer through the reference's public API:
+    ``smmconv.Conv2D(backend="smm", threads=cores).fit(x).transform(x)``
+    (estimator.py:50-125; fit repacks the weights, untimed like runner.py:120-121),
+    or -- without baseline/_ref -- the C restatement of smm_conv_parallel."""
+
+    def __init__(self, plan, cores, data=None, use_reference=True):
+        self.pkg = reference_package() if use_reference else None
+        self.cores = cores
+        self.items = []
+        self.flops = 0
+        for i, p in enumerate(plan):
+            g = p["g"]
+            if data is not None:  # (x[:1], OIHW weights of this rank's channels)
+                x, w = data[i]
+            else:
+                x, w = synthetic_layer(g, 1, p["seed"])
+                if p["c_hi"] - p["c_lo"] != g.out_channels:
+                    w = np.ascontiguousarray(w[p["c_lo"]:p["c_hi"]])
+            nc = w.shape[0]
+            if self.pkg is not None:
+                m = self.pkg.Conv2D(out_channels=nc, kernel_size=(g.k_h, g.k_w),
+                                    stride=(g.stride_h, g.stride_w), padding=(g.pad_h, g.pad_w),
+                                    backend="smm", threads=cores, weights=w)
+                m.fit(x)
+                self.items.append((m, x, None))
+            else:
+                from paper_2411_15659_b200 import ConvGeometry, repack_weights
+                gg = ConvGeometry(g.in_channels, nc, g.in_h, g.in_w, g.k_h, g.k_w,
+                                  g.stride_h, g.stride_w, g.pad_h, g.pad_w)
+                self.items.append((gg, x, repack_weights(w, gg)))
+            self.flops += 2 * nc * g.out_h * g.out_w * g.in_channels * g.k_h * g.k_w
+        if self.pkg is not None:
+            # numba compiles on the first call (cached under NUMBA_CACHE_DIR)
+            tiny = self.pkg.Conv2D(out_channels=2, kernel_size=3, padding=1, backend="smm",
+                                   threads=2).fit(np.zeros((1, 2, 5, 5), np.float32))
+            tiny.transform(np.zeros((1, 2, 5, 5), np.float32))
+
+    @property
+    def kind(self):
+        return "reference" if self.pkg is not None else "port"
+
+    def describe(self):
+        if self.pkg is not None:
+            return ("unmodified reference smmconv (baseline/_ref) Conv2D(backend='smm', "
+                    f"threads={self.cores}).transform -> smm_conv_parallel (numba, Algorithm 2)")
+        return ("oracle/smm_oracle.c: C restatement of smm_conv_parallel (Algorithm 2, "
+                "smm.py:254-306), bitwise-pinned to the reference")
+
+    def run(self):
+        outs = []
+        if self.pkg is not None:
+            for m, x, _ in self.items:
+                outs.append(m.transform(x)[0])
+        else:
+            from oracle import smm_oracle as orc
+            for gg, x, ws in self.items:
+                outs.append(orc.smm_conv_c(x[0], ws, gg, threads=self.cores))
+        return outs
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    from oracle import smm_oracle as orc
-    from paper_2411_15659_b200 import repack_weights
-    threads = orc.host_threads()
-    layers = CONFIGS[args.config]["layers"]
-    samples = []
-    for li, (name, n, g) in enumerate(layers):
-        x, w = synthetic_layer(g, 1, layer_seed(args.config, li))
-        samples.append((g, np.ascontiguousarray(x[0]), repack_weights(w, g)))
-    flops_per_step = sum(g.flops(1) for g, _, _ in samples)
-
-    def step():
-        for g, x, ws in samples:
-            orc.smm_conv_c(x, ws, g, threads=threads)
-
+    cores = os.cpu_count() or 1
+    plan = layer_plan(args.config, 0, world)
+    ref = ReferenceSample(plan, cores)
     for _ in range(args.warmup):
-        step()
+        ref.run()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        step()
+        ref.run()
     dt = time.perf_counter() - t0
-    value = flops_per_step * args.steps / dt / 1e9
-    sample = (f"1 sample of each of the {len(layers)} config-{args.config} layers per step "
-              f"(the reference loops samples sequentially, estimator.py:123-124)")
+    value = ref.flops * args.steps / dt / 1e9
+    sample = (f"1 sample of each of the {len(plan)} config-{args.config} layers (rank-0 shard) "
+              "per step; the reference loops samples sequentially (estimator.py:123-124)")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"BASELINE config {args.config}: {CONFIGS[args.config]['title']}",
-                   "layers": [nm for nm, _, _ in layers], "parallelism": "cpu threads"},
-        "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": threads,
-                         "kind": "port", "sample": sample,
-                         "impl": "oracle/smm_oracle.c: C restatement of smm_conv_parallel "
-                                 "(Algorithm 2, smm.py:254-306), bitwise-pinned to the reference"},
+        "scaling": "strong" if (args.config == 5 and world > 1) else "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": workload_config(args, world),
+        "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": cores,
+                         "cpu_model": cpu_model(), "kind": ref.kind, "sample": sample,
+                         "impl": ref.describe()},
         "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -218,8 +381,8 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2411_15659_b200 import _native, device
-    from paper_2411_15659_b200.parallel import all_gather_cout, cout_shard
+    from paper_2411_15659_b200 import ConvGeometry, _native, device
+    from paper_2411_15659_b200.parallel import all_gather_cout
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -230,22 +393,21 @@ def run_ours(args):
 
     # ---- data: synthetic host arrays -> HBM, R replicas
     layers = []
-    for name, n, g, seed, shard in plan:
-        x, w = synthetic_layer(g, n, seed)
+    for p in plan:
+        g = p["g"]
+        x, w = synthetic_layer(g, p["n"], p["seed"])
         ws = np.ascontiguousarray(w.transpose(1, 3, 2, 0))
-        c_lo, c_hi = 0, g.out_channels
+        c_lo, c_hi = p["c_lo"], p["c_hi"]
         gg = g
-        if shard == "cout":
-            c_lo, c_hi = cout_shard(g.out_channels, rank, world)
+        if p["shard"] == "cout":
             ws = np.ascontiguousarray(ws[..., c_lo:c_hi])
-            from paper_2411_15659_b200 import ConvGeometry
             gg = ConvGeometry(g.in_channels, c_hi - c_lo, g.in_h, g.in_w, g.k_h, g.k_w,
                               g.stride_h, g.stride_w, g.pad_h, g.pad_w)
-        layers.append(dict(name=name, n=n, g=g, gl=gg, shard=shard, x_host=x, w_host=ws,
-                           flops=gg.flops(n), c_range=(c_lo, c_hi)))
-    step_bytes = sum(4 * (L["x_host"].size + L["w_host"].size + L["n"] * L["gl"].out_channels
-                          * L["gl"].out_h * L["gl"].out_w) for L in layers)
-    R = args.replicas or max(1, min(8, -(-3 * L2_BYTES // max(step_bytes, 1)) + 1))
+        layers.append(dict(name=p["name"], n=p["n"], g=g, gl=gg, shard=p["shard"], x_host=x,
+                           w_host=ws, flops=gg.flops(p["n"]), c_range=(c_lo, c_hi)))
+    step_bytes = step_bytes_of(plan)
+    R = replicas_for(args, plan)
+    gather_path = None
     tc = args.mode == "bf16_tc"
     tc3 = args.mode == "bf16x3_tc"
     if tc or tc3:
@@ -282,14 +444,31 @@ def run_ours(args):
         L["ws"] = torch.empty(max(need, 16), dtype=torch.uint8, device=dev)
         if L["shard"] == "cout":
             L["full"] = torch.empty((L["n"],) + L["g"].output_shape, device=dev)
+            peers = None
             if world > 1 and args.gather == "fused" and not tc and args.mode == "ffma":
+                from paper_2411_15659_b200.errors import SmmConvError
                 from paper_2411_15659_b200.parallel import PeerBuffers
-                L["peers"] = PeerBuffers(L["full"])
+                try:
+                    peers = PeerBuffers(L["full"])
+                    ok = 1.0
+                except SmmConvError as e:  # IPC refused: every rank falls back together
+                    print(f"[rank {rank}] CUDA IPC unavailable ({e}); NCCL all-gather", file=sys.stderr)
+                    ok = 0.0
+                t_ok = torch.tensor([ok], device=dev)
+                dist.all_reduce(t_ok, op=dist.ReduceOp.MIN)
+                if t_ok.item() < 1.0:
+                    if peers is not None:
+                        peers.close()
+                    peers = None
+            if peers is not None:
+                L["peers"] = peers
                 L["flag"] = torch.zeros(1, device=dev)
                 L["ws"] = torch.empty(max(_native.gather_workspace_bytes(L["gl"], L["n"]), 16),
                                       dtype=torch.uint8, device=dev)
+                gather_path = "fused peer-write (CUDA IPC over NVLink)"
             else:
                 L["gather"] = torch.empty((world,) + shape, device=dev)
+                gather_path = "NCCL all_gather_into_tensor + permute"
 
     def run_layer(L, r):
         if "peers" in L:  # fused c_o-shard gather: fence, peer-write conv, fence
@@ -499,12 +678,9 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args, layers)
+        cpu = cpu_baseline(args, plan, layers)
 
     if rank == 0:
-        par = {"replica": f"dp{world}" if world > 1 else "single",
-               "batch": f"batch-shard{world}", "cout": f"cout-shard{world}"}
-        shards = sorted({L["shard"] for L in layers})
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
@@ -513,17 +689,12 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": ("bf16-in/f32-acc" if tc else "f32 (split bf16x3, f32 acc)" if tc3 else "f32"),
             "data": "synthetic",
-            "config": {"workload": f"BASELINE config {args.config}: {CONFIGS[args.config]['title']}",
-                       "layers": [L["name"] for L in layers],
-                       "mode": args.mode,
-                       "parallelism": "+".join(par[s] for s in shards),
-                       "l2": f"{R} rotating replicas of every buffer "
-                             f"({R * step_bytes / 2**20:.0f} MiB > 2x L2 between reuses)"
-                             if R > 1 else "inputs larger than L2",
-                       "timing": "K steps captured as one CUDA graph (no other nodes), "
-                                 "replayed once between CUDA events; max over ranks; per-layer "
-                                 "times from a second replay of the same steps with an event "
-                                 "after every layer"},
+            "config": workload_config(args, world),
+            "mode": args.mode,
+            "gather_path": gather_path,
+            "timing": "K steps captured as one CUDA graph (no other nodes), replayed once between "
+                      "CUDA events; max over ranks; per-layer times from a second replay of the "
+                      "same steps with an event after every layer",
             "gpu_launches": gpu_launches,
             "clocks": clk,
             "roofline": roofline,
@@ -691,41 +862,60 @@ def run_e2e_tc(args, layers, world, dev):
                     "host input/output, wall clock, max over ranks"}
 
 
-def cpu_baseline(args, layers):
-    """The reference's CPU algorithm (C restatement of smm_conv_parallel,
-    all host threads) on one sample of each layer, repeated for ~10 s; also
-    cross-checks our GPU output of sample 0 against it."""
+def cpu_baseline(args, plan, layers):
+    """The reference's CPU path on the box's host cores, on sample 0 of every
+    layer of this workload, repeated for ~--cpu-seconds: the unmodified
+    reference package (baseline/_ref, numba) and, beside it, the C
+    restatement in oracle/ (the port is 1.25-6x faster than the reference).
+    Also cross-checks our GPU output of sample 0 against the CPU result."""
     import torch
 
-    from oracle import smm_oracle as orc
-    threads = orc.host_threads()
-    flops = 0
+    cores = os.cpu_count() or 1
+    data = [(np.ascontiguousarray(L["x_host"][:1]),
+             np.ascontiguousarray(L["w_host"].transpose(3, 0, 2, 1))) for L in layers]
+    out = {}
     worst = 0.0
-    t0 = time.perf_counter()
-    reps = 0
-    while True:
-        for L in layers:
-            if L["n"] == 0:
-                continue
-            ref = orc.smm_conv_c(L["x_host"][0], L["w_host"], L["gl"], threads=threads)
-            flops += L["gl"].flops(1)
+    legs = [("reference", True), ("port", False)]
+    for key, use_ref in legs:
+        ref = ReferenceSample(plan, cores, data=data, use_reference=use_ref)
+        if key == "reference" and ref.kind != "reference":
+            continue
+        budget = args.cpu_seconds if key == "reference" else args.cpu_seconds / 2
+        reps, t0 = 0, time.perf_counter()
+        while True:
+            ys = ref.run()
             if reps == 0:
-                yd = L["y"][0][0].cpu().numpy()
-                worst = max(worst, orc.max_abs_ratio(yd, ref))
-        reps += 1
-        if time.perf_counter() - t0 >= args.cpu_seconds:
-            break
-    dt = time.perf_counter() - t0
+                from oracle import smm_oracle as orc
+                for L, y in zip(layers, ys):
+                    if L["n"]:
+                        worst = max(worst, orc.max_abs_ratio(L["y"][0][0].cpu().numpy(), y))
+            reps += 1
+            if time.perf_counter() - t0 >= budget:
+                break
+        dt = time.perf_counter() - t0
+        out[key] = {"value": round(ref.flops * reps / dt / 1e9, 3), "unit": "GFLOP/s",
+                    "cores": cores, "kind": ref.kind, "impl": ref.describe(),
+                    "sample": f"sample 0 of each of the {len(layers)} layers, {reps} passes "
+                              f"({dt:.1f} s)"}
     torch.cuda.synchronize()
-    return {"value": round(flops / dt / 1e9, 3), "unit": "GFLOP/s", "cores": threads,
-            "kind": "port",
-            "sample": f"sample 0 of each of the {len(layers)} layers, {reps} passes "
-                      f"({dt:.1f} s), C restatement of smm_conv_parallel (Algorithm 2)",
-            "gpu_vs_oracle_max_err_ratio": worst}
+    head = dict(out.get("reference") or out["port"])
+    head["cpu_model"] = cpu_model()
+    head["gpu_vs_cpu_max_err_ratio"] = worst
+    if "reference" in out:
+        head["port"] = out["port"]
+    return head
 
 
 def main():
     args = parse_args()
+    _, world, _ = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return relaunch(args)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch with "
+                         f"--nproc-per-node {args.gpus} or drop torchrun")
+    if args.plan_only:
+        return plan_only(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -194,12 +194,8 @@ __global__ void __launch_bounds__(THREADS, MINB) conv1x1_persistent_kernel(const
 template <int BM, int BN, int T, int MINB>
 cudaError_t launch_1x1(const Problem& p, int sm_count, cudaStream_t s) {
     constexpr int smem = kRing * kBK * (BM + BN) * (int)sizeof(float);
-    static std::once_flag once;
-    static cudaError_t attr = cudaSuccess;
     auto kern = conv1x1_persistent_kernel<BM, BN, T, MINB>;
-    std::call_once(once, [&] {
-        attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    });
+    const cudaError_t attr = smem_optin(kern, smem);
     if (attr != cudaSuccess) return attr;
     const int grid = (int)std::min<int64_t>(p.tiles, (int64_t)sm_count * MINB);
     kern<<<grid, T, smem, s>>>(p);

@@ -737,12 +737,8 @@ cudaError_t launch_one(const Problem& p, dim3 grid, cudaStream_t s) {
     constexpr int ring = G * kStages * BK * (BM + BN) * (int)sizeof(float);
     constexpr int part = BN * (BM + 4) * (int)sizeof(float);  // reduce_mode 4 partial tile
     constexpr int smem_max = ring > part ? ring : part;
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
     auto kern = conv_ffma_kernel<BM, BN, T, MINB, TM, BK, KH, KW, SH, SW, CVEC, SK, G>;
-    std::call_once(once, [&] {
-        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
-    });
+    const cudaError_t attr_err = smem_optin(kern, smem_max);
     if (attr_err != cudaSuccess) return attr_err;
     if (!SK && p.reduce_mode == 4) {  // the S splits of a tile form one cluster
         cudaLaunchConfig_t cfg{};

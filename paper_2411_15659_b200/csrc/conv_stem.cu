@@ -251,13 +251,8 @@ cudaError_t launch_stem_t(StemParams sp, cudaStream_t s) {
     constexpr int PGC = (T / 32) * (32 / NG);
     const size_t smem = (size_t)sp.k * BN * sizeof(float) + (size_t)(G - 1) * PX * (CPT / 2) * T * 8;
     if (smem > kStemMaxSmem) return cudaErrorInvalidConfiguration;
-    static std::once_flag once;
-    static cudaError_t attr = cudaSuccess;
     auto kern = conv_stem_kernel<KH, KW, SW, PX, CPT, NG, T, MINB, PF, G, VOFF>;
-    std::call_once(once, [&] {
-        attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)kStemMaxSmem);
-    });
+    const cudaError_t attr = smem_optin(kern, (int)kStemMaxSmem);
     if (attr != cudaSuccess) return attr;
     dim3 grid((sp.pg_total + PGC - 1) / PGC, (sp.co + BN - 1) / BN);
     kern<<<grid, T * G, smem, s>>>(sp);

@@ -798,18 +798,13 @@ cudaError_t launch_tc_bf16(const uint16_t* x_pad, const uint16_t* w_tc, float* y
         }
         if (pl.persistent) {
             constexpr int kPersistSmem = 227 * 1024 - 4096;
-            static std::once_flag once2;
-            static cudaError_t attr2 = cudaSuccess;
-            std::call_once(once2, [] {
-                const void* fns[3] = {(const void*)conv_tc_halo_persistent_kernel<256, 1>,
-                                      (const void*)conv_tc_halo_persistent_kernel<128, 1>,
-                                      (const void*)conv_tc_halo_persistent_kernel<128, 2>};
-                for (const void* f : fns)
-                    if (attr2 == cudaSuccess)
-                        attr2 = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                     kPersistSmem);
-            });
-            if (attr2 != cudaSuccess) return attr2;
+            const void* fns[3] = {(const void*)conv_tc_halo_persistent_kernel<256, 1>,
+                                  (const void*)conv_tc_halo_persistent_kernel<128, 1>,
+                                  (const void*)conv_tc_halo_persistent_kernel<128, 2>};
+            for (const void* f : fns) {
+                const cudaError_t attr2 = smem_optin(f, kPersistSmem);
+                if (attr2 != cudaSuccess) return attr2;
+            }
             const int mt = pl.mt;
             p.b_stages = std::min(PH_B_MAX, (kPersistSmem - 1024 - HALO_A_STAGES * mt * p.halo_stage_bytes) /
                                                 (int)p.tx_b);
@@ -838,12 +833,7 @@ cudaError_t launch_tc_bf16(const uint16_t* x_pad, const uint16_t* w_tc, float* y
             }
         } else {
             const int smem = HALO_A_STAGES * p.halo_stage_bytes + HALO_B_STAGES * (int)p.tx_b + 1024;
-            static std::once_flag once;
-            static cudaError_t attr = cudaSuccess;
-            std::call_once(once, [] {
-                attr = cudaFuncSetAttribute(conv_tc_halo_kernel<128>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, HALO_SMEM_MAX);
-            });
+            const cudaError_t attr = smem_optin(conv_tc_halo_kernel<128>, HALO_SMEM_MAX);
             if (attr != cudaSuccess) return attr;
             dim3 grid((unsigned)pl.tiles_m, (unsigned)pl.tiles_n);
             conv_tc_halo_kernel<128><<<grid, TC_THREADS, smem, s>>>(tm_a, tm_b, p);
@@ -864,12 +854,7 @@ cudaError_t launch_tc_bf16(const uint16_t* x_pad, const uint16_t* w_tc, float* y
             return cudaErrorInvalidValue;
         }
         p.tx_a = (uint32_t)(pl.tw * pl.th * pl.nb) * TC_BK * 2;
-        static std::once_flag once;
-        static cudaError_t attr = cudaSuccess;
-        std::call_once(once, [] {
-            attr = cudaFuncSetAttribute(conv_tc_box_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, BOX_SMEM);
-        });
+        const cudaError_t attr = smem_optin(conv_tc_box_kernel, BOX_SMEM);
         if (attr != cudaSuccess) return attr;
         dim3 grid((unsigned)pl.tiles_m, (unsigned)pl.tiles_n);
         conv_tc_box_kernel<<<grid, TC_THREADS, BOX_SMEM, s>>>(tm_a, tm_b, p);

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -32,6 +33,21 @@ void set_error(const char* fmt, ...) {
 }
 
 void count_launches(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+cudaError_t smem_optin(const void* fn, int bytes) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, int> done;  // (kernel, device) -> bytes set
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_pair(fn, dev);
+    auto it = done.find(key);
+    if (it != done.end() && it->second >= bytes) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done[key] = bytes;
+    return e;
+}
 
 namespace {
 
@@ -197,6 +213,37 @@ int ensure(HostPool& hp, int i, size_t bytes) {
     // split-K counters must start at zero (kernels leave them zeroed)
     return cuda_status(cudaMemset(hp.buf[i], 0, bytes), "cudaMemset(staging)");
 }
+
+// Restores the caller's current device on every return path of a host entry.
+struct DeviceGuard {
+    int prev = -1;
+    DeviceGuard() {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// On any early return after work was enqueued on a pool's streams, drain
+// them before the pool lock is released: in-flight copies may still read
+// the caller's host input / write its host output and the pool buffers.
+// Declared after the pool's lock_guard so it runs first.
+struct PoolDrain {
+    HostPool& hp;
+    bool done = false;
+    explicit PoolDrain(HostPool& h) : hp(h) {}
+    int finish(int st) {
+        done = true;
+        return st;
+    }
+    ~PoolDrain() {
+        if (done) return;
+        if (hp.s_in) cudaStreamSynchronize(hp.s_in);
+        if (hp.stream) cudaStreamSynchronize(hp.stream);
+        if (hp.s_out) cudaStreamSynchronize(hp.s_out);
+    }
+};
 
 int select_device(int device) {
     int count = 0;
@@ -540,9 +587,11 @@ int host_pipeline(const float* x, const float* w_smm, const float* w_dev, float*
         set_error("x, w_smm and y must be non-NULL host pointers");
         return SMMC_ESHAPE;
     }
+    DeviceGuard dg;
     if ((st = select_device(device))) return st;
     HostPool& hp = acquire_pool(device);
     std::lock_guard<std::mutex> lk(hp.mu, std::adopt_lock);
+    PoolDrain drain(hp);
     if ((st = ensure_streams(hp))) return st;
     const size_t xs = (size_t)g->c_i * g->h * g->w;          // floats per input sample
     const size_t ys = (size_t)g->c_o * oh * ow;              // floats per output sample
@@ -604,7 +653,7 @@ int host_pipeline(const float* x, const float* w_smm, const float* w_dev, float*
                               "D2H y")))
             return st;
     }
-    return cuda_status(cudaStreamSynchronize(hp.s_out), "conv (host path)");
+    return drain.finish(cuda_status(cudaStreamSynchronize(hp.s_out), "conv (host path)"));
 }
 }  // namespace
 }  // namespace smmc
@@ -640,6 +689,7 @@ int smmc_layer_create(const float* w_smm, const smmc_geom* g, int device, smmc_l
         set_error("w_smm must be a non-NULL host pointer");
         return SMMC_ESHAPE;
     }
+    DeviceGuard dg;
     if ((st = select_device(device))) return st;
     const size_t wb = (size_t)gg.c_i * gg.k_w * gg.k_h * gg.c_o * sizeof(float);
     smmc_layer* L = new smmc_layer{gg, device, nullptr};
@@ -929,9 +979,11 @@ int smmc_extract_slice_f32_host(const float* x, const smmc_geom* g, int32_t c, i
         set_error("slice index (c=%d, j=%d) out of range", c, j);
         return SMMC_EINDEX;
     }
+    DeviceGuard dg;
     if ((st = select_device(device))) return st;
     HostPool& hp = acquire_pool(device);
     std::lock_guard<std::mutex> lk(hp.mu, std::adopt_lock);
+    PoolDrain drain(hp);
     if ((st = ensure_streams(hp))) return st;
     const size_t xb = (size_t)g->c_i * g->h * g->w * sizeof(float);
     const size_t bb = (size_t)(g->h + 2 * g->p_h) * ow * sizeof(float);
@@ -944,7 +996,7 @@ int smmc_extract_slice_f32_host(const float* x, const smmc_geom* g, int32_t c, i
         return st;
     if ((st = cuda_status(cudaMemcpyAsync(buf, hp.buf[2], bb, cudaMemcpyDeviceToHost, s), "D2H")))
         return st;
-    return cuda_status(cudaStreamSynchronize(s), "extract_slice (host path)");
+    return drain.finish(cuda_status(cudaStreamSynchronize(s), "extract_slice (host path)"));
 }
 
 int smmc_scalar_matrix_fma_f32_host(float alpha, const float* src, int64_t src_row_stride,
@@ -956,10 +1008,12 @@ int smmc_scalar_matrix_fma_f32_host(float alpha, const float* src, int64_t src_r
         return SMMC_ESHAPE;
     }
     if (!rows || !cols) return SMMC_OK;
+    DeviceGuard dg;
     int st = select_device(device);
     if (st) return st;
     HostPool& hp = acquire_pool(device);
     std::lock_guard<std::mutex> lk(hp.mu, std::adopt_lock);
+    PoolDrain drain(hp);
     if ((st = ensure_streams(hp))) return st;
     const size_t sb = ((size_t)(rows - 1) * src_row_stride + cols) * sizeof(float);
     const size_t db = ((size_t)(rows - 1) * dst_row_stride + cols) * sizeof(float);
@@ -975,7 +1029,7 @@ int smmc_scalar_matrix_fma_f32_host(float alpha, const float* src, int64_t src_r
         return st;
     if ((st = cuda_status(cudaMemcpyAsync(dst, hp.buf[2], db, cudaMemcpyDeviceToHost, s), "D2H")))
         return st;
-    return cuda_status(cudaStreamSynchronize(s), "scalar_matrix_fma (host path)");
+    return drain.finish(cuda_status(cudaStreamSynchronize(s), "scalar_matrix_fma (host path)"));
 }
 
 }  // extern "C"

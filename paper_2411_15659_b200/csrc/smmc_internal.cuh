@@ -51,6 +51,15 @@ struct Problem {
 void set_error(const char* fmt, ...);
 void count_launches(int n);
 
+// Opt `fn` in to `bytes` of dynamic shared memory on the CURRENT device.  The
+// attribute lives in the device's context, so it is cached per (kernel,
+// device); failures are not cached (defined in smmc_api.cu).
+cudaError_t smem_optin(const void* fn, int bytes);
+template <typename F>
+inline cudaError_t smem_optin(F* fn, int bytes) {
+    return smem_optin(reinterpret_cast<const void*>(fn), bytes);
+}
+
 // Kernel launchers (defined in the kernel translation units).  They return
 // a cudaError_t from cudaGetLastError() after the launch.
 cudaError_t launch_exact(const Problem& p, cudaStream_t s);

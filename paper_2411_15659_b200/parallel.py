@@ -155,6 +155,7 @@ class ShardedSmmConv:
             self.out = out
             self.peers = PeerBuffers(self.out, ipc=ipc)
             self._flag = torch.zeros(1, dtype=torch.float32, device=weights_smm.device)
+            self._flag_host = torch.zeros(1, dtype=torch.float32)
             return
         if shard == "cout":
             self.chunk = -(-geom.out_channels // self.world)
@@ -171,7 +172,17 @@ class ShardedSmmConv:
             self.weights = weights_smm.contiguous()
 
     def _fence(self):
-        if self.world > 1:
+        """Cross-rank ordering point of the fused gather.  NCCL: a 1-element
+        all-reduce on the compute stream (stream-ordered, no host sync).
+        Other backends (gloo -- e.g. several ranks sharing one GPU, which
+        NCCL refuses): drain this rank's device work, then all-reduce a host
+        flag, so no rank passes the fence before every rank's writes landed."""
+        if self.world <= 1:
+            return
+        if self._flag.is_cuda and dist.get_backend() != "nccl":
+            torch.cuda.synchronize(self._flag.device)
+            dist.all_reduce(self._flag_host)
+        else:
             dist.all_reduce(self._flag)
 
     def forward(self, x):

@@ -154,3 +154,13 @@ def test_estimator_params_and_fit_without_gpu():
         smm.Conv2D(out_channels=2, stride=2, backend="smm_tc3").fit(X8)
     with pytest.raises(ValueError):
         smm.Conv2D(out_channels=2, weights=np.zeros((1, 2, 3, 3), np.float32)).fit(X)
+
+
+def test_estimator_threads_is_advisory_like_the_reference():
+    """The reference's Conv2D never validates `threads` (estimator.py:99-110
+    only branches on threads > 1): numpy ints and values < 1 fit fine."""
+    X = smm.random_tensor((1, 2, 6, 6), 0)
+    for t in (np.int64(4), np.int32(1), 0, -3, 16):
+        assert smm.Conv2D(out_channels=2, threads=t).fit(X).geometry_.out_h == 4
+    with pytest.raises(ValueError):
+        smm.Conv2D(out_channels=2, threads="4").fit(X)

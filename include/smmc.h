@@ -102,7 +102,10 @@ SMMC_API size_t smmc_workspace_bytes(const smmc_geom* g, int mode);
  * smm_conv_parallel (smm.py:254-306) and the per-sample loop of
  * Conv2D.transform (estimator.py:112-125) with one batched launch.
  * `workspace` must hold smmc_workspace_bytes(g, mode) bytes (may be NULL if 0),
- * 256-byte aligned.  Alignment: w_smm 16 bytes; y 16 bytes when h'*w' % 4 == 0
+ * 256-byte aligned, and be ZERO-FILLED before its first use: its leading
+ * 64 KB counter region is zero at rest (every launch that uses split-K
+ * counters re-arms them before it exits), so one workspace serves any
+ * sequence of layers on one stream without a per-call memset.  Alignment: w_smm 16 bytes; y 16 bytes when h'*w' % 4 == 0
  * (float4 stores), else 4; x 4 bytes (any sample or channel offset works). */
 SMMC_API int smmc_conv2d_fwd_f32(const float* x, const float* w_smm, float* y,
                         const smmc_geom* g, int mode, void* workspace,

@@ -95,6 +95,10 @@ __global__ void __launch_bounds__(THREADS, MINB) conv1x1_persistent_kernel(const
             const int ch = tid + i * THREADS;
             const int r = ch / (BM / 4);
             const int pq = (ch - r * (BM / 4)) * 4;
+#ifdef SMMC_CHECKED
+            SMMC_CHECK_SMEM(smem_u32(smem), adst + (r * BM + pq) * 4, 16);
+            if (a_ok[i]) SMMC_CHECK_RANGE(a_src[i] + aoff - p.x, 4, (int64_t)p.n * p.c * p.ohw);
+#endif
             cp_async16_zfill(adst + (r * BM + pq) * 4, a_ok[i] ? a_src[i] + aoff : p.x, a_ok[i] ? 16 : 0);
         }
         const uint32_t bdst = smem_u32(Bs + ld_slot * kBK * BN);
@@ -104,6 +108,10 @@ __global__ void __launch_bounds__(THREADS, MINB) conv1x1_persistent_kernel(const
             const int ch = tid + i * THREADS;
             const int r = ch / (BN / 4);
             const int cq = (ch - r * (BN / 4)) * 4;
+#ifdef SMMC_CHECKED
+            SMMC_CHECK_SMEM(smem_u32(smem), bdst + (r * BN + cq) * 4, 16);
+            if (b_bytes[i]) SMMC_CHECK_RANGE(b_src[i] + boff - p.w, b_bytes[i] / 4, (int64_t)p.c * p.co);
+#endif
             cp_async16_zfill(bdst + (r * BN + cq) * 4, b_bytes[i] ? b_src[i] + boff : p.w, b_bytes[i]);
         }
         if (++ld_kb == KT) {
@@ -125,6 +133,10 @@ __global__ void __launch_bounds__(THREADS, MINB) conv1x1_persistent_kernel(const
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc2[i][j] = 0ull;
 
+#ifdef SMMC_CHECKED
+    const uint32_t smem0 = smem_u32(smem);
+    const int64_t x_elems = (int64_t)p.n * p.c * p.ohw, w_elems = (int64_t)p.c * p.co;
+#endif
     const float* a_rd = As + pg * 4;
     const float* b_rd = Bs + cg * 4;
     int slot = 0, kb = 0, lt = 0;
@@ -135,6 +147,8 @@ __global__ void __launch_bounds__(THREADS, MINB) conv1x1_persistent_kernel(const
         cp_async_commit();
         const float* ap = a_rd + slot * (kBK * BM);
         const float* bp = b_rd + slot * (kBK * BN);
+        SMMC_CHECK_SMEM(smem0, smem_u32(ap + (kBK - 1) * BM + BM / 2), 16);
+        SMMC_CHECK_SMEM(smem0, smem_u32(bp + (kBK - 1) * BN + BN / 2), 16);
 #pragma unroll
         for (int kk = 0; kk < kBK; ++kk) {
             float a[TM];
@@ -177,6 +191,8 @@ __global__ void __launch_bounds__(THREADS, MINB) conv1x1_persistent_kernel(const
                         const float2 pr = unpack2(acc2[ib * 4 + ii][j >> 1]);
                         v[ii] = (j & 1) ? pr.y : pr.x;
                     }
+                    SMMC_CHECK_RANGE(((int64_t)n * p.co + co) * p.ohw + rem, 4,
+                                     (int64_t)p.n * p.co * p.ohw);
                     *reinterpret_cast<float4*>(p.y + ((int64_t)n * p.co + co) * p.ohw + rem) =
                         make_float4(v[0], v[1], v[2], v[3]);
                 }

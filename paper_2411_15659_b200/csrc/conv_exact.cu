@@ -48,6 +48,8 @@ __global__ void __launch_bounds__(128) conv_exact_kernel(Problem p) {
             for (int k = 0; k < p.kh; ++k) {
                 const int ih = ih0 + k;
                 if (!col_ok || (unsigned)ih >= (unsigned)p.h) continue;
+                SMMC_CHECK_RANGE(xc + (int64_t)ih * p.w_in + iw - p.x, 1, (int64_t)p.n * p.c * p.hw);
+                SMMC_CHECK_RANGE(wcj + (int64_t)k * p.co - p.w, mcount, (int64_t)p.k * p.co);
                 const float xv = __ldg(xc + (int64_t)ih * p.w_in + iw);
                 const float* wk = wcj + (int64_t)k * p.co;
 #pragma unroll
@@ -60,7 +62,10 @@ __global__ void __launch_bounds__(128) conv_exact_kernel(Problem p) {
     float* yp = p.y + ((int64_t)n * p.co + m0) * p.ohw + rem;
 #pragma unroll
     for (int i = 0; i < MB; ++i)
-        if (i < mcount) yp[(int64_t)i * p.ohw] = acc[i];
+        if (i < mcount) {
+            SMMC_CHECK_RANGE(yp + (int64_t)i * p.ohw - p.y, 1, (int64_t)p.n * p.co * p.ohw);
+            yp[(int64_t)i * p.ohw] = acc[i];
+        }
 }
 
 // buf[r, t] = x[c, r - p_h, j + t*s_w - p_w] or 0 — smm.py:56-73

@@ -56,9 +56,10 @@ constexpr int kStages = 4;
 
 #ifdef SMMC_PROBE_TL
 // Timing probe (A/B builds only, -DSMMC_PROBE_TL=1): per-CTA globaltimer
-// stamps [entry, first stage landed, K loop done, exit, smid] for
+// stamps [entry, first stage landed, K loop done, exit, smid, warp groups
+// summed, split barrier passed (mode 5), -] for
 // tools/timeline_probe.py.
-__device__ unsigned long long g_tl[16384 * 5];
+__device__ unsigned long long g_tl[16384 * 8];
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -67,7 +68,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define TL_STAMP(slot, val)                                                                   \
     do {                                                                                      \
         const unsigned bid_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); \
-        if (threadIdx.x == 0 && bid_ < 16384) g_tl[bid_ * 5 + (slot)] = (val);                \
+        if (threadIdx.x == 0 && bid_ < 16384) g_tl[bid_ * 8 + (slot)] = (val);                \
     } while (0)
 #else
 #define TL_STAMP(slot, val) \
@@ -192,6 +193,11 @@ __global__ void __launch_bounds__(THREADS * G, (G > 1 ? 1 : MINB)) conv_ffma_ker
     }
     const float* __restrict__ xg = p.x;
     const float* __restrict__ wg = p.w;
+#ifdef SMMC_CHECKED
+    const int64_t x_elems = (int64_t)p.n * p.c * p.hw;
+    const int64_t w_elems = (int64_t)p.k * p.co;
+    const uint32_t smem0 = smem_u32(smem);
+#endif
     const uint32_t as_base = smem_u32(As + lk0 * BM + lp);
     const uint32_t bs_base = smem_u32(Bs);
     const bool b_vec = (p.co & 3) == 0;
@@ -262,14 +268,19 @@ __global__ void __launch_bounds__(THREADS * G, (G > 1 ? 1 : MINB)) conv_ffma_ker
         if (CVEC) {
             const uint32_t adst = as_base + slot * AS_STAGE;
 #pragma unroll
-            for (int i = 0; i < A_PER; ++i)
+            for (int i = 0; i < A_PER; ++i) {
+                SMMC_CHECK_SMEM(smem0, adst + i * KSTEP * BM * 4, 4);
+                if (a_ok) SMMC_CHECK_RANGE(a_ptr + i * a_elem - xg, 1, x_elems);
                 cp_async4_zfill(adst + i * KSTEP * BM * 4, a_ok ? a_ptr + i * a_elem : xg, a_ok);
+            }
             const uint32_t bdst = bs_base + slot * BS_STAGE + (brow * BN + bcol) * 4;
 #pragma unroll
             for (int i = 0; i < B_PER; ++i) {
                 if (!B_FULL && tid + i * THREADS >= B_CHUNKS) break;
                 const uint32_t dst = bdst + i * B_ROWS_PER_PASS * BN * 4;
                 const float* src = b_ptr + i * b_pass;
+                SMMC_CHECK_SMEM(smem0, dst, 16);
+                if (b_bytes) SMMC_CHECK_RANGE(src - wg, b_bytes / 4, w_elems);
                 if (b_vec) {
                     cp_async16_zfill(dst, b_bytes ? src : wg, b_bytes);
                 } else {
@@ -295,6 +306,8 @@ __global__ void __launch_bounds__(THREADS * G, (G > 1 ? 1 : MINB)) conv_ffma_ker
 #pragma unroll
                 for (int i = 0; i < A_PER; ++i) {
                     const bool ok = pvalid && od_kidx < p.k && ((rowmask >> od_k) & (colmask >> od_j) & 1u);
+                    SMMC_CHECK_SMEM(smem0, as_base + slot * AS_STAGE + i * KSTEP * BM * 4, 4);
+                    if (ok) SMMC_CHECK_RANGE(xoff0 + od_off, 1, x_elems);
                     cp_async4_zfill(as_base + slot * AS_STAGE + i * KSTEP * BM * 4,
                                     ok ? xg + xoff0 + od_off : xg, ok);
 #pragma unroll
@@ -314,6 +327,7 @@ __global__ void __launch_bounds__(THREADS * G, (G > 1 ? 1 : MINB)) conv_ffma_ker
                 const bool ok = pvalid && kidx < p.k && (unsigned)ih < (unsigned)p.h &&
                                 (unsigned)iw < (unsigned)p.w_in;
                 const float* src = ok ? xg + xoff0 + (int64_t)c * p.hw + kr * p.w_in + j : xg;
+                if (ok) SMMC_CHECK_RANGE(src - xg, 1, x_elems);
                 cp_async4_zfill(as_base + slot * AS_STAGE + i * KSTEP * BM * 4, src, ok);
             }
             }
@@ -326,8 +340,10 @@ __global__ void __launch_bounds__(THREADS * G, (G > 1 ? 1 : MINB)) conv_ffma_ker
                 const int kidx = kb + row;
                 const int co = n0 + col;
                 const uint32_t dst = bs_base + slot * BS_STAGE + (row * BN + col) * 4;
+                SMMC_CHECK_SMEM(smem0, dst, 16);
                 if (b_vec) {
                     const int bytes = (kidx < p.k) ? min(max(p.co - co, 0), 4) * 4 : 0;
+                    if (bytes) SMMC_CHECK_RANGE((int64_t)kidx * p.co + co, bytes / 4, w_elems);
                     cp_async16_zfill(dst, bytes ? wg + (int64_t)kidx * p.co + co : wg, bytes);
                 } else {
 #pragma unroll
@@ -348,6 +364,7 @@ __global__ void __launch_bounds__(THREADS * G, (G > 1 ? 1 : MINB)) conv_ffma_ker
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc2[i][j] = 0ull;
 
+    TL_STAMP(7, gtimer());
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
         if (s < ktiles) load_stage(s, s);
@@ -370,6 +387,8 @@ __global__ void __launch_bounds__(THREADS * G, (G > 1 ? 1 : MINB)) conv_ffma_ker
         const int slot = kt % STAGES;
         const float* ap = a_rd + slot * (BK * BM);
         const float* bp = b_rd + slot * (BK * BN);
+        SMMC_CHECK_SMEM(smem0, smem_u32(ap + (BK - 1) * BM + (NQ - 1) * (BM / NQ)), 16);
+        SMMC_CHECK_SMEM(smem0, smem_u32(bp + (BK - 1) * BN + BN / 2), 16);
 #pragma unroll
         for (int kk = 0; kk < BK; ++kk) {
             float a[TM];
@@ -414,10 +433,12 @@ __global__ void __launch_bounds__(THREADS * G, (G > 1 ? 1 : MINB)) conv_ffma_ker
         float4* red = reinterpret_cast<float4*>(smem);
         if (!lead) {
 #pragma unroll
-            for (int g = 0; g < 2 * TM; ++g)
+            for (int g = 0; g < 2 * TM; ++g) {
+                SMMC_CHECK_SMEM(smem0, smem_u32(red + ((grp - 1) * 2 * TM + g) * THREADS + tid), 16);
                 red[((grp - 1) * 2 * TM + g) * THREADS + tid] =
                     make_float4(acc[g >> 1][(g & 1) * 4 + 0], acc[g >> 1][(g & 1) * 4 + 1],
                                 acc[g >> 1][(g & 1) * 4 + 2], acc[g >> 1][(g & 1) * 4 + 3]);
+            }
         }
         __syncthreads();
         if (lead) {
@@ -433,6 +454,7 @@ __global__ void __launch_bounds__(THREADS * G, (G > 1 ? 1 : MINB)) conv_ffma_ker
         }
         __syncthreads();  // partials read before smem is reused below
     }
+    TL_STAMP(5, gtimer());
 
     // ---- split-K / stream-K: deterministic last-arriver fixup
     bool store = true;
@@ -441,6 +463,8 @@ __global__ void __launch_bounds__(THREADS * G, (G > 1 ? 1 : MINB)) conv_ffma_ker
         float* part = p.ws + (tile * stride_slots) * (BM * BN);
         // layout [slot][2*TM float4 groups][THREADS]: warp stores are contiguous
         float4* mine = reinterpret_cast<float4*>(part + (int64_t)slot * (BM * BN));
+        SMMC_CHECK_RANGE(part - p.ws, (int64_t)nslots * BM * BN, p.ws_floats);
+        SMMC_CHECK_RANGE(tile * 4, 4, (const char*)p.ws - (const char*)p.counters);  // counter region
         if (lead)
 #pragma unroll
         for (int g = 0; g < 2 * TM; ++g)
@@ -507,6 +531,7 @@ __global__ void __launch_bounds__(THREADS * G, (G > 1 ? 1 : MINB)) conv_ffma_ker
                 for (int jj = 0; jj < 4; ++jj) {
                     const int cl = jb * (BN / 2) + cg * 4 + jj;
                     const int j = jb * 4 + jj;
+                    SMMC_CHECK_SMEM(smem0, smem_u32(part + cl * LD + ib * (BM / NQ) + pg * 4), 16);
                     *reinterpret_cast<float4*>(part + cl * LD + ib * (BM / NQ) + pg * 4) =
                         make_float4(acc[ib * 4 + 0][j], acc[ib * 4 + 1][j], acc[ib * 4 + 2][j],
                                     acc[ib * 4 + 3][j]);
@@ -520,6 +545,8 @@ __global__ void __launch_bounds__(THREADS * G, (G > 1 ? 1 : MINB)) conv_ffma_ker
             const int cl = e / (BM / 4);
             const int px = (e - cl * (BM / 4)) * 4;
             const int off = cl * LD + px;
+            SMMC_CHECK_SMEM(smem0, smem_u32(part + off), 16);
+            SMMC_ASSERT(S <= 8);
             // all S (<= 8) remote loads in flight, then the fixed-order sum
             float4 v[8];
 #pragma unroll
@@ -540,6 +567,7 @@ __global__ void __launch_bounds__(THREADS * G, (G > 1 ? 1 : MINB)) conv_ffma_ker
             const int n = pbase / p.ohw;
             const int rem = pbase - n * p.ohw;
             if (vec_ok && pbase + 3 < p.m) {
+                SMMC_CHECK_RANGE(((int64_t)n * p.co + co) * p.ohw + rem, 4, (int64_t)p.n * p.co * p.ohw);
                 *reinterpret_cast<float4*>(p.y + ((int64_t)n * p.co + co) * p.ohw + rem) = a4;
             } else {
                 const float v4[4] = {a4.x, a4.y, a4.z, a4.w};
@@ -548,11 +576,118 @@ __global__ void __launch_bounds__(THREADS * G, (G > 1 ? 1 : MINB)) conv_ffma_ker
                     const int pp = pbase + ii;
                     if (pp >= p.m) break;
                     const int nn = pp / p.ohw;
+                    SMMC_CHECK_RANGE(((int64_t)nn * p.co + co) * p.ohw + (pp - nn * p.ohw), 1,
+                                     (int64_t)p.n * p.co * p.ohw);
                     p.y[((int64_t)nn * p.co + co) * p.ohw + (pp - nn * p.ohw)] = v4[ii];
                 }
             }
         }
         cluster.sync();  // peers may still be reading this CTA's partial
+        TL_STAMP(3, gtimer());
+        return;
+    }
+
+    // ---- reduce_mode 5: split-K reduced inside this launch by ALL S CTAs of
+    // the tile (the grid is launched cooperatively, so every CTA is resident).
+    // Each split publishes its partial tile (tile-contiguous: 2*TM float4
+    // groups x THREADS, group g of lead thread t = 4 pixels of one channel)
+    // to the L2-resident workspace, arrives on the tile counter with a
+    // release reduction and waits (acquire) for all S arrivals; then CTA s
+    // sums slice s of the tile over splits 0..S-1 in order with all its
+    // threads and stores it.  One launch, no serial fixup, no second kernel;
+    // the last CTA to leave re-arms the two tile counters.  (Measured, N = 1
+    // layers: a variant that kept the own split in registers and staged the
+    // S-1 others into shared memory with cp.async on the lead threads only
+    // was 2 us slower; programmatic dependent launch on these single-wave
+    // grids changed nothing -- the next grid's CTAs do not fit beside them.)
+    if (!sk && p.reduce_mode == 5) {
+        constexpr int NG = 2 * TM;        // float4 groups per thread
+        constexpr int POS = NG * THREADS;  // float4 positions per partial tile
+        float4* wsq = reinterpret_cast<float4*>(p.ws) + tile * (int64_t)nslots * POS;
+        auto quad = [&](int g) {
+            return make_float4(acc[(g >> 3) * 4 + 0][g & 7], acc[(g >> 3) * 4 + 1][g & 7],
+                               acc[(g >> 3) * 4 + 2][g & 7], acc[(g >> 3) * 4 + 3][g & 7]);
+        };
+        if (lead) {
+            float4* dst = wsq + (int64_t)slot * POS + tid;
+            SMMC_CHECK_RANGE((const float*)(dst + (NG - 1) * THREADS) - p.ws, 4, p.ws_floats);
+#pragma unroll
+            for (int g = 0; g < NG; ++g)
+                __stcg(dst + g * THREADS, quad(g));
+        }
+        int* ctr = p.counters + 2 * tile;  // [arrive, depart]
+        SMMC_CHECK_RANGE((const char*)(ctr + 1) - (const char*)p.counters, 4,
+                         (const char*)p.ws - (const char*)p.counters);  // counter region
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            // release: this CTA's partial stores (ordered before it by the
+            // barrier) are visible to whoever acquires the count
+            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(ctr) : "memory");
+            int seen;
+            for (;;) {
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(ctr) : "memory");
+                if (seen >= nslots) break;
+                __nanosleep(32);
+            }
+        }
+        __syncthreads();
+        TL_STAMP(6, gtimer());
+        // every thread of the CTA: slice [q0, q1) of the tile's float4
+        // positions (q = g * THREADS + t), splits summed in order 0..S-1 with
+        // 8 loads in flight per round; position q is thread t's float4 g
+        const int q0 = (int)((int64_t)slot * POS / nslots);
+        const int q1 = (int)((int64_t)(slot + 1) * POS / nslots);
+        const bool vec_ok = (p.ohw & 3) == 0;
+        for (int q = q0 + (int)threadIdx.x; q < q1; q += THREADS * G) {
+            const int gq = q / THREADS, t = q - gq * THREADS;
+            float4 a4 = __ldcg(wsq + q);
+            for (int z0 = 1; z0 < nslots; z0 += 8) {
+                float4 v[8];
+#pragma unroll
+                for (int z = 0; z < 8; ++z)
+                    if (z0 + z < nslots) v[z] = __ldcg(wsq + (int64_t)(z0 + z) * POS + q);
+#pragma unroll
+                for (int z = 0; z < 8; ++z)
+                    if (z0 + z < nslots) {
+                        a4.x += v[z].x;
+                        a4.y += v[z].y;
+                        a4.z += v[z].z;
+                        a4.w += v[z].w;
+                    }
+            }
+            const int tw = t >> 5, tl = t & 31;
+            const int tcg = (tw % WCO) * 8 + (tl & 7);
+            const int tpg = (tw / WCO) * 4 + (tl >> 3);
+            const int ib = gq >> 3, j = gq & 7;
+            const int co = n0 + (j >> 2) * (BN / 2) + tcg * 4 + (j & 3);
+            const int pbase = m0 + ib * (BM / NQ) + tpg * 4;
+            if (co >= p.co || pbase >= p.m) continue;
+            const int n = pbase / p.ohw;
+            const int rem = pbase - n * p.ohw;
+            if (vec_ok && pbase + 3 < p.m) {
+                SMMC_CHECK_RANGE(((int64_t)n * p.co + co) * p.ohw + rem, 4, (int64_t)p.n * p.co * p.ohw);
+                *reinterpret_cast<float4*>(p.y + ((int64_t)n * p.co + co) * p.ohw + rem) = a4;
+            } else {
+                const float v4[4] = {a4.x, a4.y, a4.z, a4.w};
+                int nn = n, rr = rem;
+#pragma unroll
+                for (int ii = 0; ii < 4; ++ii) {
+                    if (pbase + ii >= p.m) break;
+                    SMMC_CHECK_RANGE(((int64_t)nn * p.co + co) * p.ohw + rr, 1, (int64_t)p.n * p.co * p.ohw);
+                    p.y[((int64_t)nn * p.co + co) * p.ohw + rr] = v4[ii];
+                    if (++rr == p.ohw) {
+                        rr = 0;
+                        ++nn;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && atomicAdd(ctr + 1, 1) == nslots - 1) {
+            // every split has passed the arrival wait: re-arm for the next launch
+            ctr[0] = 0;
+            ctr[1] = 0;
+        }
         TL_STAMP(3, gtimer());
         return;
     }
@@ -566,6 +701,7 @@ __global__ void __launch_bounds__(THREADS * G, (G > 1 ? 1 : MINB)) conv_ffma_ker
         if (lead) {
             float4* dst =
                 reinterpret_cast<float4*>(p.ws) + ((tile * p.splits + slot) * (2 * TM)) * THREADS + tid;
+            SMMC_CHECK_RANGE((const float*)(dst + (2 * TM - 1) * THREADS) - p.ws, 4, p.ws_floats);
 #pragma unroll
             for (int ib = 0; ib < NQ; ++ib)
 #pragma unroll
@@ -595,6 +731,7 @@ __global__ void __launch_bounds__(THREADS * G, (G > 1 ? 1 : MINB)) conv_ffma_ker
                 if (co >= p.co) continue;
                 const int j = jb * 4 + jj;
                 if (full4) {
+                    SMMC_CHECK_RANGE(((int64_t)n * p.co + co) * p.ohw + rem, 4, (int64_t)p.n * p.co * p.ohw);
                     float4 v = make_float4(acc[ib * 4 + 0][j], acc[ib * 4 + 1][j],
                                            acc[ib * 4 + 2][j], acc[ib * 4 + 3][j]);
                     *reinterpret_cast<float4*>(out + ((int64_t)n * p.co + co) * p.ohw + rem) = v;
@@ -603,6 +740,7 @@ __global__ void __launch_bounds__(THREADS * G, (G > 1 ? 1 : MINB)) conv_ffma_ker
 #pragma unroll
                     for (int ii = 0; ii < 4; ++ii) {
                         if (pbase + ii >= p.m) break;
+                        SMMC_CHECK_RANGE(((int64_t)nn * p.co + co) * p.ohw + rr, 1, (int64_t)p.n * p.co * p.ohw);
                         out[((int64_t)nn * p.co + co) * p.ohw + rr] = acc[ib * 4 + ii][j];
                         if (++rr == p.ohw) {
                             rr = 0;
@@ -626,6 +764,7 @@ __global__ void __launch_bounds__(THREADS * G, (G > 1 ? 1 : MINB)) conv_ffma_ker
 // copy engines are busy with the H2D/D2H pipeline, and a memset queued behind
 // them delayed every conv by 15-50 us (CUPTI timeline, tools/e2e_timeline.py).
 __global__ void __launch_bounds__(256) zero_counters_kernel(int* __restrict__ c, int n) {
+    // (the checked build validates the counter range on the host, conv_device_placed)
     for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) c[i] = 0;
 }
 
@@ -640,6 +779,7 @@ struct ReduceOut {
     int m, bm, bn, threads, wco, tiles_n;
     int nq;  // pixel quads per thread (float4 groups per thread = 8 * nq)
     int vec;  // every replica 16-byte aligned and ohw % 4 == 0 (float4 stores)
+    int64_t ws_floats, y_elems;  // bounds of the checked build
 };
 
 constexpr int kMaxSplits = 32;
@@ -667,6 +807,8 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
         if (co >= ro.co || pbase >= ro.m) continue;
         const float4* src = w4 + (tile * splits * ng + g) * ro.threads + t;
         const int64_t zstride = (int64_t)ng * ro.threads;
+        SMMC_CHECK_RANGE((const float*)(src + (splits - 1) * zstride) - ws, 4, ro.ws_floats);
+        SMMC_ASSERT(splits <= kMaxSplits);
         float4 v[kMaxSplits];
 #pragma unroll
         for (int z = 0; z < kMaxSplits; ++z)
@@ -684,6 +826,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
         const int rem = pbase - n * ro.ohw;
         if (ro.vec && pbase + 3 < ro.m) {  // same sample: ohw % 4 == 0
             const int64_t d = ((int64_t)n * ro.co_total + ro.co_base + co) * ro.ohw + rem;
+            SMMC_CHECK_RANGE(d, 4, ro.y_elems);
 #pragma unroll
             for (int o = 0; o < kMaxOut; ++o)
                 if (o < ro.n_out) *reinterpret_cast<float4*>(ro.ys[o] + d) = a;
@@ -694,6 +837,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
             for (int ii = 0; ii < 4; ++ii) {
                 if (pbase + ii >= ro.m) break;
                 const int64_t d = ((int64_t)nn * ro.co_total + ro.co_base + co) * ro.ohw + rr;
+                SMMC_CHECK_RANGE(d, 1, ro.y_elems);
 #pragma unroll
                 for (int o = 0; o < kMaxOut; ++o)
                     if (o < ro.n_out) ro.ys[o][d] = av[ii];
@@ -715,6 +859,7 @@ constexpr TileCfg kTiles[] = {
     {128, 64, 128, 4, 8, 1},    // 1
     {256, 64, 256, 2, 8, 1},    // 2
     {64, 128, 128, 4, 8, 1},    // 3
+    {64, 64, 64, 8, 8, 0},      // 4: small problems (N = 1), with warp groups / in-kernel split reduce
     // 4 x 8 thread tiles (64 registers, 8 CTAs/SM: latency hiding by
     // occupancy) were measured 1-13 % slower on the c_i = 3 stems and 1x1
     // layers (A/B, round 1) and are not instantiated.
@@ -740,6 +885,19 @@ cudaError_t launch_one(const Problem& p, dim3 grid, cudaStream_t s) {
     auto kern = conv_ffma_kernel<BM, BN, T, MINB, TM, BK, KH, KW, SH, SW, CVEC, SK, G>;
     const cudaError_t attr_err = smem_optin(kern, smem_max);
     if (attr_err != cudaSuccess) return attr_err;
+    if (!SK && p.reduce_mode == 5) {  // every CTA must be resident: cooperative launch
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(T * G);
+        cfg.dynamicSmemBytes = ring;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kern, p);
+    }
     if (!SK && p.reduce_mode == 4) {  // the S splits of a tile form one cluster
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = grid;
@@ -804,24 +962,27 @@ struct TunedPlan {
     int n, c_i, h, w, c_o, k, s, p;
     int variant, splits;
     int groups = 1;
+    int reduce = 0;  // 0: by split count (last arriver / reduce kernel / cluster); 5: in-kernel
 };
+void set_workspace_layout(FfmaPlan& b);
 constexpr TunedPlan kTuned[] = {
-    // N=1: warp-group split-K (third field: groups per CTA), measured as
-    // 20 back-to-back launches in a graph (tools/plan_table_sweep.py)
-    {1, 64, 56, 56, 64, 3, 1, 1, 1, 4, 3},     // 12.3 us (1,4,4: 13.1; 1,8: 14.1)
-    {1, 128, 28, 28, 128, 3, 1, 1, 1, 8, 2},   // 13.2 us (1,8: 14.4)
-    {1, 256, 14, 14, 256, 3, 1, 1, 1, 16, 2},  // 13.9 us (0,32: 15.3)
-    {1, 512, 7, 7, 512, 3, 1, 1, 3, 32, 2},    // 15.4 us (3,32: 16.8; model 42.9)
+    // N=1: 64x64 tiles, warp-group split-K inside the CTA (third field:
+    // groups) and split-K across CTAs reduced in-kernel (fourth field 5) or
+    // in a cluster (splits <= 8); 20 back-to-back launches in a graph
+    // (tools/n1_sweep.py, profiles/r02/n1_sweep.log; round-1 plans in brackets)
+    {1, 64, 56, 56, 64, 3, 1, 1, 4, 3, 4, 5},   // 11.8 us (1,4,3 cluster: 12.8)
+    {1, 128, 28, 28, 128, 3, 1, 1, 4, 5, 4},    // 12.1 us (1,8,2 cluster: 12.7)
+    {1, 256, 14, 14, 256, 3, 1, 1, 4, 9, 4, 5}, // 12.9 us (1,16,2 reduce kernel: 14.1)
+    {1, 512, 7, 7, 512, 3, 1, 1, 4, 18, 4, 5},  // 14.1 us (3,32,2 reduce kernel: 15.1)
     {32, 64, 56, 56, 64, 3, 1, 1, 2, 0},       // 160.0 us (168.0)
     {8, 96, 27, 27, 256, 5, 1, 2, 3, 4},       // 150.1 us (154.2)
-    {256, 64, 56, 56, 256, 1, 1, 0, 3, 1},     // 642.2 us (695.3)
     {256, 128, 28, 28, 128, 3, 1, 1, 0, 1},    // 1083.9 us (1119.4)
-    {8, 512, 7, 7, 512, 3, 1, 1, 3, 24},       // 60.1 us (76.3)
+    {8, 512, 7, 7, 512, 3, 1, 1, 3, 5, 2, 5},  // 53.0 us (3,24 reduce kernel: 56.4; model 76.3)
     {64, 128, 56, 56, 256, 3, 1, 1, 3, 1},     // 2136.5 us (2154.1)
     {64, 256, 56, 56, 256, 3, 1, 1, 3, 1},     // 4206.0 us (4249.3)
     {64, 256, 28, 28, 512, 3, 1, 1, 0, 3},     // 2122.6 us (2164.0)
     {8, 3, 227, 227, 96, 11, 4, 0, 1, 1},      // 73.5 us (73.9)
-    {8, 256, 56, 56, 64, 1, 1, 0, 2, 1},       // 28.6 us (30.6)
+    {8, 256, 56, 56, 64, 1, 1, 0, 4, 1, 2},    // 25.5 us (persistent 1x1 kernel: 26.8)
 };
 
 int64_t best_cost_waves(const FfmaPlan& b, int64_t m, int c_o, int sm_count) {
@@ -929,7 +1090,7 @@ static FfmaPlan plan_ffma_impl(const smmc_geom& g, int sm_count, bool allow_stem
     }
     // measured-best plans for known shapes (tuning table), then the
     // SMMC_FORCE_PLAN="variant,splits" experiment hook (splits 0 = stream-K)
-    int fv = -1, fs = -1, fg = 1;
+    int fv = -1, fs = -1, fg = 1, fr = 0;
     for (const TunedPlan& e : kTuned) {
         if (e.n == g.n && e.c_i == g.c_i && e.h == g.h && e.w == g.w && e.c_o == g.c_o &&
             e.k == g.k_h && g.k_w == g.k_h && e.s == g.s_h && g.s_w == g.s_h && e.p == g.p_h &&
@@ -937,23 +1098,27 @@ static FfmaPlan plan_ffma_impl(const smmc_geom& g, int sm_count, bool allow_stem
             fv = e.variant;
             fs = e.splits;
             fg = e.groups;
+            fr = e.reduce;
         }
     }
+    const bool table_hit = fv >= 0;  // a tuning-table hit also overrides the 1x1 kernel choice
     bool env_forced = false;
-    if (const char* f = getenv("SMMC_FORCE_PLAN")) {  // "variant,splits[,groups]"
-        int v = -1, sp = -1, gr = 1;
-        if (sscanf(f, "%d,%d,%d", &v, &sp, &gr) >= 2) {
+    if (const char* f = getenv("SMMC_FORCE_PLAN")) {  // "variant,splits[,groups[,reduce]]"
+        int v = -1, sp = -1, gr = 1, rd = 0;
+        if (sscanf(f, "%d,%d,%d,%d", &v, &sp, &gr, &rd) >= 2) {
             fv = v;
             fs = sp;
             fg = gr;
+            fr = rd;
             env_forced = true;
         }
     }
+    if (fv == 4 && (!cvec || fs == 0)) fv = -1;  // the 64x64 tile: tap-major split grids only
     // warp groups: tap-major blocks, classic split grid, instantiated
     // (variant, G) pairs only
     const bool groups_ok = cvec && fs > 0 &&
-                           ((fg == 2 && (fv == 0 || fv == 1 || fv == 3)) ||
-                            ((fg == 3 || fg == 4) && (fv == 1 || fv == 3)));
+                           ((fg == 2 && (fv == 0 || fv == 1 || fv == 3 || fv == 4)) ||
+                            ((fg == 3 || fg == 4) && (fv == 1 || fv == 3)) || (fg == 4 && fv == 4));
     if (!groups_ok) fg = 1;
     if (fv >= 0 && fv < kNumTiles && fs >= 0) {
         const TileCfg t = kTiles[fv];
@@ -982,6 +1147,7 @@ static FfmaPlan plan_ffma_impl(const smmc_geom& g, int sm_count, bool allow_stem
             best.kt_per_split = (kt_total + fs - 1) / fs;
             best.splits = (kt_total + best.kt_per_split - 1) / best.kt_per_split;
             best.reduce_mode = best.splits > 1 ? (best.splits <= 4 ? 1 : 2) : 0;
+            if (fr == 5 && best.splits > 1) best.reduce_mode = 5;
             best.groups = fg;
         }
     }
@@ -1003,7 +1169,7 @@ static FfmaPlan plan_ffma_impl(const smmc_geom& g, int sm_count, bool allow_stem
     // workspace); the tiled kernel with the same tile is its fallback for
     // operands that are not 16-byte aligned
     const char* f1 = getenv("SMMC_1X1");  // A/B hook: 0 = tiled kernel
-    if (conv1x1_eligible(g) && (!f1 || atoi(f1) != 0) && !env_forced) {
+    if (conv1x1_eligible(g) && (!f1 || atoi(f1) != 0) && !env_forced && !table_hit) {
         const int v = g.c_o <= 64 ? 1 : 3;  // 128x64 or 64x128
         const TileCfg t = kTiles[v];
         best = FfmaPlan{};
@@ -1040,19 +1206,27 @@ static FfmaPlan plan_ffma_impl(const smmc_geom& g, int sm_count, bool allow_stem
     best.kt_total = kt_total;
     best.cvec = cvec ? 1 : 0;
     best.tap_kind = tap_kind_of(g);
-    if (best.reduce_mode == 1 || best.reduce_mode == 3) {
-        const int slots_per_tile = best.reduce_mode == 1 ? best.splits : best.sk_maxseg;
-        const size_t part = (size_t)best.tiles * slots_per_tile * best.bm * best.bn * sizeof(float);
-        best.ws_counter_offset = (part + 255) & ~(size_t)255;
-        best.ws_bytes = best.ws_counter_offset + (size_t)best.tiles * sizeof(int);
-    } else if (best.reduce_mode == 2) {
-        best.ws_counter_offset = 0;
-        best.ws_bytes = (size_t)best.tiles * best.splits * best.bm * best.bn * sizeof(float);
-    } else {
-        best.ws_bytes = 0;
-        best.ws_counter_offset = 0;
-    }
+    set_workspace_layout(best);
     return best;
+}
+
+// [counter region][partial tiles] (see kCounterRegion).
+void set_workspace_layout(FfmaPlan& b) {
+    b.ws_counter_offset = 0;
+    b.ws_partial_offset = 0;
+    b.ws_bytes = 0;
+    b.zero_counters = 0;
+    if (b.reduce_mode == 0 || b.reduce_mode == 4) return;
+    const int slots_per_tile = b.reduce_mode == 3 ? b.sk_maxseg : b.splits;
+    const size_t part = (size_t)b.tiles * slots_per_tile * b.bm * b.bn * sizeof(float);
+    const size_t counters = b.reduce_mode == 2 ? 0 : (size_t)b.tiles * (b.reduce_mode == 5 ? 2 : 1) * sizeof(int);
+    size_t region = kCounterRegion;
+    if (counters > kCounterRegion) {  // rare: more tiles than the resident region holds
+        region = (counters + 255) & ~(size_t)255;
+        b.zero_counters = 1;
+    }
+    b.ws_partial_offset = region;
+    b.ws_bytes = region + part;
 }
 
 // Plan for the fused c_o-shard gather: the product plan recast to reduce
@@ -1076,17 +1250,16 @@ FfmaPlan plan_ffma_gather(const smmc_geom& g, int sm_count) {
     (void)m;
     pl.persist1x1 = 0;
     pl.reduce_mode = 2;
-    pl.ws_counter_offset = 0;
-    pl.ws_bytes = (size_t)pl.tiles * pl.splits * pl.bm * pl.bn * sizeof(float);
+    set_workspace_layout(pl);
     return pl;
 }
 
 cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
     dim3 grid((p.m + pl.bm - 1) / pl.bm, (p.co + pl.bn - 1) / pl.bn, pl.splits);
     if (pl.reduce_mode == 3) grid = dim3((unsigned)pl.sk_ctas, 1, 1);
-    if (pl.reduce_mode == 1 || pl.reduce_mode == 3) {
-        zero_counters_kernel<<<(int)std::min<int64_t>((pl.tiles + 255) / 256, 148), 256, 0, s>>>(
-            p.counters, (int)pl.tiles);
+    if (pl.zero_counters && (pl.reduce_mode == 1 || pl.reduce_mode == 3 || pl.reduce_mode == 5)) {
+        const int nc = (int)pl.tiles * (pl.reduce_mode == 5 ? 2 : 1);
+        zero_counters_kernel<<<(int)std::min<int64_t>((nc + 255) / 256, 148), 256, 0, s>>>(p.counters, nc);
         count_launches(1);
     }
     cudaError_t e;
@@ -1111,6 +1284,8 @@ cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
             case 1 * 8 + 4: e = launch_tile_groups<128, 64, 128, 4>(p, pl.tap_kind, grid, s); break;
             case 3 * 8 + 2: e = launch_tile_groups<64, 128, 128, 2>(p, pl.tap_kind, grid, s); break;
             case 3 * 8 + 4: e = launch_tile_groups<64, 128, 128, 4>(p, pl.tap_kind, grid, s); break;
+            case 4 * 8 + 2: e = launch_tile_groups<64, 64, 64, 2>(p, pl.tap_kind, grid, s); break;
+            case 4 * 8 + 4: e = launch_tile_groups<64, 64, 64, 4>(p, pl.tap_kind, grid, s); break;
             default: return cudaErrorInvalidConfiguration;
         }
     } else
@@ -1118,6 +1293,7 @@ cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
         case 0: e = launch_tile<128, 128, 256, 2>(p, pl.tap_kind, pl.cvec, grid, s); break;
         case 1: e = launch_tile<128, 64, 128, 4>(p, pl.tap_kind, pl.cvec, grid, s); break;
         case 2: e = launch_tile<256, 64, 256, 2>(p, pl.tap_kind, pl.cvec, grid, s); break;
+        case 4: e = launch_tile_groups<64, 64, 64, 1>(p, pl.tap_kind, grid, s); break;
         default: e = launch_tile<64, 128, 128, 4>(p, pl.tap_kind, pl.cvec, grid, s); break;
     }
     count_launches(1);
@@ -1140,6 +1316,8 @@ cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
     ro.co_base = p.co_base;
     ro.ohw = p.ohw;
     ro.vec = (p.ohw & 3) == 0;
+    ro.ws_floats = p.ws_floats;
+    ro.y_elems = (int64_t)p.n * p.co_total * p.ohw;
     for (int o = 0; o < p.n_out; ++o) ro.vec &= ((uintptr_t)p.ys[o] & 15) == 0;
     splitk_reduce_kernel<<<blocks, 256, 0, s>>>(p.ws, ro, positions, p.splits);
     count_launches(1);
@@ -1150,13 +1328,16 @@ cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
 extern "C" __attribute__((visibility("default"))) int smmc_probe_timeline(unsigned long long* host,
                                                                          int n) {
     if (!host) {  // clear
-        static unsigned long long zeros[16384 * 5];
+        static unsigned long long zeros[16384 * 8];
         return (int)cudaMemcpyToSymbol(g_tl, zeros, sizeof(zeros));
     }
-    return (int)cudaMemcpyFromSymbol(host, g_tl, sizeof(unsigned long long) * 5 * std::min(n, 16384));
+    return (int)cudaMemcpyFromSymbol(host, g_tl, sizeof(unsigned long long) * 8 * std::min(n, 16384));
 }
 #endif
 
-int ffma_launches(const FfmaPlan& pl) { return (pl.reduce_mode == 0 || pl.reduce_mode == 4) ? 1 : 2; }
+int ffma_launches(const FfmaPlan& pl) {
+    if (pl.stem || pl.persist1x1) return 1;
+    return (pl.reduce_mode == 2 ? 2 : 1) + (pl.zero_counters ? 1 : 0);
+}
 
 }  // namespace smmc

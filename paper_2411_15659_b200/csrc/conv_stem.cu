@@ -78,13 +78,18 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
             const int kk = i / Q, q = i - kk * Q;
             const int co = co_base + q * 4;
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (co < p.co) v = __ldg(reinterpret_cast<const float4*>(p.w + (int64_t)kk * p.co + co));
+            if (co < p.co) {
+                SMMC_CHECK_RANGE((int64_t)kk * p.co + co, 4, (int64_t)p.k * p.co);
+                v = __ldg(reinterpret_cast<const float4*>(p.w + (int64_t)kk * p.co + co));
+            }
+            SMMC_CHECK_SMEM(smem_u32(s_w), smem_u32(s_w + kk * BN + wslot(q * 4)), 16);
             *reinterpret_cast<float4*>(s_w + kk * BN + wslot(q * 4)) = v;
         }
     } else {
         for (int i = tid_all; i < p.k * BN; i += T * G) {
             const int kk = i / BN, q = i - kk * BN;
             const int co = co_base + q;
+            SMMC_CHECK_SMEM(smem_u32(s_w), smem_u32(s_w + kk * BN + wslot(q)), 4);
             s_w[kk * BN + wslot(q)] = co < p.co ? __ldg(p.w + (int64_t)kk * p.co + co) : 0.f;
         }
     }
@@ -121,6 +126,12 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
         const int ih = ih0 + kh;
         const bool row_in = (unsigned)ih < (unsigned)p.h;
         const float* xr = xn + ((int64_t)c * p.h + (row_in ? ih : 0)) * p.w_in + iw0;
+#ifdef SMMC_CHECKED
+        const int64_t x_elems = (int64_t)p.n * p.c_i * p.h * p.w_in;
+        if (row_in && cols_in && VOFF < 0) SMMC_CHECK_RANGE(xr - p.x, WIN, x_elems);
+        if (row_in && cols_in && VOFF >= 0) SMMC_CHECK_RANGE(xr - (VOFF >= 0 ? VOFF : 0) - p.x, 4 * NV, x_elems);
+        SMMC_ASSERT(c < p.c_i);
+#endif
         if (VOFF < 0 && row_in && cols_in) {
 #pragma unroll
             for (int t = 0; t < WIN; ++t) win[t] = __ldg(xr + t);
@@ -190,7 +201,10 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
 #pragma unroll
             for (int i = 0; i < PX; ++i)
 #pragma unroll
-                for (int q = 0; q < CP; ++q) red[((grp - 1) * PX * CP + i * CP + q) * T + tid] = acc[i][q];
+                for (int q = 0; q < CP; ++q) {
+                    SMMC_CHECK_SMEM(smem_u32(s_w), smem_u32(red + ((grp - 1) * PX * CP + i * CP + q) * T + tid), 8);
+                    red[((grp - 1) * PX * CP + i * CP + q) * T + tid] = acc[i][q];
+                }
         }
         __syncthreads();
         if (grp > 0 || !active) return;
@@ -222,6 +236,7 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
                 v[px] = __uint_as_float(h2 ? (uint32_t)(a >> 32) : (uint32_t)a);
             }
             float* dst = yrow + (int64_t)co * ohw;
+            SMMC_CHECK_RANGE(dst - p.y, vec ? PX : min(PX, p.ow - ow0), (int64_t)p.n * p.co * ohw);
             if (vec) {
 #pragma unroll
                 for (int v4 = 0; v4 < PX / 4; ++v4)

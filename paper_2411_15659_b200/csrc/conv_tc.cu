@@ -109,7 +109,10 @@ __device__ __forceinline__ void store_tile(const TcParams& p, uint32_t tmem, int
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
                 const int co = co0 + cc * 32 + i;
-                if (co < p.co) p.y[ybase + (int64_t)co * p.ohw] = __uint_as_float(v[i]);
+                if (co < p.co) {
+                    SMMC_CHECK_RANGE(ybase + (int64_t)co * p.ohw, 1, p.y_elems);
+                    p.y[ybase + (int64_t)co * p.ohw] = __uint_as_float(v[i]);
+                }
             }
         }
     }
@@ -382,7 +385,10 @@ conv_tc_halo_persistent_kernel(const __grid_constant__ CUtensorMap tm_a,
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
                         const int co = co0 + cc * 32 + i;
-                        if (co < p.co) yo[ybase + (int64_t)co * p.ohw] = __uint_as_float(v[i]);
+                        if (co < p.co) {
+                            SMMC_CHECK_RANGE(ybase + (int64_t)co * p.ohw, 1, p.y_elems);
+                            yo[ybase + (int64_t)co * p.ohw] = __uint_as_float(v[i]);
+                        }
                     }
                 }
             }

@@ -319,6 +319,7 @@ int conv_device_placed(const float* x, const float* w, const OutPlace& op, const
     p.co_total = op.co_total;
     p.co_base = op.co_base;
     p.ws = static_cast<float*>(ws);
+    p.ws_floats = ws ? (int64_t)(ws_bytes / sizeof(float)) : 0;
     p.n = g->n;
     p.c = g->c_i;
     p.h = g->h;
@@ -360,10 +361,11 @@ int conv_device_placed(const float* x, const float* w, const OutPlace& op, const
             return SMMC_ESHAPE;
         }
     }
-    if (pl.reduce_mode == 1 || pl.reduce_mode == 3) {
+    if (pl.ws_bytes > 0) {
+        // [counter region (zero at rest)][partial tiles], see kCounterRegion
         p.counters = reinterpret_cast<int*>(static_cast<char*>(ws) + pl.ws_counter_offset);
-        // (zeroed by launch_ffma: the workspace may hold another problem's
-        // partials where this plan keeps its counters)
+        p.ws = reinterpret_cast<float*>(static_cast<char*>(ws) + pl.ws_partial_offset);
+        p.ws_floats = (int64_t)((ws_bytes - pl.ws_partial_offset) / sizeof(float));
     }
     return cuda_status(launch_ffma(p, pl, stream), "conv_ffma launch");
 }
@@ -464,6 +466,7 @@ int smmc_plan_describe(const smmc_geom* g, int mode, char* buf, size_t len) {
              : pl.reduce_mode == 1 ? "last-arriver"
              : pl.reduce_mode == 2 ? "kernel"
              : pl.reduce_mode == 4 ? "cluster DSMEM"
+             : pl.reduce_mode == 5 ? "in-kernel, all splits"
                                    : "stream-K",
              (long long)pl.tiles);
     if (pl.groups > 1) {

@@ -9,6 +9,46 @@
 
 #include "../../include/smmc.h"
 
+// ---- SMMC_CHECKED builds (tools/checked_build.sh -> lib/checked/libsmmc.so,
+// selected with SMMC_LIB): device-side bounds asserts on the global and
+// shared-memory accesses of every kernel family; a violation prints the
+// site and traps.  compute-sanitizer is closed on the GPU pool, so this is
+// the out-of-bounds check.  Compiled out of the product library.
+#ifdef SMMC_CHECKED
+#include <cstdio>
+#define SMMC_ASSERT(cond)                                                                    \
+    do {                                                                                     \
+        if (!(cond)) {                                                                       \
+            printf("SMMC_CHECKED %s:%d: %s (block %d,%d,%d thread %d)\n", __FILE__, __LINE__, \
+                   #cond, (int)blockIdx.x, (int)blockIdx.y, (int)blockIdx.z, (int)threadIdx.x);     \
+            __trap();                                                                        \
+        }                                                                                    \
+    } while (0)
+__device__ __forceinline__ uint32_t smmc_dyn_smem_bytes() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+    return r;
+}
+// [addr, addr + bytes) inside the dynamic shared memory starting at base (u32 addresses)
+#define SMMC_CHECK_SMEM(base, addr, bytes)                                 \
+    SMMC_ASSERT((uint32_t)(addr) >= (uint32_t)(base) &&                    \
+                (uint32_t)(addr) - (uint32_t)(base) + (uint32_t)(bytes) <= \
+                    smmc_dyn_smem_bytes())
+// [off, off + count) inside [0, total)
+#define SMMC_CHECK_RANGE(off, count, total) \
+    SMMC_ASSERT((int64_t)(off) >= 0 && (int64_t)(off) + (int64_t)(count) <= (int64_t)(total))
+#else
+#define SMMC_ASSERT(cond) \
+    do {                  \
+    } while (0)
+#define SMMC_CHECK_SMEM(base, addr, bytes) \
+    do {                                   \
+    } while (0)
+#define SMMC_CHECK_RANGE(off, count, total) \
+    do {                                    \
+    } while (0)
+#endif
+
 namespace smmc {
 
 // ----------------------------------------------------------------- problem
@@ -20,6 +60,7 @@ struct Problem {
     const float* w;      // (c_i, k_w, k_h, c_o) == row-major [K][c_o], K = c_i*k_w*k_h
     float* y;            // (n, c_o, oh, ow)
     float* ws;           // split-K partial tiles [tiles][splits][BM*BN] (or null)
+    int64_t ws_floats;   // capacity of ws in floats (bounds of the checked build)
     int* counters;       // split-K arrival counters [tiles] (zero at rest)
     int n, c, h, w_in, co, kh, kw, sh, sw, ph, pw, oh, ow;
     int hw;              // h*w
@@ -31,7 +72,8 @@ struct Problem {
     int splits;
     int cvec;            // 1: tap-major K order (c_i % BK == 0)
     int reduce_mode;     // 0 none, 1 split-K last-arriver, 2 split-K reduce kernel, 3 stream-K,
-                         // 4 split-K reduced in a thread-block cluster (DSMEM)
+                         // 4 split-K reduced in a thread-block cluster (DSMEM),
+                         // 5 split-K reduced in-kernel by all S CTAs of a tile (co-resident grid)
     int64_t tiles;       // pixel tiles x channel tiles
     int tiles_n;         // channel tiles
     int sk_iters;        // stream-K: tap blocks per CTA
@@ -81,9 +123,18 @@ struct FfmaPlan {
     int sk_ctas;       // stream-K grid
     int sk_iters;      // stream-K tap blocks per CTA
     int sk_maxseg;
-    size_t ws_bytes;   // partial tiles + counters
-    size_t ws_counter_offset;
+    size_t ws_bytes;   // counter region + partial tiles
+    size_t ws_counter_offset;   // counters (modes 1, 3, 5): always 0
+    size_t ws_partial_offset;   // partial tiles: after the counter region
+    int zero_counters;          // counters do not fit the resident region: zero per call
 };
+// Workspace layout of every split plan: [counter region][partial tiles].  The
+// counter region (kCounterRegion bytes) is zero at rest: it must be zero-filled
+// once when the workspace is allocated, and every kernel that uses counters
+// re-arms them before it exits, so no per-call zeroing launch is needed.  Plans
+// of other reduce modes never touch it, so one workspace may serve any
+// sequence of layers.
+constexpr size_t kCounterRegion = 64 * 1024;
 FfmaPlan plan_ffma(const smmc_geom& g, int sm_count);
 FfmaPlan plan_ffma_gather(const smmc_geom& g, int sm_count);
 cudaError_t launch_ffma(const Problem& p, const FfmaPlan& plan, cudaStream_t s);

@@ -41,13 +41,27 @@ def repack_weights(weights, geom):
     return weights.permute(1, 3, 2, 0).contiguous()
 
 
+def new_workspace(geom, batch, mode="ffma", device=None):
+    """A zero-filled workspace for ``conv2d`` of this problem (None if the plan
+    needs none)."""
+    torch = _torch()
+    need = _native.workspace_bytes(geom, batch, mode)
+    if not need:
+        return None
+    return torch.zeros(need, dtype=torch.uint8, device=device or torch.cuda.current_device())
+
+
 def conv2d(x, weights_smm, geom, *, mode="ffma", out=None, workspace=None):
     """Batched NCHW forward conv on torch's current stream.
 
     ``x`` (N, c_i, h, w), ``weights_smm`` (c_i, k_w, k_h, c_o) on the same
     device; returns ``out`` (N, c_o, h', w').  Split-K problems need a
-    workspace: pass one (uint8 tensor of ``_native.workspace_bytes`` bytes) to
-    stay allocation-free, else one is taken from torch's caching allocator.
+    workspace: pass one (uint8 tensor of ``_native.workspace_bytes`` bytes,
+    e.g. ``new_workspace``) to stay allocation-free, else a zeroed one is
+    taken from torch's caching allocator.  A workspace must be ZERO-FILLED
+    before its first use (its leading counter region is zero at rest: every
+    launch that uses split-K counters re-arms them), and may then be reused
+    by any sequence of layers on one stream.
     """
     torch = _torch()
     if not isinstance(x, torch.Tensor) or x.dim() != 4:
@@ -71,7 +85,7 @@ def conv2d(x, weights_smm, geom, *, mode="ffma", out=None, workspace=None):
         ws_ptr, ws_len = None, 0
         if need:
             if workspace is None or workspace.numel() * workspace.element_size() < need:
-                workspace = torch.empty(need, dtype=torch.uint8, device=x.device)
+                workspace = torch.zeros(need, dtype=torch.uint8, device=x.device)
             ws_ptr, ws_len = workspace.data_ptr(), workspace.numel() * workspace.element_size()
         stream = torch.cuda.current_stream(x.device).cuda_stream
         _native.check(lib.smmc_conv2d_fwd_f32(
@@ -117,7 +131,7 @@ def conv2d_gather(x, w_slice, outs, geom_local, co_base, co_total, *, workspace=
         ws_ptr, ws_len = None, 0
         if need:
             if workspace is None or workspace.numel() * workspace.element_size() < need:
-                workspace = torch.empty(need, dtype=torch.uint8, device=x.device)
+                workspace = torch.zeros(need, dtype=torch.uint8, device=x.device)
             ws_ptr, ws_len = workspace.data_ptr(), workspace.numel() * workspace.element_size()
         arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
         stream = torch.cuda.current_stream(x.device).cuda_stream
@@ -157,7 +171,7 @@ class SmmConv2d:
         torch = _torch()
         need = _native.workspace_bytes(self.geom, batch, self.mode)
         if need and (self._ws is None or self._ws.numel() < need):
-            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+            self._ws = torch.zeros(need, dtype=torch.uint8, device=self.device)
         return self._ws
 
     def launches(self, batch):

@@ -89,6 +89,7 @@ def test_both_arms_share_the_config_dict():
     class A:
         config = 2
         replicas = 0
+        steps = 20
     for world in (1, 2):
         c = bench.workload_config(A, world)
         assert set(c) == {"workload", "layers", "batch", "parallelism", "l2"}
@@ -107,6 +108,7 @@ def test_reference_arm_line_config1():
     class A:
         config = 1
         replicas = 0
+        steps = 1
     assert d["config"] == bench.workload_config(A, 1)
 
 

@@ -176,7 +176,9 @@ def test_device_path_rejects_bad_tensors():
 def test_split_k_and_fused_plans_both_exercised():
     g_small = ConvGeometry(512, 512, 7, 7, 3, 3, pad_h=1, pad_w=1)
     g_big = ConvGeometry(64, 128, 112, 112, 3, 3, pad_h=1, pad_w=1)
-    assert _native.plan_launches(g_small, 1) == 2
+    # N=1 512@7: split-K reduced inside the one launch (reduce mode 5)
+    assert _native.plan_launches(g_small, 1) == 1
+    assert "in-kernel" in _native.plan_describe(g_small, 1)
     assert _native.workspace_bytes(g_small, 1) > 0
     assert _native.plan_launches(g_big, 64) == 1
     assert _native.workspace_bytes(g_big, 64) == 0
@@ -420,3 +422,58 @@ def test_random_geometries_wide_channels():
         ref = orc.smm_conv_c(x, orc.repack(wt), g, threads=orc.host_threads())
         assert orc.max_abs_ratio(y1.cpu().numpy(), ref) <= TOL_FP32, (g, n, desc)
     assert len(plans) >= 3, plans  # several reduction schemes were exercised
+
+
+@pytest.mark.parametrize("plan", ["4,3,4,5", "4,9,4,5", "4,18,2,5", "1,4,1,5", "3,5,2,5", "0,6,1,5",
+                                  "4,32,1,5", "1,16,2,5"])
+def test_in_kernel_split_reduction(plan, monkeypatch):
+    """Reduce mode 5: all S split CTAs of a tile (cooperative grid) publish
+    their partial tiles, wait on the tile counter and each sums a slice in
+    split order -- S beyond the cluster limit, warp groups, ragged tiles and
+    7x7 planes (h'*w' % 4 != 0).  Oracle parity, bitwise run to run, and the
+    counters re-armed: the same zero-at-rest workspace serves other layers
+    and plans in between."""
+    import torch
+    from paper_2411_15659_b200 import device
+    monkeypatch.setenv("SMMC_FORCE_PLAN", plan)
+    ws = None
+    for g, n in ((ConvGeometry(64, 96, 20, 20, 3, 3, pad_h=1, pad_w=1), 1),
+                 (ConvGeometry(128, 72, 7, 7, 3, 3, pad_h=1, pad_w=1), 2),
+                 (ConvGeometry(64, 64, 9, 11, 3, 3, pad_h=1, pad_w=1), 1)):
+        desc = _native.plan_describe(g, n)
+        assert "in-kernel" in desc and _native.plan_launches(g, n) == 1, desc
+        x, w = synthetic_layer(g, n, 91)
+        wd = torch.from_numpy(smm.repack_weights(w, g)).cuda()
+        xd = torch.from_numpy(x).cuda()
+        need = _native.workspace_bytes(g, n)
+        if ws is None or ws.numel() < need:
+            ws = torch.zeros(max(need, 1 << 22), dtype=torch.uint8, device="cuda")
+        y1 = device.conv2d(xd, wd, g, workspace=ws)
+        y2 = device.conv2d(xd, wd, g, workspace=ws)
+        torch.cuda.synchronize()
+        assert torch.equal(y1, y2), desc
+        ref = orc.smm_conv_c(x, orc.repack(w), g, threads=orc.host_threads())
+        assert orc.max_abs_ratio(y1.cpu().numpy(), ref) <= TOL_FP32, desc
+    # the counter region is zero again after the launches
+    assert int(ws[: 64 * 1024].count_nonzero()) == 0
+
+
+def test_workspace_counter_region_shared_across_plans(monkeypatch):
+    """One zero-initialised workspace reused by a last-arriver plan, a
+    stream-K plan, a reduce-kernel plan and an in-kernel plan in turn (no
+    per-call zeroing): every result matches the oracle."""
+    import torch
+    from paper_2411_15659_b200 import device
+    g = ConvGeometry(64, 96, 14, 14, 3, 3, pad_h=1, pad_w=1)
+    x, w = synthetic_layer(g, 2, 17)
+    ref = orc.smm_conv_c(x, orc.repack(w), g, threads=orc.host_threads())
+    xd, wd = torch.from_numpy(x).cuda(), torch.from_numpy(smm.repack_weights(w, g)).cuda()
+    ws = torch.zeros(64 << 20, dtype=torch.uint8, device="cuda")
+    for rep in range(2):
+        for plan in ("1,3", "3,0", "1,8", "4,6,2,5", "1,2", "0,4,1,5"):
+            monkeypatch.setenv("SMMC_FORCE_PLAN", plan)
+            monkeypatch.setenv("SMMC_CLUSTER_RED", "0")
+            y = device.conv2d(xd, wd, g, workspace=ws)
+            torch.cuda.synchronize()
+            assert orc.max_abs_ratio(y.cpu().numpy(), ref) <= TOL_FP32, (plan, rep)
+    assert int(ws[: 64 * 1024].count_nonzero()) == 0

@@ -72,7 +72,7 @@ for nm, f, b in (("h2d", h2d, hb), ("d2h", d2h, db), ("both", both, hb + db), ("
 from paper_2411_15659_b200 import device  # noqa: E402
 
 sc = torch.cuda.Stream()
-wsd = torch.empty(max(1, _native.workspace_bytes(g, n)), dtype=torch.uint8, device="cuda")
+wsd = torch.zeros(max(1, _native.workspace_bytes(g, n)), dtype=torch.uint8, device="cuda")
 for chunks in (1, 2, 4, 8, 16):
     if chunks > n:
         break

@@ -21,7 +21,7 @@ for li, (name, n, g) in enumerate(CONFIGS[cfg]["layers"]):
     xd, wd = torch.from_numpy(x).cuda(), torch.from_numpy(ws).cuda()
     layers.append(dict(g=g, x=[xd.clone() for _ in range(R)], w=[wd.clone() for _ in range(R)],
                        y=[torch.empty((n,) + g.output_shape, device="cuda") for _ in range(R)],
-                       ws=torch.empty(max(_native.workspace_bytes(g, n), 16), dtype=torch.uint8,
+                       ws=torch.zeros(max(_native.workspace_bytes(g, n), 16), dtype=torch.uint8,
                                       device="cuda")))
 
 

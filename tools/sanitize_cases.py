@@ -24,6 +24,12 @@ import numpy as np  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="")
+    ap.add_argument("--repeat", type=int, default=1,
+                    help="race hunt: relaunch each FFMA case this many times into a NaN-poisoned "
+                         "output (and, with --noise, beside a concurrent stream of unrelated "
+                         "kernels that perturbs CTA scheduling); every result must be bitwise "
+                         "equal to the first")
+    ap.add_argument("--noise", action="store_true")
     args = ap.parse_args()
 
     import torch
@@ -54,6 +60,9 @@ def main():
         ffma("warp_groups_4_last_arriver", g3, 1, {"SMMC_FORCE_PLAN": "1,3,4", "SMMC_CLUSTER_RED": "0"}),
         ffma("warp_groups_4_cluster", g3, 1, {"SMMC_FORCE_PLAN": "3,2,4", "SMMC_CLUSTER_RED": "1"}),
         ffma("warp_groups_reduce_kernel", g3, 1, {"SMMC_FORCE_PLAN": "1,8,2", "SMMC_CLUSTER_RED": "0"}),
+        ffma("inkernel_split_S9_groups4", g3, 1, {"SMMC_FORCE_PLAN": "4,9,4,5"}),
+        ffma("inkernel_split_S18_7x7", G(128, 72, 7, 7, 3), 2, {"SMMC_FORCE_PLAN": "4,18,2,5"}),
+        ffma("inkernel_split_128x64", g3, 2, {"SMMC_FORCE_PLAN": "1,4,1,5"}),
         ffma("generic_order_ci3", G(3, 16, 12, 12, 5), 2, {"SMMC_STEM": "0"}),
         ffma("ragged_co37", G(24, 37, 11, 9, 3), 3, {}),
         ffma("planner_default_n1", G(128, 128, 14, 14, 3), 1, {}),
@@ -91,6 +100,15 @@ def main():
 
     failures = 0
     seed = 1
+    noise_stream = torch.cuda.Stream() if args.noise else None
+    noise_a = torch.randn(2048, 2048, device="cuda") if args.noise else None
+
+    def noise():
+        if noise_stream is not None:
+            with torch.cuda.stream(noise_stream):
+                for _ in range(4):
+                    noise_a.copy_(noise_a @ noise_a * 1e-3)
+
     for name, _, g, n, env, mode, tol in cases:
         if args.only and args.only not in name:
             continue
@@ -103,9 +121,21 @@ def main():
         ref = orc.smm_conv_c(x, ws, g, threads=2)
         err = orc.max_abs_ratio(y.cpu().numpy(), ref)
         ok = (err == 0.0) if tol == 0.0 else err <= tol
+        mism = 0
+        if args.repeat > 1:
+            xd, wd = torch.from_numpy(x).cuda(), torch.from_numpy(ws).cuda()
+            out = torch.empty_like(y)
+            for _ in range(args.repeat - 1):
+                out.fill_(float("nan"))
+                noise()
+                device.conv2d(xd, wd, g, mode=mode, out=out)
+                mism += not torch.equal(out, y)
+            torch.cuda.synchronize()
+            ok = ok and mism == 0
         failures += not ok
-        print(f"{name:32s} {'ok' if ok else 'FAIL'} err={err:.2e} plan: "
-              f"{_native.plan_describe(g, n, mode)}", flush=True)
+        print(f"{name:32s} {'ok' if ok else 'FAIL'} err={err:.2e}"
+              + (f" relaunch mismatches {mism}/{args.repeat - 1}" if args.repeat > 1 else "")
+              + f" plan: {_native.plan_describe(g, n, mode)}", flush=True)
     for name, g, n, env in tc_cases:
         if args.only and args.only not in name:
             continue

@@ -57,9 +57,9 @@ def main():
         mod(xd, out=y)
         e.record()
         torch.cuda.synchronize()
-        buf = np.zeros(16384 * 5, dtype=np.uint64)
+        buf = np.zeros(16384 * 8, dtype=np.uint64)
         probe(buf.ctypes.data, 16384)
-        t = buf.reshape(-1, 5)
+        t = buf.reshape(-1, 8)
         t = t[t[:, 0] != 0].astype(np.int64)
         t0 = t[:, 0].min()
         r = (t[:, :4] - t0) / 1e3
@@ -77,9 +77,16 @@ def main():
         last = np.array([max(v) for v in by_sm.values()])
         print(f"   per-SM exit spread p50 {pct(spread, 50):.1f} max {spread.max():.1f} us; "
               f"SM done p10 {pct(last, 10):.1f} p50 {pct(last, 50):.1f} max {last.max():.1f} us")
+        if (t[:, 7] > 0).all():
+            st = (t[:, 7] - t0) / 1e3
+            print(f"   setup (entry -> first load issued) p50 {pct(st - r[:, 0], 50):.2f}  "
+                  f"loads -> landed p50 {pct(r[:, 1] - st, 50):.2f} us")
         for lab, v in (("entry", r[:, 0]), ("prologue", r[:, 1] - r[:, 0]),
                        ("loop", r[:, 2] - r[:, 1]), ("epilogue", r[:, 3] - r[:, 2]),
-                       ("exit", r[:, 3])):
+                       ("exit", r[:, 3])) + (
+                          (("groups", (t[:, 5] - t0) / 1e3 - r[:, 2]),) if (t[:, 5] > 0).all() else ()) + (
+                          (("barrier", (t[:, 6] - t[:, 5]) / 1e3), ("reduce", r[:, 3] - (t[:, 6] - t0) / 1e3))
+                          if (t[:, 6] > 0).all() else ()):
             print(f"   {lab:9s} min {v.min():7.2f}  p50 {pct(v, 50):7.2f}  p90 {pct(v, 90):7.2f}"
                   f"  max {v.max():7.2f}")
 

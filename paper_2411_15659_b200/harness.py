@@ -4,9 +4,10 @@ GPU counterparts of the reference's harness pieces, same formats:
 
 * layer configs — the reference's line format (``layers.py:1-11, 43-97``):
   ``layer name=<label> ci= co= h= w= kh= kw= [sh= sw= ph= pw=]``;
-* the paper's four parameter sweeps (``layers.py:114-135``) and the VGG-16
-  network (BASELINE config 4 shapes, ``presets/vgg16.cfg``); other presets are
-  read from the reference's own .cfg files via ``load_layer_config``;
+* the paper's four parameter sweeps (``layers.py:114-135``) and the three
+  network presets (AlexNet, VGG-16 -- the BASELINE config 4 shapes -- and
+  YOLOv3-tiny, ``layers.py:28, 100-106``) as data (``workloads.NETWORKS``);
+  any other network is read from a .cfg file via ``load_layer_config``;
 * ``run_bench`` (``runner.py:97-172``): deterministic splitmix64 inputs, one
   warm-up run, median of >= 3 CUDA-event-timed repeats, float64 checksums that
   must agree across backends (1e-3 relative; 2e-2 for the bf16 variant) or
@@ -44,7 +45,7 @@ from .tensors import random_tensor
 __all__ = [
     "LayerSpec", "parse_layer_config", "load_layer_config", "sweep", "builtin_network",
     "BenchRecord", "run_bench", "emit_csv", "parse_csv", "CSV_HEADER", "BACKENDS",
-    "SWEEP_KINDS",
+    "SWEEP_KINDS", "NETWORK_NAMES",
 ]
 
 BACKENDS = ("b200_im2col", "b200_smm", "b200_exact", "b200_bf16_tc", "b200_bf16x3_tc")
@@ -120,15 +121,16 @@ def load_layer_config(path):
     return parse_layer_config(Path(path).read_text())
 
 
+NETWORK_NAMES = ("alexnet", "vgg16", "yolov3")
+
+
 def builtin_network(name):
-    """VGG-16 (the BASELINE config-4 layer shapes, named as in vgg16.cfg)."""
-    if name != "vgg16":
-        raise ConfigError(f"unknown network {name!r}; available: vgg16 "
-                          "(other presets: load_layer_config(<reference .cfg>))")
-    from .workloads import CONFIGS
-    names = ["conv1_1", "conv1_2", "conv2_1", "conv2_2", "conv3_1", "conv3_2", "conv3_3",
-             "conv4_1", "conv4_2", "conv4_3", "conv5_1", "conv5_2", "conv5_3"]
-    return [LayerSpec(nm, g) for nm, (_, _, g) in zip(names, CONFIGS[4]["layers"])]
+    """Convolutional layers of a named architecture (the reference's presets,
+    ``layers.py:100-106``; tables in ``workloads.NETWORKS``)."""
+    if name not in NETWORK_NAMES:
+        raise ConfigError(f"unknown network {name!r}; available: {', '.join(NETWORK_NAMES)}")
+    from .workloads import network_geometries
+    return [LayerSpec(nm, g) for nm, g in network_geometries(name)]
 
 
 def _sq(ci, co, size, k):
@@ -334,7 +336,7 @@ def parse_csv(text):
 def main(argv=None):
     ap = argparse.ArgumentParser(prog="paper_2411_15659_b200.harness")
     src = ap.add_mutually_exclusive_group(required=True)
-    src.add_argument("--network", help="vgg16")
+    src.add_argument("--network", choices=NETWORK_NAMES)
     src.add_argument("--config", help="layer config file (reference .cfg format)")
     src.add_argument("--sweep", choices=SWEEP_KINDS)
     ap.add_argument("--backends", default=",".join(BACKENDS))

@@ -8,7 +8,8 @@ BASELINE.md).  No dataset items are involved: BASELINE names only shapes.
 
 from .geometry import ConvGeometry
 
-__all__ = ["CONFIGS", "layer_seed", "config_layers", "all_layers"]
+__all__ = ["CONFIGS", "NETWORKS", "network_geometries", "layer_seed", "config_layers",
+           "all_layers"]
 
 
 def _c3(c_i, c_o, hw, k=3, s=1, p=1):
@@ -69,3 +70,43 @@ def all_layers():
     for ci, cfg in CONFIGS.items():
         for li, (name, n, g) in enumerate(cfg["layers"]):
             yield ci, li, name, n, g
+
+
+# The reference's three network presets (``layers.py:28``, ``builtin_network``
+# over ``presets/{alexnet,vgg16,yolov3}.cfg``) as layer tables: (name, c_i, c_o,
+# h, w, k_h, k_w, s_h, s_w, p_h, p_w).  Spatial sizes account for the
+# interleaved pooling layers; AlexNet is the single-tower (ungrouped) variant
+# at 224x224, YOLOv3 the compact ("tiny") detector at 416x416 whose conv12
+# consumes the 256 + 128 channel route concatenation.
+NETWORKS = {
+    "alexnet": [
+        ("conv1", 3, 64, 224, 224, 11, 11, 4, 4, 2, 2),
+        ("conv2", 64, 192, 27, 27, 5, 5, 1, 1, 2, 2),
+        ("conv3", 192, 384, 13, 13, 3, 3, 1, 1, 1, 1),
+        ("conv4", 384, 256, 13, 13, 3, 3, 1, 1, 1, 1),
+        ("conv5", 256, 256, 13, 13, 3, 3, 1, 1, 1, 1),
+    ],
+    "vgg16": [(nm, ci, co, hw, hw, 3, 3, 1, 1, 1, 1) for nm, (ci, co, hw) in zip(
+        ["conv1_1", "conv1_2", "conv2_1", "conv2_2", "conv3_1", "conv3_2", "conv3_3",
+         "conv4_1", "conv4_2", "conv4_3", "conv5_1", "conv5_2", "conv5_3"], _VGG16)],
+    "yolov3": [
+        ("conv1", 3, 16, 416, 416, 3, 3, 1, 1, 1, 1),
+        ("conv2", 16, 32, 208, 208, 3, 3, 1, 1, 1, 1),
+        ("conv3", 32, 64, 104, 104, 3, 3, 1, 1, 1, 1),
+        ("conv4", 64, 128, 52, 52, 3, 3, 1, 1, 1, 1),
+        ("conv5", 128, 256, 26, 26, 3, 3, 1, 1, 1, 1),
+        ("conv6", 256, 512, 13, 13, 3, 3, 1, 1, 1, 1),
+        ("conv7", 512, 1024, 13, 13, 3, 3, 1, 1, 1, 1),
+        ("conv8", 1024, 256, 13, 13, 1, 1, 1, 1, 0, 0),
+        ("conv9", 256, 512, 13, 13, 3, 3, 1, 1, 1, 1),
+        ("conv10", 512, 255, 13, 13, 1, 1, 1, 1, 0, 0),
+        ("conv11", 256, 128, 13, 13, 1, 1, 1, 1, 0, 0),
+        ("conv12", 384, 256, 26, 26, 3, 3, 1, 1, 1, 1),
+        ("conv13", 256, 255, 26, 26, 1, 1, 1, 1, 0, 0),
+    ],
+}
+
+
+def network_geometries(name):
+    """[(layer name, ConvGeometry)] of a preset network."""
+    return [(row[0], ConvGeometry(*row[1:])) for row in NETWORKS[name]]

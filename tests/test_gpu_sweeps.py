@@ -1,0 +1,68 @@
+"""SURVEY §8(f)2 on the GPU: the paper's four parameter sweeps and the three
+network presets (AlexNet, VGG-16, YOLOv3-tiny) through the product kernel
+and the bitwise mode, checked against the CPU oracle on the reference
+harness's own data (splitmix64 [0, 1) inputs, seed = spec index, as
+runner.py:118-121), plus the harness records (acceptance criteria 3 and 5
+restated for the GPU backends)."""
+
+import numpy as np
+import pytest
+
+from oracle import smm_oracle as orc
+from paper_2411_15659_b200 import harness as H
+from paper_2411_15659_b200.tensors import random_tensor
+
+pytestmark = pytest.mark.gpu
+
+SPECS = ([("sweep:" + k, s) for k in H.SWEEP_KINDS for s in H.sweep(k)] +
+         [("net:" + n, s) for n in H.NETWORK_NAMES for s in H.builtin_network(n)])
+
+
+@pytest.mark.parametrize("tag,spec", SPECS, ids=[f"{t}:{s.name}" for t, s in SPECS])
+def test_sweep_and_preset_layers_vs_oracle(tag, spec):
+    import torch
+
+    from paper_2411_15659_b200 import device, repack_weights
+    g = spec.geometry
+    x = random_tensor((1,) + g.input_shape, 0)
+    w = random_tensor(g.weights_shape, 1)
+    ws = repack_weights(w, g)
+    ref = orc.smm_conv_c(x, ws, g, threads=orc.host_threads())
+    xd, wd = torch.from_numpy(x).cuda(), torch.from_numpy(ws).cuda()
+    y = device.conv2d(xd, wd, g).cpu().numpy()
+    # the reference's own metric on its own positive data (test_acceptance.py:71-99)
+    assert orc.max_rel_diff(y, ref) <= 1e-4
+    assert orc.max_abs_ratio(y, ref) <= 1e-4
+    if g.flops(1) <= 2e9:  # bitwise mode on the smaller layers
+        ye = device.conv2d(xd, wd, g, mode="exact").cpu().numpy()
+        assert np.array_equal(ye, ref)
+
+
+def test_criterion3_gpu_scratch_records_all_sweeps():
+    """On all 47 sweep geometries: b200_im2col allocates exactly the lowered
+    matrix c_i*k_h*k_w*h'*w' floats (Eq. 1 numerator); b200_smm's global
+    scratch is its split-K workspace only (0 when unsplit: the zero-packed
+    slice lives in shared memory); checksums agree (runner guard)."""
+    specs = [s for k in H.SWEEP_KINDS for s in H.sweep(k)]
+    recs = H.run_bench(specs, ["b200_im2col", "b200_smm"], repeats=3)
+    by = {(r.layer, r.backend): r for r in recs}
+    from paper_2411_15659_b200 import _native
+    for s in specs:
+        g = s.geometry
+        assert by[(s.name, "b200_im2col")].scratch_bytes == \
+            4 * g.in_channels * g.k_h * g.k_w * g.out_h * g.out_w
+        assert by[(s.name, "b200_smm")].scratch_bytes == _native.workspace_bytes(g, 1)
+    assert len(recs) == 2 * 47
+
+
+def test_criterion5_vgg16_speedup_vs_im2col():
+    """Acceptance criterion 5 (test_acceptance.py:174-188) restated on the
+    GPU: the SMM kernel against im2col + cuBLAS SGEMM (TF32 off) per VGG-16
+    layer at the reference harness's batch of 1: >= 80 % layer wins and a
+    whole-network speedup >= 1.3x."""
+    recs = H.run_bench(H.builtin_network("vgg16"), ["b200_im2col", "b200_smm"], repeats=3)
+    im = {r.layer: r.median_time_s for r in recs if r.backend == "b200_im2col"}
+    sm = {r.layer: r.median_time_s for r in recs if r.backend == "b200_smm"}
+    wins = sum(sm[k] <= im[k] for k in im)
+    assert wins / len(im) >= 0.8, (wins, len(im))
+    assert sum(im.values()) / sum(sm.values()) >= 1.3

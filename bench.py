@@ -60,9 +60,12 @@ def parse_args():
     ap.add_argument("--config", type=int, default=None, choices=sorted(CONFIGS),
                     help="BASELINE.json config (default: 4 at --gpus 1, 5 at --gpus > 1)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="ffma", choices=["ffma", "exact", "bf16_tc", "bf16x3_tc"],
+    ap.add_argument("--mode", default="ffma",
+                    choices=["ffma", "exact", "bf16_tc", "bf16_tc_prepacked", "bf16x3_tc"],
                     help="ffma: fp32 product kernel; exact: bitwise mode; bf16_tc: separately "
-                         "labelled bf16-input tcgen05 variant (stride-1 layers); bf16x3_tc: "
+                         "labelled bf16-input tcgen05 variant (stride-1 layers), the fp32 NCHW -> "
+                         "zero-padded bf16 NHWC pack inside the timed step; bf16_tc_prepacked: the "
+                         "same with the input packed once, untimed (the conv kernel alone); bf16x3_tc: "
                          "fp32-accurate split-bf16 tcgen05 path (fp32 in/out, fp32 parity bar; "
                          "input split/pack inside the timed step)")
     ap.add_argument("--replicas", type=int, default=0, help="0 = auto (>2x L2 between reuses)")
@@ -417,7 +420,8 @@ def run_ours(args):
     step_bytes = step_bytes_of(plan)
     R = replicas_for(args, plan)
     gather_path = None
-    tc = args.mode == "bf16_tc"
+    tc = args.mode in ("bf16_tc", "bf16_tc_prepacked")
+    tc_pack = args.mode == "bf16_tc"  # the zero-packing pack inside the timed step
     tc3 = args.mode == "bf16x3_tc"
     if tc or tc3:
         for L in layers:
@@ -427,7 +431,16 @@ def run_ours(args):
     for L in layers:
         xd = torch.from_numpy(L["x_host"]).to(dev)
         wd = torch.from_numpy(L["w_host"]).to(dev)
-        if tc:
+        if tc and tc_pack:
+            # fp32 NCHW inputs, packed to zero-padded bf16 NHWC inside every
+            # step (that pack IS the zero packing); weights once per layer
+            L["x"] = [xd] + [xd.clone() for _ in range(R - 1)]
+            L["xb"] = [torch.empty(device.packed_input_shape(L["gl"], L["n"]), dtype=torch.bfloat16,
+                                   device=dev)]
+            wt = device.pack_weights_bf16(wd, L["gl"])
+            L["wt"] = [wt] + [wt.clone() for _ in range(R - 1)]
+            del wd
+        elif tc:
             # untimed packs: weights once per layer (as the reference's repack),
             # inputs once per replica (the variant's input is bf16 NHWC)
             xb = device.pack_input_bf16(xd, L["gl"])
@@ -489,7 +502,10 @@ def run_ours(args):
             return
         if L["n"] == 0:
             return
-        if tc:
+        if tc and tc_pack:
+            device.pack_input_bf16(L["x"][r], L["gl"], out=L["xb"][0])
+            device.conv2d_bf16_tc(L["xb"][0], L["wt"][r], L["gl"], out=L["y"][r], workspace=L["ws"])
+        elif tc:
             device.conv2d_bf16_tc(L["xb"][r], L["wt"][r], L["gl"], out=L["y"][r], workspace=L["ws"])
         elif tc3:
             device.pack_input_bf16x3(L["x"][r], L["gl"], out=L["x3"])
@@ -603,7 +619,8 @@ def run_ours(args):
         avg = sum(d) / len(d)
         tf = L["flops"] / (avg / 1e3) / 1e12 if avg > 0 else 0.0
         gl = L["gl"]
-        byts = (gl.compulsory_bytes(L["n"], in_bytes=2, w_bytes=2) if tc
+        byts = (gl.compulsory_bytes(L["n"], in_bytes=4, w_bytes=2) if tc_pack
+                else gl.compulsory_bytes(L["n"], in_bytes=2, w_bytes=2) if tc
                 else gl.compulsory_bytes(L["n"], w_bytes=6) if tc3
                 else gl.compulsory_bytes(L["n"]))
         # split-bf16: three bf16 MMAs per fp32-accurate product
@@ -659,10 +676,13 @@ def run_ours(args):
         roofline = {"bound": "tensor", "achieved": dom["tflops"], "peak": bf16_peak_tf,
                     "unit": "TFLOP/s", "frac": round(dom["tflops"] / bf16_peak_tf, 4),
                     "traffic": traffic,
-                    "kernel": f"tcgen05 conv ({dom['layer']}: {dom['plan']})",
+                    "kernel": f"{'bf16 NHWC pack + ' if tc_pack else ''}tcgen05 conv "
+                              f"({dom['layer']}: {dom['plan']})",
                     "peak_source": "bf16_tflops (burst) of MEASURED_PEAKS.json (cuBLAS bf16 GEMM)",
-                    "achieved_def": "dense algorithmic FLOPs of one launch / its avg CUDA-event "
-                                    "duration (per-layer event replay of the timed steps)"}
+                    "achieved_def": "dense algorithmic FLOPs of one layer "
+                                    f"({'pack + conv' if tc_pack else 'conv only, input pre-packed'}) "
+                                    "/ its avg CUDA-event duration (per-layer event replay of the "
+                                    "timed steps)"}
     else:
         roofline = {"bound": "fp32", "achieved": dom["tflops"], "peak": round(fp32_peak_tf, 2),
                     "unit": "TFLOP/s", "frac": dom["frac_fp32_peak"], "traffic": traffic,
@@ -699,7 +719,8 @@ def run_ours(args):
             "ms_per_step": round(max_ms / args.steps, 5), "higher_is_better": True,
             "scaling": "strong" if (args.config == 5 and world > 1) else "weak",
             "vs_baseline": None,
-            "dtype": ("bf16-in/f32-acc" if tc else "f32 (split bf16x3, f32 acc)" if tc3 else "f32"),
+            "dtype": ("bf16-in/f32-acc" + ("" if tc_pack else " (input pre-packed, untimed)")
+                      if tc else "f32 (split bf16x3, f32 acc)" if tc3 else "f32"),
             "data": "synthetic",
             "config": workload_config(args, world),
             "mode": args.mode,
@@ -734,7 +755,7 @@ def run_e2e(args, layers, world, dev):
     import torch.distributed as dist
 
     from paper_2411_15659_b200 import _native
-    if args.mode in ("bf16_tc", "bf16x3_tc"):
+    if args.mode in ("bf16_tc", "bf16_tc_prepacked", "bf16x3_tc"):
         return run_e2e_tc(args, layers, world, dev)
     lib = _native.lib()
     bufs = []
@@ -758,6 +779,15 @@ def run_e2e(args, layers, world, dev):
     def step_fitted():
         for x, _, y, _, layer in bufs:
             layer.forward(x, y, mode=mode)
+
+    def step_async():
+        # every layer's H2D / conv / D2H enqueued on its own staging buffers
+        # and streams, then one wait per layer: layer i's copy-back overlaps
+        # layer i+1's upload and conv
+        for x, _, y, _, layer in bufs:
+            layer.forward_async(x, y, mode=mode)
+        for b in bufs:
+            b[4].wait()
 
     def step_per_call():
         for x, w, y, g, _ in bufs:
@@ -788,7 +818,7 @@ def run_e2e(args, layers, world, dev):
     steps = max(1, min(args.steps, 10))
     flops = sum(L["flops"] for L in layers) * world
     res = {}
-    for key, fn in (("fitted", step_fitted), ("per_call", step_per_call),
+    for key, fn in (("async", step_async), ("fitted", step_fitted), ("per_call", step_per_call),
                     ("threads", step_threads)):
         fn()
         if world > 1:
@@ -804,15 +834,19 @@ def run_e2e(args, layers, world, dev):
     pool.shutdown()
     for b in bufs:
         b[4].close()
-    return {"value": round(res["fitted"], 2), "unit": "GFLOP/s",
+    return {"value": round(res["async"], 2), "unit": "GFLOP/s",
+            "synchronous": {"value": round(res["fitted"], 2),
+                            "path": "smmc_layer_forward_host per layer (each call fills and "
+                                    "drains its own copy pipeline)"},
             "two_host_threads": {"value": round(res["threads"], 2),
                                  "path": "the same smmc_layer_forward_host calls split over two "
                                          "host threads (independent layers; re-entrant C entry, "
                                          "one staging pool and stream set per concurrent call)"},
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
-            "path": "smmc_layer_forward_host (C ABI fitted layer = Conv2D.fit/transform: weights "
-                    "resident after fit, untimed) with page-locked host input/output, wall clock, "
-                    "max over ranks",
+            "path": "smmc_layer_forward_host_async for every layer of the step, then "
+                    "smmc_layer_wait (C ABI fitted layers = Conv2D.fit/transform: weights resident "
+                    "after fit, untimed) with page-locked host input/output, wall clock, max over "
+                    "ranks",
             "per_call_weights": {"value": round(res["per_call"], 2),
                                  "h2d_bytes_per_step": h2d + w_bytes,
                                  "path": "smmc_conv2d_fwd_f32_host (smm_conv_single drop-in: "

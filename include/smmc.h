@@ -227,6 +227,16 @@ SMMC_API int smmc_layer_create(const float* w_smm, const smmc_geom* g, int devic
                                smmc_layer** out);
 SMMC_API int smmc_layer_forward_host(smmc_layer* layer, const float* x, float* y, int n,
                                      int mode);
+/* Asynchronous forward of a fitted layer on host buffers: enqueues the
+ * H2D / conv / D2H pipeline on the layer's OWN staging buffers and streams
+ * (created on first use) and returns at once, so calls on different layers
+ * overlap (one layer's output copy-back with the next layer's upload and
+ * conv).  x and y must stay valid (and y unread) until smmc_layer_wait;
+ * page-locked buffers make the copies truly asynchronous.  A second async
+ * call on the same layer first waits for the previous one. */
+SMMC_API int smmc_layer_forward_host_async(smmc_layer* layer, const float* x, float* y, int n,
+                                           int mode);
+SMMC_API int smmc_layer_wait(smmc_layer* layer);
 SMMC_API int smmc_layer_destroy(smmc_layer* layer);
 
 /* ---- Fused output-channel-shard all-gather.

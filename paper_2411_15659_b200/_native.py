@@ -45,6 +45,7 @@ EXPORTED_SYMBOLS = (
     "smmc_conv2d_fwd_f32_gather", "smmc_gather_workspace_bytes", "smmc_ipc_handle",
     "smmc_ipc_open", "smmc_ipc_close", "smmc_host_alloc_pinned", "smmc_host_free_pinned",
     "smmc_layer_create", "smmc_layer_forward_host", "smmc_layer_destroy",
+    "smmc_layer_forward_host_async", "smmc_layer_wait",
 )
 
 SMMC_MAX_OUT = 8
@@ -126,6 +127,8 @@ _SIGNATURES = {
     "smmc_layer_create": (ctypes.c_int, [_P, _GP, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
     "smmc_layer_forward_host": (ctypes.c_int, [_P, _P, _P, ctypes.c_int, ctypes.c_int]),
     "smmc_layer_destroy": (ctypes.c_int, [_P]),
+    "smmc_layer_forward_host_async": (ctypes.c_int, [_P, _P, _P, ctypes.c_int, ctypes.c_int]),
+    "smmc_layer_wait": (ctypes.c_int, [_P]),
 }
 
 
@@ -254,6 +257,19 @@ class Layer:
                                             ctypes.c_void_p(y.ctypes.data), n, mode_id(mode)),
               "smmc_layer_forward_host")
         return y
+
+    def forward_async(self, x, y, mode="ffma"):
+        """Enqueue x -> y on the layer's own staging buffers and streams and
+        return; ``x`` and ``y`` must stay alive (and ``y`` unread) until
+        ``wait()``.  Calls on different layers overlap their copies."""
+        n = int(x.shape[0])
+        check(lib().smmc_layer_forward_host_async(self._h, ctypes.c_void_p(x.ctypes.data),
+                                                  ctypes.c_void_p(y.ctypes.data), n,
+                                                  mode_id(mode)), "smmc_layer_forward_host_async")
+        return y
+
+    def wait(self):
+        check(lib().smmc_layer_wait(self._h), "smmc_layer_wait")
 
     def close(self):
         if self._h and self._h.value:

@@ -51,7 +51,11 @@ struct StemParams {
 // VOFF >= 0: interior windows start VOFF floats past a 16-byte boundary
 // (fixed per launch: PX * SW % 4 == 0, w_in % 4 == 0), so they are read as
 // float4s (LDG.128) and sliced at compile-time offsets.
-template <int KH, int KW, int SW, int PX, int CPT, int NG, int T, int MINB, bool PF, int G, int VOFF>
+// CI > 0: c_i known at compile time (G == 1, unpipelined): all CI*KH row
+// windows are loaded before the first FMA (one round of loads in flight
+// instead of one per row).
+template <int KH, int KW, int SW, int PX, int CPT, int NG, int T, int MINB, bool PF, int G, int VOFF,
+          int CI = 0>
 __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams p) {
     constexpr int BN = CPT * NG;
     constexpr int PGW = 32 / NG;          // pixel groups per warp
@@ -97,9 +101,16 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
 
     const int lane = tid & 31;
     const int cg = lane % NG;
-    const int pg_raw = blockIdx.x * PGC + (tid >> 5) * PGW + lane / NG;
+    // persistent CTAs: the weight slice above is loaded once, then the CTA
+    // walks pixel-group blocks blockIdx.x, +gridDim.x, ... (a CTA's work per
+    // block is ~1 us: a CTA per block spent a large share of its life in
+    // start-up, weight staging and drain)
+    const int nblk = (p.pg_total + PGC - 1) / PGC;
+#pragma unroll 1
+    for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const int pg_raw = blk * PGC + (tid >> 5) * PGW + lane / NG;
     const bool active = pg_raw < p.pg_total;
-    if (G == 1 && !active) return;
+    if (G == 1 && !active) continue;
     const int pg = active ? pg_raw : p.pg_total - 1;  // G > 1: stay for the barrier
     const int n = pg / p.ohgpr;
     const int rem = pg - n * p.ohgpr;
@@ -173,7 +184,13 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
     const int rows_all = p.c_i * KH;
     const int r_begin = grp * rows_all / G;
     const int rows = (grp + 1) * rows_all / G;
-    if (PF) {
+    if constexpr (CI > 0 && G == 1 && !PF) {
+        float win[CI * KH][WIN];
+#pragma unroll
+        for (int r = 0; r < CI * KH; ++r) load_win(r, win[r]);
+#pragma unroll
+        for (int r = 0; r < CI * KH; ++r) fma_row(r, win[r]);
+    } else if (PF) {
         float wa[WIN], wb[WIN];
         int r = r_begin;
         if (r < rows) load_win(r, wa);
@@ -207,7 +224,7 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
                 }
         }
         __syncthreads();
-        if (grp > 0 || !active) return;
+        if (grp == 0 && active)
 #pragma unroll 1
         for (int g = 1; g < G; ++g)
 #pragma unroll
@@ -220,6 +237,7 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
                 }
     }
     // epilogue: NCHW, PX consecutive columns per channel
+    if (G == 1 || (grp == 0 && active)) {
     const int64_t ohw = (int64_t)p.oh * p.ow;
     const bool vec = PX % 4 == 0 && (p.ow & 3) == 0 && ow0 + PX <= p.ow;
     float* yrow = p.y + ((int64_t)n * p.co) * ohw + (int64_t)orow * p.ow + ow0;
@@ -249,15 +267,23 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
             }
         }
     }
+    }  // epilogue
+    if (G > 1) __syncthreads();  // the partial-tile buffer is reused by the next block
+    }  // persistent block loop
 }
 
-template <int KH, int KW, int SW, int PX, int CPT, int NG, int T, int MINB, bool PF, int G, int VOFF = -1>
+template <int KH, int KW, int SW, int PX, int CPT, int NG, int T, int MINB, bool PF, int G, int VOFF = -1,
+          int CI = 0>
 cudaError_t launch_stem_t(StemParams sp, cudaStream_t s) {
+    if constexpr (CI > 0) {
+        if (sp.c_i != CI || getenv("SMMC_STEM_CI0"))  // A/B hook: runtime-c_i kernel
+            return launch_stem_t<KH, KW, SW, PX, CPT, NG, T, MINB, PF, G, VOFF, 0>(sp, s);
+    }
     if constexpr (VOFF >= 0) {  // vector windows: aligned rows and window starts only
         static_assert((PX * SW) % 4 == 0, "window starts must step by whole float4s");
         const bool ok = (sp.w_in & 3) == 0 && (reinterpret_cast<uintptr_t>(sp.x) & 15) == 0 &&
                         ((-sp.pw) & 3) == VOFF && !getenv("SMMC_STEM_SCALAR");  // A/B hook
-        if (!ok) return launch_stem_t<KH, KW, SW, PX, CPT, NG, T, MINB, PF, G, -1>(sp, s);
+        if (!ok) return launch_stem_t<KH, KW, SW, PX, CPT, NG, T, MINB, PF, G, -1, CI>(sp, s);
     }
     sp.gpr = (sp.ow + PX - 1) / PX;
     sp.ohgpr = sp.oh * sp.gpr;
@@ -266,10 +292,18 @@ cudaError_t launch_stem_t(StemParams sp, cudaStream_t s) {
     constexpr int PGC = (T / 32) * (32 / NG);
     const size_t smem = (size_t)sp.k * BN * sizeof(float) + (size_t)(G - 1) * PX * (CPT / 2) * T * 8;
     if (smem > kStemMaxSmem) return cudaErrorInvalidConfiguration;
-    auto kern = conv_stem_kernel<KH, KW, SW, PX, CPT, NG, T, MINB, PF, G, VOFF>;
+    auto kern = conv_stem_kernel<KH, KW, SW, PX, CPT, NG, T, MINB, PF, G, VOFF, CI>;
     const cudaError_t attr = smem_optin(kern, (int)kStemMaxSmem);
     if (attr != cudaSuccess) return attr;
     dim3 grid((sp.pg_total + PGC - 1) / PGC, (sp.co + BN - 1) / BN);
+    if (!getenv("SMMC_STEM_PERSIST0")) {  // A/B hook: one CTA per pixel-group block
+        int occ = 0, dev = 0, sms = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess)
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T * G, smem) == cudaSuccess &&
+            occ > 0)
+            grid.x = std::max(1u, std::min(grid.x, (unsigned)(sms * occ) / grid.y));
+    }
     kern<<<grid, T * G, smem, s>>>(sp);
     return cudaGetLastError();
 }
@@ -372,7 +406,7 @@ cudaError_t launch_stem(const Problem& p, int kind, cudaStream_t s) {
         // tiled 71.6)
         // 3x3 s1 windows as float4s (w_in % 4 == 0): 370.0 -> 368.0 us; the
         // 7x7 s2 stem measured slower with them (53.3 -> 56.0 us), scalar there
-        case 1: e = launch_stem_t<3, 3, 1, SV1_PX, SV1_CPT, SV1_NG, SV1_T, SV1_MINB, SV1_PF, SV1_G, 3>(sp, s); break;
+        case 1: e = launch_stem_t<3, 3, 1, SV1_PX, SV1_CPT, SV1_NG, SV1_T, SV1_MINB, SV1_PF, SV1_G, 3, 3>(sp, s); break;
         case 2: e = launch_stem_t<7, 7, 2, SV2_PX, SV2_CPT, SV2_NG, SV2_T, SV2_MINB, SV2_PF, SV2_G>(sp, s); break;
         case 3: e = launch_stem_t<11, 11, 4, SV3_PX, SV3_CPT, SV3_NG, SV3_T, SV3_MINB, SV3_PF, SV3_G>(sp, s); break;
         default: return cudaErrorInvalidConfiguration;

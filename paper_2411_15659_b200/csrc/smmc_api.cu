@@ -142,7 +142,7 @@ size_t workspace_for(const smmc_geom& g, int mode, int sm_count) {
 }
 
 // Per-device staging buffers for the *_host entry points.
-constexpr int kMaxChunks = 8;
+constexpr int kMaxChunks = 64;  // ~4 MB chunks up to 64 per call (fill/drain of the copy pipeline)
 
 struct HostPool {
     std::mutex mu;
@@ -199,6 +199,18 @@ HostPool& acquire_pool(int device) {
     }
     wait_on->mu.lock();
     return *wait_on;
+}
+
+void destroy_pool(HostPool& hp) {
+    for (int i = 0; i < 4; ++i)
+        if (hp.buf[i]) cudaFree(hp.buf[i]);
+    for (int i = 0; i < kMaxChunks; ++i) {
+        if (hp.ev_in[i]) cudaEventDestroy(hp.ev_in[i]);
+        if (hp.ev_done[i]) cudaEventDestroy(hp.ev_done[i]);
+    }
+    if (hp.stream) cudaStreamDestroy(hp.stream);
+    if (hp.s_in) cudaStreamDestroy(hp.s_in);
+    if (hp.s_out) cudaStreamDestroy(hp.s_out);
 }
 
 int ensure(HostPool& hp, int i, size_t bytes) {
@@ -577,24 +589,14 @@ int smmc_ipc_close(void* dev_ptr, size_t offset) {
 
 namespace smmc {
 namespace {
-// The host-buffer pipeline.  `w_dev` non-NULL: the weights already live on
-// the device (a fitted smmc_layer) and are not uploaded.
-int host_pipeline(const float* x, const float* w_smm, const float* w_dev, float* y,
-                  const smmc_geom* g, int mode, int device) {
+// The host-buffer pipeline on one staging pool's streams, enqueued only
+// (the caller synchronizes hp.s_out).  `w_dev` non-NULL: the weights already
+// live on the device (a fitted smmc_layer) and are not uploaded.
+int enqueue_host_pipeline(HostPool& hp, const float* x, const float* w_smm, const float* w_dev,
+                          float* y, const smmc_geom* g, int mode, int device) {
     int oh = 0, ow = 0;
     int st = check_geom(g, &oh, &ow);
     if (st) return st;
-    if ((st = check_mode(mode))) return st;
-    if (g->n == 0) return SMMC_OK;
-    if (!x || !(w_smm || w_dev) || !y) {
-        set_error("x, w_smm and y must be non-NULL host pointers");
-        return SMMC_ESHAPE;
-    }
-    DeviceGuard dg;
-    if ((st = select_device(device))) return st;
-    HostPool& hp = acquire_pool(device);
-    std::lock_guard<std::mutex> lk(hp.mu, std::adopt_lock);
-    PoolDrain drain(hp);
     if ((st = ensure_streams(hp))) return st;
     const size_t xs = (size_t)g->c_i * g->h * g->w;          // floats per input sample
     const size_t ys = (size_t)g->c_o * oh * ow;              // floats per output sample
@@ -609,7 +611,7 @@ int host_pipeline(const float* x, const float* w_smm, const float* w_dev, float*
     int chunks = (int)std::min<size_t>((size_t)kMaxChunks, (size_t)g->n);
     static const size_t chunk_bytes = [] {
         const char* f = getenv("SMMC_HOST_CHUNK_MB");  // tuning hook
-        return (size_t)(f && atoi(f) > 0 ? atoi(f) : 4) << 20;
+        return (size_t)(f && atoi(f) > 0 ? atoi(f) : 16) << 20;
     }();
     chunks = (int)std::min<size_t>((size_t)chunks, std::max<size_t>(1, (per_sample * g->n) / chunk_bytes));
     const int per = (g->n + chunks - 1) / chunks;
@@ -656,6 +658,34 @@ int host_pipeline(const float* x, const float* w_smm, const float* w_dev, float*
                               "D2H y")))
             return st;
     }
+    return SMMC_OK;
+}
+
+int check_host_args(const float* x, const float* w_smm, const float* w_dev, float* y,
+                    const smmc_geom* g, int mode) {
+    int oh = 0, ow = 0;
+    int st = check_geom(g, &oh, &ow);
+    if (st) return st;
+    if ((st = check_mode(mode))) return st;
+    if (g->n == 0) return SMMC_OK;
+    if (!x || !(w_smm || w_dev) || !y) {
+        set_error("x, w_smm and y must be non-NULL host pointers");
+        return SMMC_ESHAPE;
+    }
+    return SMMC_OK;
+}
+
+// Synchronous host entry: a free staging pool, the pipeline, then wait.
+int host_pipeline(const float* x, const float* w_smm, const float* w_dev, float* y,
+                  const smmc_geom* g, int mode, int device) {
+    int st = check_host_args(x, w_smm, w_dev, y, g, mode);
+    if (st || g->n == 0) return st;
+    DeviceGuard dg;
+    if ((st = select_device(device))) return st;
+    HostPool& hp = acquire_pool(device);
+    std::lock_guard<std::mutex> lk(hp.mu, std::adopt_lock);
+    PoolDrain drain(hp);
+    if ((st = enqueue_host_pipeline(hp, x, w_smm, w_dev, y, g, mode, device))) return st;
     return drain.finish(cuda_status(cudaStreamSynchronize(hp.s_out), "conv (host path)"));
 }
 }  // namespace
@@ -675,6 +705,10 @@ struct smmc_layer {
     smmc_geom g;     // n unused
     int device;
     float* w = nullptr;
+    // asynchronous forward: the layer's own staging buffers and streams
+    std::mutex mu;
+    smmc::HostPool* pool = nullptr;
+    bool pending = false;
 };
 
 int smmc_layer_create(const float* w_smm, const smmc_geom* g, int device, smmc_layer** out) {
@@ -695,7 +729,9 @@ int smmc_layer_create(const float* w_smm, const smmc_geom* g, int device, smmc_l
     DeviceGuard dg;
     if ((st = select_device(device))) return st;
     const size_t wb = (size_t)gg.c_i * gg.k_w * gg.k_h * gg.c_o * sizeof(float);
-    smmc_layer* L = new smmc_layer{gg, device, nullptr};
+    smmc_layer* L = new smmc_layer();
+    L->g = gg;
+    L->device = device;
     if ((st = cuda_status(cudaMalloc(&L->w, wb), "cudaMalloc(weights)")) ||
         (st = cuda_status(cudaMemcpy(L->w, w_smm, wb, cudaMemcpyHostToDevice), "H2D weights"))) {
         if (L->w) cudaFree(L->w);
@@ -716,15 +752,55 @@ int smmc_layer_forward_host(smmc_layer* L, const float* x, float* y, int n, int 
     return host_pipeline(x, nullptr, L->w, y, &g, mode, L->device);
 }
 
+int smmc_layer_forward_host_async(smmc_layer* L, const float* x, float* y, int n, int mode) {
+    if (!L) {
+        set_error("layer is NULL");
+        return SMMC_ESHAPE;
+    }
+    smmc_geom g = L->g;
+    g.n = n;
+    int st = check_host_args(x, nullptr, L->w, y, &g, mode);
+    if (st || n == 0) return st;
+    DeviceGuard dg;
+    if ((st = select_device(L->device))) return st;
+    std::lock_guard<std::mutex> lk(L->mu);
+    if (!L->pool) L->pool = new HostPool();
+    if (L->pending) {  // the layer's buffers are still in use by the previous call
+        L->pending = false;
+        if ((st = cuda_status(cudaStreamSynchronize(L->pool->s_out), "conv (async host path)")))
+            return st;
+    }
+    PoolDrain drain(*L->pool);
+    if ((st = enqueue_host_pipeline(*L->pool, x, nullptr, L->w, y, &g, mode, L->device))) return st;
+    L->pending = true;
+    return drain.finish(SMMC_OK);  // in flight: smmc_layer_wait drains it
+}
+
+int smmc_layer_wait(smmc_layer* L) {
+    if (!L) {
+        set_error("layer is NULL");
+        return SMMC_ESHAPE;
+    }
+    std::lock_guard<std::mutex> lk(L->mu);
+    if (!L->pending) return SMMC_OK;
+    L->pending = false;
+    DeviceGuard dg;
+    cudaSetDevice(L->device);
+    return cuda_status(cudaStreamSynchronize(L->pool->s_out), "conv (async host path)");
+}
+
 int smmc_layer_destroy(smmc_layer* L) {
     if (!L) return SMMC_OK;
-    int st = SMMC_OK;
+    int st = smmc_layer_wait(L);
+    DeviceGuard dg;
+    cudaSetDevice(L->device);
     if (L->w) {
-        int prev = 0;
-        cudaGetDevice(&prev);
-        cudaSetDevice(L->device);
-        st = cuda_status(cudaFree(L->w), "cudaFree(weights)");
-        cudaSetDevice(prev);
+        const int e = cuda_status(cudaFree(L->w), "cudaFree(weights)");
+        if (!st) st = e;
+    }
+    if (L->pool) {
+        destroy_pool(*L->pool);
+        delete L->pool;
     }
     delete L;
     return st;

@@ -243,3 +243,36 @@ def test_fitted_layer_api():
     assert float(np.abs(est.transform(x)).max()) == 0.0
     import pickle
     assert pickle.loads(pickle.dumps(est)).transform(x).shape == a.shape
+
+
+def test_fitted_layer_async_forward():
+    """smmc_layer_forward_host_async: several layers in flight at once on
+    their own staging buffers/streams (pinned and pageable host buffers),
+    a second call on a busy layer, and close() with work pending -- results
+    equal the synchronous entry bitwise."""
+    layers = []
+    for gt, n, seed in (((64, 64, 28, 28, 3, 3, 1, 1, 1, 1), 6, 1),
+                        ((128, 256, 14, 14, 3, 3, 1, 1, 1, 1), 3, 2),
+                        ((3, 64, 64, 64, 3, 3, 1, 1, 1, 1), 4, 3),
+                        ((32, 16, 9, 9, 1, 1, 1, 1, 0, 0), 2, 4)):
+        g = ConvGeometry(*gt)
+        x, w = synthetic_layer(g, n, seed)
+        ws = smm.repack_weights(w, g)
+        L = _native.Layer(ws, g)
+        ref = np.empty((n,) + g.output_shape, np.float32)
+        L.forward(x, ref)
+        layers.append((L, _native.pinned_copy(x), x, ref,
+                       _native.pinned_empty((n,) + g.output_shape), np.empty_like(ref)))
+    for L, xp, x, _, yp, y in layers:
+        L.forward_async(xp, yp)
+    for L, xp, x, _, yp, y in layers:      # second call on each busy layer (pageable buffers)
+        L.forward_async(x, y)
+    for L, *_ in layers:
+        L.wait()
+        L.wait()                           # idempotent
+    for L, xp, x, ref, yp, y in layers:
+        assert np.array_equal(yp, ref) and np.array_equal(y, ref)
+    layers[0][0].forward_async(layers[0][1], layers[0][4])
+    for L, *_ in layers:                   # destroy with work in flight: waits first
+        L.close()
+    assert np.array_equal(layers[0][4], layers[0][3])

@@ -530,13 +530,15 @@ def run_ours(args):
     nl = len(layers)
     ev = [[torch.cuda.Event(enable_timing=True, external=True) for _ in range(nl + 1)]
           for _ in range(args.steps)]
-    graph = layer_graph = None
+    graph = None
+    layer_graphs = []
     use_graph = world == 1 or all(L["shard"] != "cout" for L in layers)
     if use_graph:
         # timed graph: the K steps back to back, nothing else.  Per-layer
         # event nodes inside it cost ~5 us each (tools/event_overhead_probe.py),
-        # so the per-layer breakdown comes from a second, separately replayed
-        # capture of the same steps with an external event after every layer.
+        # so the per-layer breakdown comes from one more graph per layer: that
+        # layer's K launches of the timed steps (same replicas, same order)
+        # back to back, replayed between two events after an L2 flush.
         cap_stream = torch.cuda.Stream(device=dev)
         cap_stream.wait_stream(torch.cuda.current_stream())
         graph = torch.cuda.CUDAGraph()
@@ -546,13 +548,19 @@ def run_ours(args):
                     step(s % R)
         torch.cuda.synchronize()
         gpu_launches = _native.launch_count() - launches_before
-        layer_graph = torch.cuda.CUDAGraph()
-        cap_stream.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(cap_stream):
-            with torch.cuda.graph(layer_graph, stream=cap_stream):
-                for s in range(args.steps):
-                    ev[s][0].record()
-                    step(s % R, ev[s])
+        for L in layers:
+            lg = torch.cuda.CUDAGraph()
+            cap_stream.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(cap_stream):
+                with torch.cuda.graph(lg, stream=cap_stream):
+                    for s in range(args.steps):
+                        run_layer(L, s % R)
+            layer_graphs.append(lg)
+        torch.cuda.synchronize()
+        # one untimed replay of every graph: the first launch of a graph exec
+        # uploads it (measured: +30 us per step on the 20-node config-1 graph)
+        for g_ in [graph] + layer_graphs:
+            g_.replay()
         torch.cuda.synchronize()
     else:
         gpu_launches = _native.launch_count() - launches_before
@@ -581,12 +589,19 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     elapsed_ms = start.elapsed_time(end)
-    if layer_graph is not None:  # per-layer breakdown (not the headline timing)
-        flush.fill_(2)
-        layer_graph.replay()
-        torch.cuda.synchronize()
-    per_layer = [[ev[s][li].elapsed_time(ev[s][li + 1]) for s in range(args.steps)]
-                 for li in range(nl)]
+    if layer_graphs:  # per-layer breakdown (not the headline timing)
+        per_layer = []
+        for lg in layer_graphs:
+            flush.fill_(2)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            lg.replay()
+            b.record()
+            torch.cuda.synchronize()
+            per_layer.append([a.elapsed_time(b) / args.steps] * args.steps)
+    else:
+        per_layer = [[ev[s][li].elapsed_time(ev[s][li + 1]) for s in range(args.steps)]
+                     for li in range(nl)]
     # soak for the clock record when the timed region is short
     soak_t0 = time.perf_counter()
     while graph is not None and time.perf_counter() - soak_t0 < 1.0 and elapsed_ms < 1000:
@@ -660,7 +675,7 @@ def run_ours(args):
                               f"({dom['layer']}: {dom['plan']})",
                     "peak_source": "hbm_gbs of MEASURED_PEAKS.json (measured copy bandwidth)",
                     "achieved_def": "compulsory bytes (input + weights + output) of one launch / "
-                                    "its avg CUDA-event duration (per-layer event replay of the "
+                                    "its avg CUDA-event duration (per-layer graph replay of the "
                                     "timed steps)"}
     elif tc3:
         roofline = {"bound": "tensor", "achieved": dom["tflops"],
@@ -671,7 +686,7 @@ def run_ours(args):
                                    "MMAs per fp32-accurate product)",
                     "fp32_cuda_core_peak": round(fp32_peak_tf, 2),
                     "achieved_def": "dense algorithmic FLOPs of one layer (pack + conv) / its avg "
-                                    "CUDA-event duration (per-layer event replay of the timed steps)"}
+                                    "CUDA-event duration (per-layer graph replay of the timed steps)"}
     elif tc:
         roofline = {"bound": "tensor", "achieved": dom["tflops"], "peak": bf16_peak_tf,
                     "unit": "TFLOP/s", "frac": round(dom["tflops"] / bf16_peak_tf, 4),
@@ -681,7 +696,7 @@ def run_ours(args):
                     "peak_source": "bf16_tflops (burst) of MEASURED_PEAKS.json (cuBLAS bf16 GEMM)",
                     "achieved_def": "dense algorithmic FLOPs of one layer "
                                     f"({'pack + conv' if tc_pack else 'conv only, input pre-packed'}) "
-                                    "/ its avg CUDA-event duration (per-layer event replay of the "
+                                    "/ its avg CUDA-event duration (per-layer graph replay of the "
                                     "timed steps)"}
     else:
         roofline = {"bound": "fp32", "achieved": dom["tflops"], "peak": round(fp32_peak_tf, 2),
@@ -691,7 +706,7 @@ def run_ours(args):
                                    f"{sm_max:.0f} MHz (sm_max_mhz of MEASURED_PEAKS.json; no "
                                    "measured FP32 peak exists)",
                     "achieved_def": "dense algorithmic FLOPs of one launch / its avg CUDA-event "
-                                    "duration (per-layer event replay of the timed steps)"}
+                                    "duration (per-layer graph replay of the timed steps)"}
         cfile = ROOT / "profiles" / "ffma_ceiling.json"
         if cfile.exists():  # measured register-only FFMA2 ceiling, context for `frac`
             try:
@@ -726,8 +741,9 @@ def run_ours(args):
             "mode": args.mode,
             "gather_path": gather_path,
             "timing": "K steps captured as one CUDA graph (no other nodes), replayed once between "
-                      "CUDA events; max over ranks; per-layer times from a second replay of the "
-                      "same steps with an event after every layer",
+                      "CUDA events after an L2 flush; max over ranks; per-layer times (layers[], "
+                      "roofline) from one graph per layer of its K launches, replayed between "
+                      "CUDA events after an L2 flush",
             "gpu_launches": gpu_launches,
             "clocks": clk,
             "roofline": roofline,

@@ -222,8 +222,19 @@ int ensure(HostPool& hp, int i, size_t bytes) {
     int st = cuda_status(cudaMalloc(&hp.buf[i], bytes), "cudaMalloc(staging)");
     if (st) return st;
     hp.cap[i] = bytes;
-    // split-K counters must start at zero (kernels leave them zeroed)
-    return cuda_status(cudaMemset(hp.buf[i], 0, bytes), "cudaMemset(staging)");
+    if (i != 3) return SMMC_OK;
+    // the workspace's counter region must start at zero (kernels leave it
+    // zeroed).  Ordered on the pool's COMPUTE stream: the pool streams are
+    // non-blocking, so a plain cudaMemset (legacy default stream) is not
+    // ordered before the conv that uses the buffer -- on a first call with
+    // page-locked inputs (fast async H2D) the conv's partial tiles could be
+    // zeroed behind its back (seen once as a wrong 512@7 N=1 host-entry
+    // result on a fresh box)
+#ifdef SMMC_AB_LEGACY_MEMSET  // A/B build reproducing the round-1 race
+    return cuda_status(cudaMemset(hp.buf[i], 0, bytes), "cudaMemset(workspace)");
+#else
+    return cuda_status(cudaMemsetAsync(hp.buf[i], 0, bytes, hp.stream), "cudaMemsetAsync(workspace)");
+#endif
 }
 
 // Restores the caller's current device on every return path of a host entry.

@@ -276,3 +276,50 @@ def test_fitted_layer_async_forward():
     for L, *_ in layers:                   # destroy with work in flight: waits first
         L.close()
     assert np.array_equal(layers[0][4], layers[0][3])
+
+
+_FIRST_CALL = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2411_15659_b200 as smm
+from paper_2411_15659_b200 import ConvGeometry, _native
+d = np.load(sys.argv[2])
+g = ConvGeometry(*[int(v) for v in d["geom"]])
+xp, wp = _native.pinned_copy(d["x"]), _native.pinned_copy(d["ws"])
+if sys.argv[3] == "busy":  # ~40 ms of unrelated work queued on the legacy default stream
+    import torch
+    torch.backends.cuda.matmul.allow_tf32 = False
+    a = torch.randn(4096, 4096, device="cuda")
+    for _ in range(20):
+        a = a @ a * 1e-3
+y = smm.smm_conv_batched(xp, wp, g)
+err = float(np.abs(y.astype(np.float64) - d["ref"]).max() / np.abs(d["ref"]).max())
+print("ERR", err)
+"""
+
+
+@pytest.mark.parametrize("gt,n", [((512, 512, 7, 7, 3, 3, 1, 1, 1, 1), 1),
+                                  ((256, 256, 14, 14, 3, 3, 1, 1, 1, 1), 1)])
+def test_host_entry_first_call_in_fresh_process(gt, n, tmp_path):
+    """The first host-entry call of a process allocates the staging pool and
+    zeroes the split-K workspace; with page-locked inputs the conv starts
+    almost at once.  The zeroing must be ordered before the conv on the
+    pool's (non-blocking) compute stream -- a legacy-stream cudaMemset was
+    not: queued behind other work on the legacy default stream ("busy": a
+    torch GEMM chain), it zeroed the conv's partial tiles."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    g = ConvGeometry(*gt)
+    x, w = synthetic_layer(g, n, 31)
+    ws = smm.repack_weights(w, g)
+    ref = orc.smm_conv_c(x, orc.repack(w), g, threads=orc.host_threads())
+    f = tmp_path / "case.npz"
+    np.savez(f, x=x, ws=ws, ref=ref.astype(np.float64), geom=np.array(gt))
+    root = str(Path(__file__).resolve().parents[1])
+    for mode in ("idle", "busy", "idle", "busy"):
+        out = subprocess.run([sys.executable, "-c", _FIRST_CALL, root, str(f), mode],
+                             capture_output=True, text=True, timeout=180)
+        assert out.returncode == 0, out.stderr[-2000:]
+        err = float(out.stdout.split("ERR")[-1])
+        assert err <= TOL, err

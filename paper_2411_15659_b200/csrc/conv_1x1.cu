@@ -207,6 +207,178 @@ __global__ void __launch_bounds__(THREADS, MINB) conv1x1_persistent_kernel(const
     cp_async_wait<0>();
 }
 
+// Weight-resident variant (round 2): the CTA's whole weight slice
+// W_smm[0:K, n0:n0+BN] (K x BN floats, <= 64 KB) is staged into shared
+// memory ONCE, then the CTA walks the pixel tiles of its channel slice
+// (blockIdx.y) as one continuous stream of 16-deep input blocks through the
+// cp.async ring -- only the input is streamed; no weight tile per block, so
+// c_o = 256 runs as one 64 x 256 tile (input read once, not once per
+// 128-channel tile).  Same thread tile and summation order as the other
+// kernels (bitwise identical results).
+template <int BM, int BN, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) conv1x1_wres_kernel(const Problem p) {
+    constexpr int TM = 8;
+    constexpr int TPX = BM / TM, TCO = BN / 8;
+    static_assert(TPX * TCO == THREADS && TCO % 8 == 0 && TPX % 4 == 0, "thread tile");
+    constexpr int WCO = TCO / 8;
+    constexpr int A_CHUNKS = kBK * BM / 4;
+    static_assert(A_CHUNKS % THREADS == 0, "loader split");
+    constexpr int A_PER = A_CHUNKS / THREADS;
+
+    extern __shared__ __align__(16) float smem[];
+    float* As = smem;                          // [kRing][kBK][BM]
+    float* Ws = smem + kRing * kBK * BM;       // [K][BN]
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int cg = (warp % WCO) * 8 + (lane & 7);
+    const int pg = (warp / WCO) * 4 + (lane >> 3);
+    const int KT = p.c / kBK;
+    const int n0 = blockIdx.y * BN;
+    const int64_t mtiles = (p.m + BM - 1) / BM;
+    const int my_tiles = mtiles > blockIdx.x ? (int)((mtiles - 1 - blockIdx.x) / gridDim.x) + 1 : 0;
+    const int nq = my_tiles * KT;
+
+    // weight slice: K rows x BN columns, 16-byte copies (c_o % 4 == 0)
+    for (int i = tid; i < p.c * (BN / 4); i += THREADS) {
+        const int row = i / (BN / 4), cq = (i - row * (BN / 4)) * 4;
+        const int bytes = min(max(p.co - (n0 + cq), 0), 4) * 4;
+        SMMC_CHECK_SMEM(smem_u32(smem), smem_u32(Ws + row * BN + cq), 16);
+        if (bytes) SMMC_CHECK_RANGE((int64_t)row * p.co + n0 + cq, bytes / 4, (int64_t)p.c * p.co);
+        cp_async16_zfill(smem_u32(Ws + row * BN + cq), bytes ? p.w + (int64_t)row * p.co + n0 + cq : p.w,
+                         bytes);
+    }
+    cp_async_commit();
+
+    int ld_kb = 0, ld_lt = 0, ld_slot = 0;
+    const float* a_src[A_PER];
+    bool a_ok[A_PER];
+    auto tile_setup = [&](int lt) {
+        const int m0 = (int)((blockIdx.x + (int64_t)lt * gridDim.x) * BM);
+#pragma unroll
+        for (int i = 0; i < A_PER; ++i) {
+            const int ch = tid + i * THREADS;
+            const int r = ch / (BM / 4);
+            const int pm = m0 + (ch - r * (BM / 4)) * 4;
+            a_ok[i] = pm < p.m;
+            const int n = a_ok[i] ? pm / p.ohw : 0;
+            const int px = a_ok[i] ? pm - n * p.ohw : 0;
+            a_src[i] = p.x + ((int64_t)n * p.c + r) * p.ohw + px;
+        }
+    };
+    auto load_next = [&]() {
+        if (ld_kb == 0) tile_setup(ld_lt);
+        const uint32_t adst = smem_u32(As + ld_slot * kBK * BM);
+        const int64_t aoff = (int64_t)ld_kb * kBK * p.ohw;
+#pragma unroll
+        for (int i = 0; i < A_PER; ++i) {
+            const int ch = tid + i * THREADS;
+            const int r = ch / (BM / 4);
+            const int pq = (ch - r * (BM / 4)) * 4;
+            SMMC_CHECK_SMEM(smem_u32(smem), adst + (r * BM + pq) * 4, 16);
+            if (a_ok[i]) SMMC_CHECK_RANGE(a_src[i] + aoff - p.x, 4, (int64_t)p.n * p.c * p.ohw);
+            cp_async16_zfill(adst + (r * BM + pq) * 4, a_ok[i] ? a_src[i] + aoff : p.x, a_ok[i] ? 16 : 0);
+        }
+        if (++ld_kb == KT) {
+            ld_kb = 0;
+            ++ld_lt;
+        }
+        ld_slot = ld_slot == kRing - 1 ? 0 : ld_slot + 1;
+    };
+
+#pragma unroll
+    for (int s = 0; s < kRing - 1; ++s) {
+        if (s < nq) load_next();
+        cp_async_commit();
+    }
+
+    uint64_t acc2[TM][4];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc2[i][j] = 0ull;
+
+    const float* a_rd = As + pg * 4;
+    const float* w_rd = Ws + cg * 4;
+    int slot = 0, kb = 0, lt = 0;
+    for (int q = 0; q < nq; ++q) {
+        cp_async_wait<kRing - 2>();  // (the weight group is the oldest: complete first)
+        __syncthreads();
+        if (q + kRing - 1 < nq) load_next();
+        cp_async_commit();
+        const float* ap = a_rd + slot * (kBK * BM);
+        const float* bp = w_rd + kb * kBK * BN;
+#pragma unroll
+        for (int kk = 0; kk < kBK; ++kk) {
+            float a[TM];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const float4 v = *reinterpret_cast<const float4*>(ap + kk * BM + h * (BM / 2));
+                a[4 * h + 0] = v.x;
+                a[4 * h + 1] = v.y;
+                a[4 * h + 2] = v.z;
+                a[4 * h + 3] = v.w;
+            }
+            const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(bp + kk * BN);
+            const ulonglong2 b1 = *reinterpret_cast<const ulonglong2*>(bp + kk * BN + BN / 2);
+            const uint64_t b[4] = {b0.x, b0.y, b1.x, b1.y};
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc2[i][j] = ffma2_bcast(a[i], b[j], acc2[i][j]);
+        }
+        slot = slot == kRing - 1 ? 0 : slot + 1;
+        if (++kb == KT) {  // last block of this tile: store it, restart
+            kb = 0;
+            const int m0 = (int)((blockIdx.x + (int64_t)lt * gridDim.x) * BM);
+#pragma unroll
+            for (int ib = 0; ib < 2; ++ib) {
+                const int pbase = m0 + ib * (BM / 2) + pg * 4;
+                if (pbase >= p.m) continue;
+                const int n = pbase / p.ohw;
+                const int rem = pbase - n * p.ohw;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int co = n0 + (j >> 2) * (BN / 2) + cg * 4 + (j & 3);
+                    if (co >= p.co) continue;
+                    float v[4];
+#pragma unroll
+                    for (int ii = 0; ii < 4; ++ii) {
+                        const float2 pr = unpack2(acc2[ib * 4 + ii][j >> 1]);
+                        v[ii] = (j & 1) ? pr.y : pr.x;
+                    }
+                    SMMC_CHECK_RANGE(((int64_t)n * p.co + co) * p.ohw + rem, 4,
+                                     (int64_t)p.n * p.co * p.ohw);
+                    *reinterpret_cast<float4*>(p.y + ((int64_t)n * p.co + co) * p.ohw + rem) =
+                        make_float4(v[0], v[1], v[2], v[3]);
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc2[i][j] = 0ull;
+            ++lt;
+        }
+    }
+    cp_async_wait<0>();
+}
+
+template <int BM, int BN, int T, int MINB>
+cudaError_t launch_1x1_wres(const Problem& p, int sm_count, cudaStream_t s) {
+    const int smem = (kRing * kBK * BM + p.c * BN) * (int)sizeof(float);
+    auto kern = conv1x1_wres_kernel<BM, BN, T, MINB>;
+    const cudaError_t attr = smem_optin(kern, 227 * 1024);
+    if (attr != cudaSuccess) return attr;
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T, smem) != cudaSuccess || occ < 1)
+        return cudaErrorInvalidConfiguration;
+    const int ntiles = (p.co + BN - 1) / BN;
+    const int64_t mtiles = ((int64_t)p.m + BM - 1) / BM;
+    dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(mtiles, (int64_t)sm_count * occ / ntiles)),
+              (unsigned)ntiles);
+    kern<<<grid, T, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
 template <int BM, int BN, int T, int MINB>
 cudaError_t launch_1x1(const Problem& p, int sm_count, cudaStream_t s) {
     constexpr int smem = kRing * kBK * (BM + BN) * (int)sizeof(float);
@@ -229,8 +401,16 @@ bool conv1x1_eligible(const smmc_geom& g) {
 // (64 x 256 tiles, 256 threads, 2 CTAs/SM — the input read once instead of
 // twice for c_o = 256 — measured 2x slower on the 64->256 layer, dropped.)
 cudaError_t launch_conv1x1(const Problem& p, int bn, int sm_count, cudaStream_t s) {
-    cudaError_t e = bn == 64 ? launch_1x1<128, 64, 128, 4>(p, sm_count, s)
-                             : launch_1x1<64, 128, 128, 4>(p, sm_count, s);
+    cudaError_t e;
+    const char* f = getenv("SMMC_1X1_WRES");  // A/B hook: 0 = streamed-weight kernel
+    const bool wres_ok = (!f || atoi(f) != 0) && p.c <= 256;
+    if (wres_ok && p.co > 128 && p.c * 256 * (int)sizeof(float) <= 96 * 1024)
+        e = launch_1x1_wres<64, 256, 256, 2>(p, sm_count, s);
+    else if (wres_ok && p.co <= 64 && p.c * 64 * (int)sizeof(float) <= 96 * 1024)
+        e = launch_1x1_wres<128, 64, 128, 2>(p, sm_count, s);
+    else
+        e = bn == 64 ? launch_1x1<128, 64, 128, 4>(p, sm_count, s)
+                     : launch_1x1<64, 128, 128, 4>(p, sm_count, s);
     count_launches(1);
     return e;
 }

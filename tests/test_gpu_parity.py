@@ -335,12 +335,15 @@ def test_acceptance_sweep_200_random_geometries():
 @pytest.mark.parametrize("gt,n", [((64, 256, 56, 56, 1, 1), 3), ((256, 64, 28, 28, 1, 1), 2),
                                   ((48, 100, 6, 10, 1, 1), 3), ((16, 4, 4, 4, 1, 1), 1)],
                          ids=["64to256", "256to64", "ragged", "tiny"])
-def test_persistent_1x1_matches_tiled_kernel_bitwise(gt, n, monkeypatch):
-    """1x1 layers run the persistent block-stream kernel: same summation
+@pytest.mark.parametrize("wres", ["1", "0"], ids=["weights_resident", "weights_streamed"])
+def test_persistent_1x1_matches_tiled_kernel_bitwise(gt, n, wres, monkeypatch):
+    """1x1 layers run a persistent block-stream kernel (the weight slice
+    resident in shared memory, or streamed with the input): same summation
     order as the tiled kernel (bitwise equal to it), oracle parity, and the
     tiled fallback for operands that are not 16-byte aligned."""
     import torch
     from paper_2411_15659_b200 import device
+    monkeypatch.setenv("SMMC_1X1_WRES", wres)
     g = ConvGeometry(*gt)
     assert "persistent 1x1" in _native.plan_describe(g, n)
     x, w = synthetic_layer(g, n, 99)

@@ -73,6 +73,9 @@ def main():
         ffma("conv1x1_persistent", G(64, 64, 12, 12, 1, 1, 0), 2, {}),
         ffma("conv1x1_persistent_co128", G(32, 128, 8, 8, 1, 1, 0), 3, {}),
         ffma("conv1x1_tiled", G(64, 64, 12, 12, 1, 1, 0), 2, {"SMMC_1X1": "0"}),
+        ffma("conv1x1_streamed_weights", G(64, 256, 12, 12, 1, 1, 0), 2, {"SMMC_1X1_WRES": "0"}),
+        ffma("conv1x1_resident_w_co256", G(64, 256, 12, 12, 1, 1, 0), 3, {}),
+        ffma("conv1x1_resident_w_co64", G(256, 64, 12, 12, 1, 1, 0), 2, {}),
         ffma("exact_mode", G(5, 7, 9, 8, 3), 2, {}, mode="exact", tol=0.0),
         # the planner's own N=1 plans of config 2 (tuning table: warp groups,
         # cluster DSMEM and reduce-kernel split-K)
@@ -91,6 +94,7 @@ def main():
         ("tc_1x1", G(64, 256, 8, 8, 1, 1, 0), 2, {}),
     ]
     hooks = ("SMMC_FORCE_PLAN", "SMMC_CLUSTER_RED", "SMMC_STEM", "SMMC_STEM_SCALAR", "SMMC_1X1",
+             "SMMC_1X1_WRES",
              "SMMC_TC_PERSIST", "SMMC_TC_MT", "SMMC_TC_BN", "SMMC_TC_KERNEL", "SMMC_TC_SPLIT")
 
     def set_env(env):

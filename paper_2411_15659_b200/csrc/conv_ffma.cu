@@ -82,10 +82,23 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // groups' partial tiles are summed in group order through shared memory
 // (deterministic) and group 0 carries on with the split-K epilogue.  More
 // warps per SM without more global partials or a second reduction level.
+// 64x64 warp-group tiles (the N = 1 plans) run a 3-stage ring per group and
+// are register-capped for 2 CTAs per SM, so the next launch's CTAs fit beside
+// a running grid (programmatic dependent launch, reduce mode 5).
+template <int BM, int BN, int G>
+constexpr int ring_stages() {
+    return (BM == 64 && BN == 64 && G > 1) ? 3 : kStages;
+}
+template <int BM, int BN, int THREADS, int G, int MINB>
+constexpr int min_blocks() {
+    return G > 1 ? ((BM == 64 && BN == 64 && THREADS * G <= 256) ? 2 : 1) : MINB;
+}
+
 template <int BM, int BN, int THREADS, int MINB, int TM, int BK, int KH, int KW, int SH, int SW,
           bool CVEC, bool SK, int G = 1>
-__global__ void __launch_bounds__(THREADS * G, (G > 1 ? 1 : MINB)) conv_ffma_kernel(const Problem p) {
-    constexpr int STAGES = kStages;
+__global__ void __launch_bounds__(THREADS * G, (min_blocks<BM, BN, THREADS, G, MINB>()))
+    conv_ffma_kernel(const Problem p) {
+    constexpr int STAGES = ring_stages<BM, BN, G>();
     constexpr int NQ = TM / 4;             // 4-pixel blocks per thread, BM/NQ apart
     constexpr int TPX = BM / TM;           // pixel groups
     constexpr int TCO = BN / 8;            // channel groups (4 + 4 channels each)
@@ -365,6 +378,10 @@ __global__ void __launch_bounds__(THREADS * G, (G > 1 ? 1 : MINB)) conv_ffma_ker
         for (int j = 0; j < 4; ++j) acc2[i][j] = 0ull;
 
     TL_STAMP(7, gtimer());
+    // mode 5 grids are launched with programmatic stream serialization: the
+    // launch and the setup above overlap the previous grid's tail; wait for
+    // its completion (and memory) before the first global read
+    if (!sk && p.reduce_mode == 5) asm volatile("griddepcontrol.wait;" ::: "memory");
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
         if (s < ktiles) load_stage(s, s);
@@ -410,6 +427,8 @@ __global__ void __launch_bounds__(THREADS * G, (G > 1 ? 1 : MINB)) conv_ffma_ker
         }
     }
     cp_async_wait<0>();
+    // single-wave grid: the next grid may start its setup on freed resources
+    if (!sk && p.reduce_mode == 5) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #ifdef SMMC_PROBE_TL
     if (tl_first) TL_STAMP(2, gtimer());
     tl_first = false;
@@ -879,7 +898,7 @@ cudaError_t launch_one(const Problem& p, dim3 grid, cudaStream_t s) {
     if constexpr (G == 1)
         if (!SK && p.reduce_mode == 3)
             return launch_one<BM, BN, T, MINB, TM, BK, KH, KW, SH, SW, CVEC, true>(p, grid, s);
-    constexpr int ring = G * kStages * BK * (BM + BN) * (int)sizeof(float);
+    constexpr int ring = G * ring_stages<BM, BN, G>() * BK * (BM + BN) * (int)sizeof(float);
     constexpr int part = BN * (BM + 4) * (int)sizeof(float);  // reduce_mode 4 partial tile
     constexpr int smem_max = ring > part ? ring : part;
     auto kern = conv_ffma_kernel<BM, BN, T, MINB, TM, BK, KH, KW, SH, SW, CVEC, SK, G>;
@@ -891,11 +910,13 @@ cudaError_t launch_one(const Problem& p, dim3 grid, cudaStream_t s) {
         cfg.blockDim = dim3(T * G);
         cfg.dynamicSmemBytes = ring;
         cfg.stream = s;
-        cudaLaunchAttribute at[1];
+        cudaLaunchAttribute at[2];
         at[0].id = cudaLaunchAttributeCooperative;
         at[0].val.cooperative = 1;
+        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
-        cfg.numAttrs = 1;
+        cfg.numAttrs = getenv("SMMC_NO_PDL") ? 1 : 2;  // A/B hook
         return cudaLaunchKernelEx(&cfg, kern, p);
     }
     if (!SK && p.reduce_mode == 4) {  // the S splits of a tile form one cluster

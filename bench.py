@@ -397,10 +397,19 @@ def run_ours(args):
     from paper_2411_15659_b200.parallel import all_gather_cout
 
     rank, world, local = dist_env()
+    # SMMC_BENCH_BACKEND=gloo: a plumbing check of the N>1 path with several
+    # ranks on fewer GPUs (NCCL refuses two ranks per device; timings of such
+    # a run mean nothing)
+    backend = os.environ.get("SMMC_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     plan = layer_plan(args.config, rank, world)
 
     # ---- data: synthetic host arrays -> HBM, R replicas

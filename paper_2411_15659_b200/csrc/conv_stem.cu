@@ -32,6 +32,20 @@
 namespace smmc {
 namespace {
 
+// cp.async.wait_group with a count that is constant after unrolling (the
+// instruction takes an immediate); counts past the table wait for everything.
+__device__ __forceinline__ void cp_async_wait_pending(int n) {
+#define SMMC_WAIT_CASE(N) \
+    case N: asm volatile("cp.async.wait_group " #N ";\n" ::: "memory"); break;
+    switch (n) {
+        SMMC_WAIT_CASE(1) SMMC_WAIT_CASE(2) SMMC_WAIT_CASE(3) SMMC_WAIT_CASE(4) SMMC_WAIT_CASE(5)
+        SMMC_WAIT_CASE(6) SMMC_WAIT_CASE(7) SMMC_WAIT_CASE(8) SMMC_WAIT_CASE(9) SMMC_WAIT_CASE(10)
+        SMMC_WAIT_CASE(11) SMMC_WAIT_CASE(12) SMMC_WAIT_CASE(13) SMMC_WAIT_CASE(14) SMMC_WAIT_CASE(15)
+        default: asm volatile("cp.async.wait_group 0;\n" ::: "memory"); break;
+    }
+#undef SMMC_WAIT_CASE
+}
+
 struct StemParams {
     const float* x;
     const float* w;
@@ -129,8 +143,14 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
     const float* wcg = s_w + cg * 4;
     // interior windows need no column predicate
     constexpr int NV = VOFF >= 0 ? (VOFF + WIN + 3) / 4 : 1;  // float4s per vector window
+    // Scalar windows may run past the row end when the columns past it feed only
+    // this thread's discarded output columns (ow0 + px >= ow, right-edge group
+    // of a row whose width is not a multiple of PX): they read the next row's
+    // floats, never zero padding -- except in the tensor's very last row.
+    const int px_valid = min(PX, p.ow - ow0);
     const bool cols_in = VOFF >= 0 ? iw0 - VOFF >= 0 && iw0 - VOFF + 4 * NV <= p.w_in
-                                   : iw0 >= 0 && iw0 + WIN <= p.w_in;
+                                   : iw0 >= 0 && iw0 + (px_valid - 1) * SW + KW <= p.w_in &&
+                                         (iw0 + WIN <= p.w_in || n + 1 < p.n || ih0 + KH < p.h);
     // one (c, kh) input row window; columns/rows in the zero padding read as 0
     auto load_win = [&](int r, float (&win)[WIN]) {
         const int c = r / KH, kh = r - c * KH;
@@ -143,10 +163,13 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
         if (row_in && cols_in && VOFF >= 0) SMMC_CHECK_RANGE(xr - (VOFF >= 0 ? VOFF : 0) - p.x, 4 * NV, x_elems);
         SMMC_ASSERT(c < p.c_i);
 #endif
-        if (VOFF < 0 && row_in && cols_in) {
+        // one path per warp: a warp with an edge lane runs the predicated loads
+        // for all its lanes instead of both paths one after the other
+        const bool fast = __all_sync(__activemask(), row_in && cols_in);
+        if (VOFF < 0 && fast) {
 #pragma unroll
             for (int t = 0; t < WIN; ++t) win[t] = __ldg(xr + t);
-        } else if (VOFF >= 0 && row_in && cols_in) {
+        } else if (VOFF >= 0 && fast) {
             float4 v[NV];
             const float4* xv = reinterpret_cast<const float4*>(xr - (VOFF >= 0 ? VOFF : 0));
 #pragma unroll
@@ -308,7 +331,353 @@ cudaError_t launch_stem_t(StemParams sp, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Resident-window variant (round 2): for stems whose CI*KH row windows all fit
+// in registers (3x3 s1, c_i = 3: 9 windows of 6 floats).  Three changes
+// against conv_stem_kernel, each aimed at the non-FFMA2 half of its dynamic
+// instruction count (ncu: 52 % FFMA2, issue slots 44 % busy, long-scoreboard
+// stalls behind the per-tile window loads):
+//   * NP channel passes per window set: a CTA owns CPT*NG*NP output channels
+//     and a thread runs its PX x CPT accumulator tile NP times over the SAME
+//     window registers -- window loads, predicates and index math per FFMA2
+//     drop by NP, and the input is read once per CTA instead of once per
+//     channel tile;
+//   * cross-tile prefetch without a second buffer: in the last pass, as soon
+//     as row r's FFMA2s are issued its window registers are dead, and the NEXT
+//     tile's row r window is loaded into them -- every window load has a whole
+//     tile of math in flight ahead of its first use;
+//   * the persistent walk advances (n, row, column group) by a precomputed
+//     stride with carries instead of two integer divisions per tile.
+// Windows are read as [HEAD scalars][NV4 aligned float4s][TAIL scalars] (rows
+// 16-byte aligned, window starts at a fixed offset from a 16-byte boundary), so
+// every load carries ONE predicate (zero padding = predicate off) and no
+// per-element column test exists.
+//
+// ASYNC = 1 (the shipped conv1_1 plan): the windows are not held in registers
+// but staged in a PRIVATE per-thread slice of shared memory by cp.async (the
+// zero padding = src-size 0, the same zero packing as the tiled kernel's
+// loader), one commit group per row.  The register version's 27 loads share
+// one scoreboard, so its first FMA waited for the LAST window issued (ncu: 7.5 %
+// of all stall samples on that one FFMA2); cp.async groups complete in order,
+// `wait_group R-1-r` waits for exactly row r, and the ~54 window registers it
+// frees buy a 512-thread CTA (16 warps per SM instead of 12).  No CTA barrier:
+// every thread reads only what it copied itself.
+template <int KH, int KW, int SW, int PX, int CPT, int NG, int NP, int T, int MINB, int CI, int VOFF,
+          int ASYNC = 0>
+__global__ void __launch_bounds__(T, MINB) conv_stem_rw_kernel(const StemParams p) {
+    constexpr int BNP = CPT * NG;         // channels per pass
+    constexpr int BN = BNP * NP;          // channels per CTA
+    constexpr int PGW = 32 / NG;
+    constexpr int PGC = (T / 32) * PGW;
+    constexpr int WIN = (PX - 1) * SW + KW;
+    constexpr int CP = CPT / 2;
+    constexpr int R = CI * KH;
+    constexpr int HEAD = (4 - VOFF) % 4 < WIN ? (4 - VOFF) % 4 : WIN;
+    constexpr int NV4 = (WIN - HEAD) / 4;
+    constexpr int TAIL = WIN - HEAD - 4 * NV4;
+    extern __shared__ __align__(16) float s_w[];  // [k][BN]: pass-major, then permuted as above
+    auto wslot = [](int col) {
+        const int ps = col / BNP, c2 = col - ps * BNP;
+        const int cg_ = c2 / CPT, r = c2 - cg_ * CPT;
+        return ps * BNP + (r >> 2) * (4 * NG) + cg_ * 4 + (r & 3);
+    };
+    const int tid = threadIdx.x;
+    const int co_base = blockIdx.y * BN;
+    {
+        constexpr int Q = BN / 4;  // launcher guarantees co % 4 == 0
+        for (int i = tid; i < p.k * Q; i += T) {
+            const int kk = i / Q, q = i - kk * Q;
+            const int co = co_base + q * 4;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (co < p.co) {
+                SMMC_CHECK_RANGE((int64_t)kk * p.co + co, 4, (int64_t)p.k * p.co);
+                v = __ldg(reinterpret_cast<const float4*>(p.w + (int64_t)kk * p.co + co));
+            }
+            SMMC_CHECK_SMEM(smem_u32(s_w), smem_u32(s_w + kk * BN + wslot(q * 4)), 16);
+            *reinterpret_cast<float4*>(s_w + kk * BN + wslot(q * 4)) = v;
+        }
+    }
+    __syncthreads();
+
+    const int lane = tid & 31;
+    const int cg = lane % NG;
+    int pg = blockIdx.x * PGC + (tid >> 5) * PGW + lane / NG;
+    if (pg >= p.pg_total) return;  // no CTA barrier below
+    // (n, orow, gcol) of this thread's tile, advanced by the grid stride
+    const int stride = gridDim.x * PGC;
+    const int st_n = stride / p.ohgpr;
+    const int st_rem = stride - st_n * p.ohgpr;
+    const int st_row = st_rem / p.gpr;
+    const int st_col = st_rem - st_row * p.gpr;
+    int n = pg / p.ohgpr;
+    int orow, gcol;
+    {
+        const int rem = pg - n * p.ohgpr;
+        orow = rem / p.gpr;
+        gcol = rem - orow * p.gpr;
+    }
+    const float* wcg = s_w + cg * 4;
+    const int64_t plane = (int64_t)p.h * p.w_in;
+#ifdef SMMC_CHECKED
+    const int64_t x_elems = (int64_t)p.n * p.c_i * plane;
+#endif
+
+    constexpr int NS = WIN - 4 * NV4;  // scalars per window (head + tail)
+    // ASYNC staging: quads [R][NV4][T] float4, then scalars [R][NS][T] float
+    float* s_q = s_w + ((p.k * BN + 3) & ~3);
+    float* s_s = s_q + R * NV4 * T * 4;
+    auto stage_row = [&](int r, int tn, int trow, int tcol, bool on) {
+        const int c = r / KH, kh = r - c * KH;
+        const int ih = trow * p.sh - p.ph + kh;
+        const int iw0 = tcol * (PX * SW) - p.pw;
+        const bool row_in = on && (unsigned)ih < (unsigned)p.h;
+        const float* xr = p.x + ((int64_t)tn * p.c_i + c) * plane + (int64_t)(row_in ? ih : 0) * p.w_in + iw0;
+#pragma unroll
+        for (int i = 0; i < NV4; ++i) {
+            const bool ok = row_in && (unsigned)(iw0 + HEAD + 4 * i) < (unsigned)p.w_in;
+            const float* src = ok ? xr + HEAD + 4 * i : p.x;
+#ifdef SMMC_CHECKED
+            if (ok) SMMC_CHECK_RANGE(src - p.x, 4, x_elems);
+            SMMC_CHECK_SMEM(smem_u32(s_w), smem_u32(s_q + ((r * NV4 + i) * T + tid) * 4), 16);
+#endif
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
+                             smem_u32(s_q + ((r * NV4 + i) * T + tid) * 4)),
+                         "l"(src), "r"(ok ? 16 : 0)
+                         : "memory");
+        }
+#pragma unroll
+        for (int j = 0; j < NS; ++j) {
+            const int t = j < HEAD ? j : 4 * NV4 + j;
+            const bool ok = row_in && (unsigned)(iw0 + t) < (unsigned)p.w_in;
+            const float* src = ok ? xr + t : p.x;
+#ifdef SMMC_CHECKED
+            if (ok) SMMC_CHECK_RANGE(src - p.x, 1, x_elems);
+            SMMC_CHECK_SMEM(smem_u32(s_w), smem_u32(s_s + (r * NS + j) * T + tid), 4);
+#endif
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(
+                             smem_u32(s_s + (r * NS + j) * T + tid)),
+                         "l"(src), "r"(ok ? 4 : 0)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    auto read_row = [&](int r, float (&w)[WIN]) {
+#pragma unroll
+        for (int i = 0; i < NV4; ++i) {
+            const float4 v = *reinterpret_cast<const float4*>(s_q + ((r * NV4 + i) * T + tid) * 4);
+            w[HEAD + 4 * i] = v.x;
+            w[HEAD + 4 * i + 1] = v.y;
+            w[HEAD + 4 * i + 2] = v.z;
+            w[HEAD + 4 * i + 3] = v.w;
+        }
+#pragma unroll
+        for (int j = 0; j < NS; ++j) w[j < HEAD ? j : 4 * NV4 + j] = s_s[(r * NS + j) * T + tid];
+    };
+
+    float win[ASYNC ? 1 : R][WIN];
+    // row r of tile (tn, trow, tcol): zero padding and `on` are load predicates
+    auto load_win = [&](int r, int tn, int trow, int tcol, bool on) {
+        const int c = r / KH, kh = r - c * KH;
+        const int ih = trow * p.sh - p.ph + kh;
+        const int iw0 = tcol * (PX * SW) - p.pw;
+        const bool row_in = on && (unsigned)ih < (unsigned)p.h;
+        const float* xr = p.x + ((int64_t)tn * p.c_i + c) * plane + (int64_t)(row_in ? ih : 0) * p.w_in + iw0;
+#pragma unroll
+        for (int t = 0; t < HEAD; ++t) {
+            const bool ok = row_in && (unsigned)(iw0 + t) < (unsigned)p.w_in;
+#ifdef SMMC_CHECKED
+            if (ok) SMMC_CHECK_RANGE(xr + t - p.x, 1, x_elems);
+#endif
+            win[ASYNC ? 0 : r][t] = ok ? __ldg(xr + t) : 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < NV4; ++i) {
+            // rows are whole float4s: a quad is entirely inside or outside
+            const bool ok = row_in && (unsigned)(iw0 + HEAD + 4 * i) < (unsigned)p.w_in;
+#ifdef SMMC_CHECKED
+            if (ok) SMMC_CHECK_RANGE(xr + HEAD + 4 * i - p.x, 4, x_elems);
+            if (ok) SMMC_ASSERT((reinterpret_cast<uintptr_t>(xr + HEAD + 4 * i) & 15) == 0);
+#endif
+            const float4 v = ok ? __ldg(reinterpret_cast<const float4*>(xr + HEAD + 4 * i))
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+            win[ASYNC ? 0 : r][HEAD + 4 * i] = v.x;
+            win[ASYNC ? 0 : r][HEAD + 4 * i + 1] = v.y;
+            win[ASYNC ? 0 : r][HEAD + 4 * i + 2] = v.z;
+            win[ASYNC ? 0 : r][HEAD + 4 * i + 3] = v.w;
+        }
+#pragma unroll
+        for (int t = HEAD + 4 * NV4; t < WIN; ++t) {
+            const bool ok = row_in && (unsigned)(iw0 + t) < (unsigned)p.w_in;
+#ifdef SMMC_CHECKED
+            if (ok) SMMC_CHECK_RANGE(xr + t - p.x, 1, x_elems);
+#endif
+            win[ASYNC ? 0 : r][t] = ok ? __ldg(xr + t) : 0.f;
+        }
+        (void)TAIL;
+    };
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        if constexpr (ASYNC) stage_row(r, n, orow, gcol, true);
+        else load_win(r, n, orow, gcol, true);
+    }
+
+    const int64_t ohw = (int64_t)p.oh * p.ow;
+#pragma unroll 1
+    while (true) {
+        // the tile after this one
+        int n2 = n + st_n, row2 = orow + st_row, col2 = gcol + st_col;
+        if (col2 >= p.gpr) { col2 -= p.gpr; ++row2; }
+        if (row2 >= p.oh) { row2 -= p.oh; ++n2; }
+        const bool has_next = n2 < p.n;
+        const int ow0 = gcol * PX;
+        const bool vec = PX % 4 == 0 && (p.ow & 3) == 0 && ow0 + PX <= p.ow;
+        float* yrow = p.y + ((int64_t)n * p.co) * ohw + (int64_t)orow * p.ow + ow0;
+#pragma unroll
+        for (int ps = 0; ps < NP; ++ps) {
+            uint64_t acc[PX][CP];
+#pragma unroll
+            for (int i = 0; i < PX; ++i)
+#pragma unroll
+                for (int q = 0; q < CP; ++q) acc[i][q] = 0ull;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int c = r / KH, kh = r - c * KH;
+                // W_smm row of tap (c, j = kw, k = kh): (c*KW + kw)*KH + kh
+                const float* wr = wcg + ps * BNP + ((c * KW) * KH + kh) * BN;
+                float wrow[ASYNC ? WIN : 1];
+                if constexpr (ASYNC) {
+                    // groups complete in order: row r of this tile has landed once at
+                    // most the groups committed after it are pending (NP == 1: the
+                    // next tile's rows 0..r-1 are already behind it, R-1 in all)
+                    if (ps == 0) cp_async_wait_pending(NP == 1 ? R - 1 : R - 1 - r);
+                    read_row(r, wrow);
+                }
+#pragma unroll
+                for (int kw = 0; kw < KW; ++kw) {
+                    uint64_t wp[CP];
+#pragma unroll
+                    for (int q = 0; q < CP; q += 2) {
+                        const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(
+                            wr + kw * KH * BN + (q >> 1) * (4 * NG));
+                        wp[q] = v.x;
+                        wp[q + 1] = v.y;
+                    }
+#pragma unroll
+                    for (int px = 0; px < PX; ++px)
+#pragma unroll
+                        for (int q = 0; q < CP; ++q)
+                            acc[px][q] = ffma2_bcast(ASYNC ? wrow[px * SW + kw] : win[ASYNC ? 0 : r][px * SW + kw],
+                                                     wp[q], acc[px][q]);
+                }
+                // last pass: row r's window is dead -- refill it for the next tile
+                if (ps == NP - 1) {
+                    if constexpr (ASYNC) stage_row(r, n2, row2, col2, has_next);
+                    else load_win(r, n2, row2, col2, has_next);
+                }
+            }
+            // NCHW, PX consecutive columns per channel.  Whole tile inside the
+            // tensor and 16-byte rows: straight-line STG.128s off one base.
+            const int co0 = co_base + ps * BNP + cg * CPT;
+            if (vec && co_base + BN <= p.co) {
+                float* d = yrow + (int64_t)co0 * ohw;
+                SMMC_CHECK_RANGE(d - p.y + (int64_t)(CPT - 1) * ohw, PX, (int64_t)p.n * p.co * ohw);
+                const uint32_t ohw32 = (uint32_t)ohw;  // one plane < 2^31 floats (checked at launch)
+#pragma unroll
+                for (int q = 0; q < CP; ++q) {
+#pragma unroll
+                    for (int h2 = 0; h2 < 2; ++h2) {
+                        float* dst = d + (size_t)((2 * q + h2) * ohw32);
+#pragma unroll
+                        for (int v4 = 0; v4 < PX / 4; ++v4) {
+                            float v[4];
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const uint64_t a = acc[4 * v4 + e][q];
+                                v[e] = __uint_as_float(h2 ? (uint32_t)(a >> 32) : (uint32_t)a);
+                            }
+                            reinterpret_cast<float4*>(dst)[v4] = make_float4(v[0], v[1], v[2], v[3]);
+                        }
+                    }
+                }
+            } else {
+#pragma unroll 1
+                for (int q = 0; q < CP; ++q) {
+#pragma unroll 1
+                    for (int h2 = 0; h2 < 2; ++h2) {
+                        const int co = co0 + 2 * q + h2;
+                        if (co >= p.co) continue;
+                        float* dst = yrow + (int64_t)co * ohw;
+                        SMMC_CHECK_RANGE(dst - p.y, min(PX, p.ow - ow0), (int64_t)p.n * p.co * ohw);
+#pragma unroll
+                        for (int px = 0; px < PX; ++px) {
+                            // acc[px][q] with a runtime q: select through the unrolled pairs
+                            uint64_t a = 0;
+#pragma unroll
+                            for (int qq = 0; qq < CP; ++qq) a = qq == q ? acc[px][qq] : a;
+                            if (ow0 + px < p.ow)
+                                dst[px] = __uint_as_float(h2 ? (uint32_t)(a >> 32) : (uint32_t)a);
+                        }
+                    }
+                }
+            }
+        }
+        if (!has_next) break;
+        n = n2;
+        orow = row2;
+        gcol = col2;
+    }
+}
+
+template <int KH, int KW, int SW, int PX, int CPT, int NG, int NP, int T, int MINB, int CI, int VOFF, int ASYNC>
+constexpr size_t stem_rw_smem(int k) {
+    constexpr int WIN = (PX - 1) * SW + KW;
+    return (((size_t)k * CPT * NG * NP + 3) & ~(size_t)3) * sizeof(float) +
+           (ASYNC ? (size_t)CI * KH * WIN * T * sizeof(float) : 0);
+}
+
+template <int KH, int KW, int SW, int PX, int CPT, int NG, int NP, int T, int MINB, int CI, int VOFF, int ASYNC>
+bool stem_rw_eligible(const StemParams& sp) {
+    static_assert((PX * SW) % 4 == 0, "window starts must step by whole float4s");
+    return sp.c_i == CI && (sp.w_in & 3) == 0 && (reinterpret_cast<uintptr_t>(sp.x) & 15) == 0 &&
+           sp.pw < 4 && ((-sp.pw) & 3) == VOFF && (sp.co & 3) == 0 &&
+           (int64_t)sp.oh * sp.ow * CPT < (1ll << 31) &&
+           stem_rw_smem<KH, KW, SW, PX, CPT, NG, NP, T, MINB, CI, VOFF, ASYNC>(sp.k) <= kStemMaxSmem;
+}
+
+template <int KH, int KW, int SW, int PX, int CPT, int NG, int NP, int T, int MINB, int CI, int VOFF, int ASYNC>
+cudaError_t launch_stem_rw(StemParams sp, cudaStream_t s) {
+    sp.gpr = (sp.ow + PX - 1) / PX;
+    sp.ohgpr = sp.oh * sp.gpr;
+    sp.pg_total = sp.n * sp.ohgpr;
+    constexpr int BN = CPT * NG * NP;
+    constexpr int PGC = (T / 32) * (32 / NG);
+    const size_t smem = stem_rw_smem<KH, KW, SW, PX, CPT, NG, NP, T, MINB, CI, VOFF, ASYNC>(sp.k);
+    auto kern = conv_stem_rw_kernel<KH, KW, SW, PX, CPT, NG, NP, T, MINB, CI, VOFF, ASYNC>;
+    const cudaError_t attr = smem_optin(kern, (int)kStemMaxSmem);
+    if (attr != cudaSuccess) return attr;
+    dim3 grid((sp.pg_total + PGC - 1) / PGC, (sp.co + BN - 1) / BN);
+    int occ = 0, dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T, smem) == cudaSuccess && occ > 0)
+        grid.x = std::max(1u, std::min(grid.x, (unsigned)(sms * occ) / grid.y));
+    kern<<<grid, T, smem, s>>>(sp);
+    return cudaGetLastError();
+}
+
 }  // namespace
+
+// Resident-window tile of the 3x3 s1 c_i = 3 stem (conv_stem_rw_kernel):
+// PX x CPT per thread, NG channel groups per warp, NP passes, T threads, MINB CTAs/SM.
+#ifndef RW1_PX
+#define RW1_PX 4
+#define RW1_CPT 16
+#define RW1_NG 2
+#define RW1_NP 2
+#define RW1_T 384
+#define RW1_MINB 1
+#define RW1_ASYNC 0
+#endif
 
 // Thread tiles (PX pixels x CPT channels, NG channel groups per warp, T
 // threads, MINB CTAs/SM, PF pipelined windows), measured on B200
@@ -406,7 +775,14 @@ cudaError_t launch_stem(const Problem& p, int kind, cudaStream_t s) {
         // tiled 71.6)
         // 3x3 s1 windows as float4s (w_in % 4 == 0): 370.0 -> 368.0 us; the
         // 7x7 s2 stem measured slower with them (53.3 -> 56.0 us), scalar there
-        case 1: e = launch_stem_t<3, 3, 1, SV1_PX, SV1_CPT, SV1_NG, SV1_T, SV1_MINB, SV1_PF, SV1_G, 3, 3>(sp, s); break;
+        case 1:
+            // resident windows, NP channel passes, cross-tile prefetch (3x3 s1 p1, c_i = 3, aligned rows)
+            if (stem_rw_eligible<3, 3, 1, RW1_PX, RW1_CPT, RW1_NG, RW1_NP, RW1_T, RW1_MINB, 3, 3, RW1_ASYNC>(sp) &&
+                !getenv("SMMC_STEM_RW0"))  // A/B hook: round-1 kernel
+                e = launch_stem_rw<3, 3, 1, RW1_PX, RW1_CPT, RW1_NG, RW1_NP, RW1_T, RW1_MINB, 3, 3, RW1_ASYNC>(sp, s);
+            else
+                e = launch_stem_t<3, 3, 1, SV1_PX, SV1_CPT, SV1_NG, SV1_T, SV1_MINB, SV1_PF, SV1_G, 3, 3>(sp, s);
+            break;
         case 2: e = launch_stem_t<7, 7, 2, SV2_PX, SV2_CPT, SV2_NG, SV2_T, SV2_MINB, SV2_PF, SV2_G>(sp, s); break;
         case 3: e = launch_stem_t<11, 11, 4, SV3_PX, SV3_CPT, SV3_NG, SV3_T, SV3_MINB, SV3_PF, SV3_G>(sp, s); break;
         default: return cudaErrorInvalidConfiguration;

@@ -120,3 +120,54 @@ def test_other_small_channel_layers_stay_on_the_tiled_kernel():
     for gt in [(3, 16, 20, 20, 5, 5, 1, 1, 2, 2), (5, 64, 40, 40, 7, 7, 2, 2, 3, 3),
                (8, 64, 40, 40, 3, 3, 1, 1, 1, 1), (3, 16, 20, 20, 3, 3, 1, 2, 1, 1)]:
         assert "direct stem" not in _native.plan_describe(ConvGeometry(*gt), 2), gt
+
+
+# c_i = 3, 3x3 s1 p_w = 1 layers with 16-byte rows run the resident-window
+# kernel (conv_stem_rw_kernel: channel passes over one window set, cross-tile
+# prefetch, strided tile walk): tile tails in every dimension of that walk.
+RW_CASES = [
+    # (c_i, c_o, h, w, kh, kw, sh, sw, ph, pw), n
+    ((3, 64, 224, 224, 3, 3, 1, 1, 1, 1), 2),   # VGG conv1_1, two samples (n carry)
+    ((3, 64, 12, 16, 3, 3, 1, 1, 1, 1), 5),     # fewer tiles than threads in the grid
+    ((3, 16, 20, 8, 3, 3, 1, 1, 1, 1), 3),      # c_o < one pass: scalar epilogue
+    ((3, 40, 9, 12, 3, 3, 1, 1, 1, 1), 2),      # c_o tail inside the second pass
+    ((3, 132, 10, 20, 3, 3, 1, 1, 0, 1), 2),    # three channel tiles, no row padding
+    ((3, 64, 7, 4, 3, 3, 2, 1, 1, 1), 4),       # one column group per row, s_h = 2
+    ((3, 128, 64, 256, 3, 3, 1, 1, 1, 1), 1),   # wide rows, two channel tiles
+    ((3, 64, 1, 36, 3, 3, 1, 1, 1, 1), 7),      # 1-row planes: every window row is padding but one
+]
+
+
+@pytest.mark.parametrize("gt,n", RW_CASES, ids=lambda v: str(v))
+def test_resident_window_stem_matches_oracle_and_round1_kernel(gt, n, monkeypatch):
+    import torch
+    g = ConvGeometry(*gt)
+    assert "direct stem" in _native.plan_describe(g, n)
+    x, w, xd, wd, device = _run(g, n, 23)
+    y1 = device.conv2d(xd, wd, g)
+    y2 = device.conv2d(xd, wd, g)
+    monkeypatch.setenv("SMMC_STEM_RW0", "1")   # the round-1 stem kernel: same (c, kh, kw) order
+    y0 = device.conv2d(xd, wd, g)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+    assert torch.equal(y1, y0), "resident-window kernel differs from the round-1 stem kernel"
+    ref = orc.smm_conv_c(x, orc.repack(w), g, threads=orc.host_threads())
+    assert orc.max_abs_ratio(y1.cpu().numpy(), ref) <= TOL_FP32
+
+
+def test_resident_window_stem_large_batch_linearity():
+    """Whole conv1_1 batch of config 4 at a reduced N: conv(2x) == 2 conv(x)
+    exactly and every sample equals sample-by-sample launches (the strided
+    walk crosses samples)."""
+    import torch
+    from paper_2411_15659_b200 import device
+    g = ConvGeometry(3, 64, 224, 224, 3, 3, 1, 1, 1, 1)
+    x, w = synthetic_layer(g, 16, 5)
+    wd = torch.from_numpy(smm.repack_weights(w, g)).cuda()
+    xd = torch.from_numpy(x).cuda()
+    y = device.conv2d(xd, wd, g)
+    y2 = device.conv2d(2 * xd, wd, g)
+    assert torch.equal(y2, 2 * y)
+    for i in (0, 7, 15):
+        yi = device.conv2d(xd[i:i + 1].contiguous(), wd, g)
+        assert torch.equal(yi[0], y[i])

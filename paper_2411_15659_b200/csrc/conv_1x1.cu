@@ -29,13 +29,24 @@ namespace {
 
 constexpr int kBK = 16;
 constexpr int kRing = 4;
+// A warp = kLanePx pixel groups x kLaneCo channel groups.  8 x 4 (round 2;
+// was 4 x 8): a warp's STG.128 of one channel covers 8 quads = 128 contiguous
+// bytes, so a tile's 16 stores per thread are 4 full-line writes each instead
+// of 8 half-line ones -- ncu had the epilogue's address math waiting on the
+// stores' source registers (long-scoreboard, ~15 % of all samples on the
+// ResNet-50 64->256 layer).  Both LDS.128 fragments stay <= 128 distinct bytes.
+#ifndef SMMC_1X1_LANE_CO
+#define SMMC_1X1_LANE_CO 4
+#endif
+constexpr int kLaneCo = SMMC_1X1_LANE_CO;
+constexpr int kLanePx = 32 / kLaneCo;
 
 template <int BM, int BN, int THREADS, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB) conv1x1_persistent_kernel(const Problem p) {
     constexpr int TM = 8;
     constexpr int TPX = BM / TM, TCO = BN / 8;
-    static_assert(TPX * TCO == THREADS && TCO % 8 == 0 && TPX % 4 == 0, "thread tile");
-    constexpr int WCO = TCO / 8;
+    static_assert(TPX * TCO == THREADS && TCO % kLaneCo == 0 && TPX % kLanePx == 0, "thread tile");
+    constexpr int WCO = TCO / kLaneCo;
     constexpr int A_CHUNKS = kBK * BM / 4;   // 16-byte chunks per A stage
     constexpr int B_CHUNKS = kBK * BN / 4;
     static_assert(A_CHUNKS % THREADS == 0 && B_CHUNKS % THREADS == 0, "loader split");
@@ -46,8 +57,8 @@ __global__ void __launch_bounds__(THREADS, MINB) conv1x1_persistent_kernel(const
     float* Bs = smem + kRing * kBK * BM;       // [kRing][kBK][BN]
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int cg = (warp % WCO) * 8 + (lane & 7);
-    const int pg = (warp / WCO) * 4 + (lane >> 3);
+    const int cg = (warp % WCO) * kLaneCo + (lane % kLaneCo);
+    const int pg = (warp / WCO) * kLanePx + (lane / kLaneCo);
     const int KT = p.c / kBK;
     const int64_t tiles = p.tiles;
     // this CTA's tiles: blockIdx.x, +gridDim.x, ...; global block q of the
@@ -219,8 +230,8 @@ template <int BM, int BN, int THREADS, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB) conv1x1_wres_kernel(const Problem p) {
     constexpr int TM = 8;
     constexpr int TPX = BM / TM, TCO = BN / 8;
-    static_assert(TPX * TCO == THREADS && TCO % 8 == 0 && TPX % 4 == 0, "thread tile");
-    constexpr int WCO = TCO / 8;
+    static_assert(TPX * TCO == THREADS && TCO % kLaneCo == 0 && TPX % kLanePx == 0, "thread tile");
+    constexpr int WCO = TCO / kLaneCo;
     constexpr int A_CHUNKS = kBK * BM / 4;
     static_assert(A_CHUNKS % THREADS == 0, "loader split");
     constexpr int A_PER = A_CHUNKS / THREADS;
@@ -230,8 +241,8 @@ __global__ void __launch_bounds__(THREADS, MINB) conv1x1_wres_kernel(const Probl
     float* Ws = smem + kRing * kBK * BM;       // [K][BN]
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int cg = (warp % WCO) * 8 + (lane & 7);
-    const int pg = (warp / WCO) * 4 + (lane >> 3);
+    const int cg = (warp % WCO) * kLaneCo + (lane % kLaneCo);
+    const int pg = (warp / WCO) * kLanePx + (lane / kLaneCo);
     const int KT = p.c / kBK;
     const int n0 = blockIdx.y * BN;
     const int64_t mtiles = (p.m + BM - 1) / BM;

@@ -695,9 +695,9 @@ cudaError_t launch_stem_rw(StemParams sp, cudaStream_t s) {
 #define SV2_PX 8
 #define SV2_CPT 8
 #define SV2_NG 8
-#define SV2_T 128
-#define SV2_MINB 3
-#define SV2_PF true
+#define SV2_T 352
+#define SV2_MINB 1
+#define SV2_PF false
 #define SV2_G 1
 #endif
 #ifndef SV3_PX

@@ -6,9 +6,8 @@ sys_path_fix = __import__("sys").path.insert(0, str(__import__("pathlib").Path(_
 from pathlib import Path
 from paper_2411_15659_b200 import build as b
 V = {
- "m2a": ("SV2", (8,8,8,128,4,1,1)), "m2b": ("SV2", (8,8,8,256,2,1,1)),
- "m1a": ("SV1", (4,16,2,128,4,0,1)), "m1b": ("SV1", (4,16,2,256,2,0,1)),
- "m3a": ("SV3", (4,16,2,128,3,0,2)), "m3b": ("SV3", (4,16,2,128,2,1,2)),
+ "m2a": ("SV2", (8,8,8,352,1,1,1)), "m2b": ("SV2", (8,8,8,352,1,0,1)), "m2c": ("SV2", (8,8,4,352,1,1,1)),
+ "m2d": ("SV2", (8,8,4,384,1,1,1)), "m2e": ("SV2", (8,8,8,288,1,1,1)),
 }
 exe = b.nvcc()
 objs = [str(o) for o in sorted(Path("build/smmc").glob("*.o")) if o.stem != "conv_stem"]

@@ -53,6 +53,15 @@ namespace smmc {
 namespace {
 
 constexpr int kStages = 4;
+// A warp = kLanePx pixel groups x kLaneCo channel groups of 8 x 8 thread tiles.
+// 8 x 4 (round 2; round 1: 4 x 8): a warp's STG.128 of one channel covers 8
+// pixel quads = one full 128-byte line (was two half lines), the A fragment
+// LDS.128 reads 128 contiguous bytes and the B fragment 4 broadcast quads.
+#ifndef SMMC_LANE_CO
+#define SMMC_LANE_CO 4
+#endif
+constexpr int kLaneCo = SMMC_LANE_CO;
+constexpr int kLanePx = 32 / kLaneCo;
 
 #ifdef SMMC_PROBE_TL
 // Timing probe (A/B builds only, -DSMMC_PROBE_TL=1): per-CTA globaltimer
@@ -103,7 +112,7 @@ __global__ void __launch_bounds__(THREADS * G, (min_blocks<BM, BN, THREADS, G, M
     constexpr int TPX = BM / TM;           // pixel groups
     constexpr int TCO = BN / 8;            // channel groups (4 + 4 channels each)
     static_assert(TPX * TCO == THREADS, "thread tile must cover the CTA tile");
-    static_assert(TCO % 8 == 0 && TPX % 4 == 0, "warp = 4 pixel groups x 8 channel groups");
+    static_assert(TCO % kLaneCo == 0 && TPX % kLanePx == 0, "warp = kLanePx pixel groups x kLaneCo channel groups");
     static_assert(THREADS % BM == 0, "loader maps one pixel column per thread");
     constexpr int KSTEP = THREADS / BM;    // k rows apart for one thread's A loads
     constexpr int A_PER = BK * BM / THREADS;
@@ -140,9 +149,9 @@ __global__ void __launch_bounds__(THREADS * G, (min_blocks<BM, BN, THREADS, G, M
     }
     bool tl_first = true;
 #endif
-    constexpr int WCO = TCO / 8;
-    const int cg = (warp % WCO) * 8 + (lane & 7);
-    const int pg = (warp / WCO) * 4 + (lane >> 3);
+    constexpr int WCO = TCO / kLaneCo;
+    const int cg = (warp % WCO) * kLaneCo + (lane % kLaneCo);
+    const int pg = (warp / WCO) * kLanePx + (lane / kLaneCo);
 
     // ---- work decomposition.  Modes 0-2: one (tile, split) per CTA from the
     // 3-D grid.  Mode 3 (stream-K): CTA b walks iterations [b*I, (b+1)*I) of
@@ -675,8 +684,8 @@ __global__ void __launch_bounds__(THREADS * G, (min_blocks<BM, BN, THREADS, G, M
                     }
             }
             const int tw = t >> 5, tl = t & 31;
-            const int tcg = (tw % WCO) * 8 + (tl & 7);
-            const int tpg = (tw / WCO) * 4 + (tl >> 3);
+            const int tcg = (tw % WCO) * kLaneCo + (tl % kLaneCo);
+            const int tpg = (tw / WCO) * kLanePx + (tl / kLaneCo);
             const int ib = gq >> 3, j = gq & 7;
             const int co = n0 + (j >> 2) * (BN / 2) + tcg * 4 + (j & 3);
             const int pbase = m0 + ib * (BM / NQ) + tpg * 4;
@@ -816,8 +825,8 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
         const int g = (int)(r - tile * ng);
         // (thread, g) -> pixel quad and channel, as in the conv epilogue
         const int warp = t >> 5, lane = t & 31;
-        const int cg = (warp % ro.wco) * 8 + (lane & 7);
-        const int pg = (warp / ro.wco) * 4 + (lane >> 3);
+        const int cg = (warp % ro.wco) * kLaneCo + (lane % kLaneCo);
+        const int pg = (warp / ro.wco) * kLanePx + (lane / kLaneCo);
         const int ib = g >> 3, j = g & 7;
         const int tm = (int)(tile / ro.tiles_n);
         const int tn = (int)(tile - (int64_t)tm * ro.tiles_n);
@@ -1327,7 +1336,7 @@ cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
     ro.bm = pl.bm;
     ro.bn = pl.bn;
     ro.threads = pl.threads;
-    ro.wco = pl.bn / 64;
+    ro.wco = pl.bn / (8 * kLaneCo);
     ro.nq = kTiles[pl.variant].tm / 4;
     ro.tiles_n = pl.tiles_n;
     for (int o = 0; o < p.n_out; ++o) ro.ys[o] = p.ys[o];

@@ -727,12 +727,38 @@ int stem_kind(const smmc_geom& g) {
     return kind;
 }
 
+// Channels per CTA of the resident-window kernel: 64 (two passes of 32), 32 or
+// 16 -- the one that pads c_o least (ties: the widest).
+static int stem_rw_bn(int co) {
+    int best = 64, best_pad = (co + 63) / 64 * 64;
+    for (int bn : {32, 16}) {
+        const int pad = (co + bn - 1) / bn * bn;
+        if (pad < best_pad) best = bn, best_pad = pad;
+    }
+    return best;
+}
+
+// Geometry part of the resident-window eligibility (the launch also needs a
+// 16-byte aligned input pointer).
+static bool stem_rw_geom(const smmc_geom& g) {
+    return g.c_i == 3 && g.k_h == 3 && g.k_w == 3 && g.s_w == 1 && g.p_w == 1 && (g.w & 3) == 0 &&
+           (g.c_o & 3) == 0 && !getenv("SMMC_STEM_RW0");
+}
+
 int stem_bn(const smmc_geom& g, int kind) {
-    (void)g;
+    if (kind == 1 && stem_rw_geom(g)) return stem_rw_bn(g.c_o);
     return kind == 1 ? SV1_CPT * SV1_NG : kind == 2 ? SV2_CPT * SV2_NG : SV3_CPT * SV3_NG;
 }
 
-int stem_describe(int kind, char* buf, size_t len) {
+int stem_describe(const smmc_geom& geom, int kind, char* buf, size_t len) {
+    if (kind == 1 && stem_rw_geom(geom)) {
+        const int bn = stem_rw_bn(geom.c_o);
+        return snprintf(buf, len,
+                        "ffma: direct stem kernel (weights in smem, resident register windows refilled "
+                        "for the next tile), %d px x %d c_o per thread, %d c_o per CTA in %d pass(es), %d "
+                        "threads, %d CTA/SM, split_k=1 (reduce=none)",
+                        RW1_PX, RW1_CPT, bn, bn == 64 ? RW1_NP : 1, RW1_T, RW1_MINB);
+    }
     int px, cpt, ng, t, minb, g;
     bool pf;
     switch (kind) {
@@ -775,14 +801,20 @@ cudaError_t launch_stem(const Problem& p, int kind, cudaStream_t s) {
         // tiled 71.6)
         // 3x3 s1 windows as float4s (w_in % 4 == 0): 370.0 -> 368.0 us; the
         // 7x7 s2 stem measured slower with them (53.3 -> 56.0 us), scalar there
-        case 1:
-            // resident windows, NP channel passes, cross-tile prefetch (3x3 s1 p1, c_i = 3, aligned rows)
-            if (stem_rw_eligible<3, 3, 1, RW1_PX, RW1_CPT, RW1_NG, RW1_NP, RW1_T, RW1_MINB, 3, 3, RW1_ASYNC>(sp) &&
-                !getenv("SMMC_STEM_RW0"))  // A/B hook: round-1 kernel
+        case 1: {
+            // resident windows, channel passes, cross-tile prefetch (3x3 s1 p_w = 1, c_i = 3,
+            // aligned rows); channels per CTA from the layer's c_o (least padding)
+            const int rw = getenv("SMMC_STEM_RW0") ? 0 : stem_rw_bn(sp.co);  // A/B hook: round-1 kernel
+            if (rw == 64 && stem_rw_eligible<3, 3, 1, RW1_PX, RW1_CPT, RW1_NG, RW1_NP, RW1_T, RW1_MINB, 3, 3, RW1_ASYNC>(sp))
                 e = launch_stem_rw<3, 3, 1, RW1_PX, RW1_CPT, RW1_NG, RW1_NP, RW1_T, RW1_MINB, 3, 3, RW1_ASYNC>(sp, s);
+            else if (rw == 32 && stem_rw_eligible<3, 3, 1, 4, 16, 2, 1, RW1_T, RW1_MINB, 3, 3, RW1_ASYNC>(sp))
+                e = launch_stem_rw<3, 3, 1, 4, 16, 2, 1, RW1_T, RW1_MINB, 3, 3, RW1_ASYNC>(sp, s);
+            else if (rw == 16 && stem_rw_eligible<3, 3, 1, 4, 16, 1, 1, RW1_T, RW1_MINB, 3, 3, RW1_ASYNC>(sp))
+                e = launch_stem_rw<3, 3, 1, 4, 16, 1, 1, RW1_T, RW1_MINB, 3, 3, RW1_ASYNC>(sp, s);
             else
                 e = launch_stem_t<3, 3, 1, SV1_PX, SV1_CPT, SV1_NG, SV1_T, SV1_MINB, SV1_PF, SV1_G, 3, 3>(sp, s);
             break;
+        }
         case 2: e = launch_stem_t<7, 7, 2, SV2_PX, SV2_CPT, SV2_NG, SV2_T, SV2_MINB, SV2_PF, SV2_G>(sp, s); break;
         case 3: e = launch_stem_t<11, 11, 4, SV3_PX, SV3_CPT, SV3_NG, SV3_T, SV3_MINB, SV3_PF, SV3_G>(sp, s); break;
         default: return cudaErrorInvalidConfiguration;

@@ -477,7 +477,7 @@ int smmc_plan_describe(const smmc_geom* g, int mode, char* buf, size_t len) {
     }
     const FfmaPlan pl = plan_ffma(*g, sm_count_for(current_device()));
     if (pl.stem) {
-        stem_describe(pl.stem, buf, len);
+        stem_describe(*g, pl.stem, buf, len);
         return SMMC_OK;
     }
     snprintf(buf, len,

@@ -144,7 +144,7 @@ constexpr size_t kStemMaxSmem = 200 * 1024;
 int stem_kind(const smmc_geom& g);
 int stem_bn(const smmc_geom& g, int kind);
 cudaError_t launch_stem(const Problem& p, int kind, cudaStream_t s);
-int stem_describe(int kind, char* buf, size_t len);
+int stem_describe(const smmc_geom& g, int kind, char* buf, size_t len);
 cudaError_t launch_conv1x1(const Problem& p, int bn, int sm_count, cudaStream_t s);
 int ffma_launches(const FfmaPlan& plan);
 // bf16 tensor-core variant (conv_tc.cu)

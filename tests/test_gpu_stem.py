@@ -135,6 +135,8 @@ RW_CASES = [
     ((3, 64, 7, 4, 3, 3, 2, 1, 1, 1), 4),       # one column group per row, s_h = 2
     ((3, 128, 64, 256, 3, 3, 1, 1, 1, 1), 1),   # wide rows, two channel tiles
     ((3, 64, 1, 36, 3, 3, 1, 1, 1, 1), 7),      # 1-row planes: every window row is padding but one
+    ((3, 96, 8, 16, 3, 3, 1, 1, 1, 1), 2),      # c_o = 96: three 32-channel CTAs, one pass each
+    ((3, 16, 416, 416, 3, 3, 1, 1, 1, 1), 1),   # YOLOv3-tiny conv1: one 16-channel group per warp
 ]
 
 

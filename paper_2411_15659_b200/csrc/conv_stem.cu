@@ -59,7 +59,14 @@ struct StemParams {
 };
 
 // T threads = (T/32) warps; a warp = (32/NG) pixel groups x NG channel groups.
-// PF: software-pipelined windows (row r+1 in flight while row r is consumed).
+// PF = 1: software-pipelined windows (row r+1 loaded into a second register
+// buffer while row r is consumed).  PF = D >= 2: the row windows go through a
+// D-deep PRIVATE per-thread ring in shared memory filled by cp.async (zero
+// padding = src-size 0), one commit group per row: row r+D-1 is in flight while
+// row r is consumed and `wait_group D-1` waits for exactly row r.  (The
+// register versions' loads share one scoreboard with the next row's, so the
+// first FMA of every row waited for the loads issued last -- ncu: 16-26 % of
+// all stall samples on that one FFMA2 of the 7x7 / 11x11 stems.)
 // G > 1: G groups of T threads share a tile, group g over the g-th 1/G of
 // the (c, kh) rows; partial tiles summed in group order through shared memory.
 // VOFF >= 0: interior windows start VOFF floats past a 16-byte boundary
@@ -68,7 +75,7 @@ struct StemParams {
 // CI > 0: c_i known at compile time (G == 1, unpipelined): all CI*KH row
 // windows are loaded before the first FMA (one round of loads in flight
 // instead of one per row).
-template <int KH, int KW, int SW, int PX, int CPT, int NG, int T, int MINB, bool PF, int G, int VOFF,
+template <int KH, int KW, int SW, int PX, int CPT, int NG, int T, int MINB, int PF, int G, int VOFF,
           int CI = 0>
 __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams p) {
     constexpr int BN = CPT * NG;
@@ -124,8 +131,10 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
     for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
     const int pg_raw = blk * PGC + (tid >> 5) * PGW + lane / NG;
     const bool active = pg_raw < p.pg_total;
-    if (G == 1 && !active) continue;
-    const int pg = active ? pg_raw : p.pg_total - 1;  // G > 1: stay for the barrier
+    constexpr bool kWarpRing = PF >= 10;  // warp-shared staging: a warp stays together
+    if (G == 1 && !kWarpRing && !active) continue;
+    if (G == 1 && kWarpRing && !__any_sync(0xffffffffu, active)) continue;
+    const int pg = active ? pg_raw : p.pg_total - 1;  // G > 1 / warp ring: stay for the barrier
     const int n = pg / p.ohgpr;
     const int rem = pg - n * p.ohgpr;
     const int orow = rem / p.gpr;
@@ -213,7 +222,140 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
         for (int r = 0; r < CI * KH; ++r) load_win(r, win[r]);
 #pragma unroll
         for (int r = 0; r < CI * KH; ++r) fma_row(r, win[r]);
-    } else if (PF) {
+    } else if constexpr (PF >= 10) {
+        // Warp-cooperative window ring: the PGW pixel groups of a warp need
+        // PGW x WQ aligned 16-byte chunks of an input row; lane l < PGW*WQ copies
+        // chunk l % WQ of pixel group l / WQ with ONE cp.async.cg (zero padding =
+        // src-size 0: rows are whole float4s, a chunk is inside or outside), so
+        // a row costs each thread at most one copy instead of WIN scalar loads
+        // repeated by the NG lanes that share a window; every lane then reads
+        // its group's WQ quads back (broadcast LDS.128).  D rows in flight.
+        static_assert(G == 1 && VOFF >= 0, "warp ring: one row group, aligned windows");
+        constexpr int D = PF - 10;
+        constexpr int WQ = (VOFF + WIN + 3) / 4;
+        constexpr int CH = PGW * WQ;
+        static_assert(CH <= 32, "one chunk per lane");
+        float4* ring = reinterpret_cast<float4*>(s_w + ((p.k * BN + 3) & ~3)) + (tid >> 5) * (D * CH);
+        // the pixel group this lane copies for: coordinates from its first lane
+        const int cpg = lane / WQ < PGW ? lane / WQ : 0, cch = lane - (lane / WQ) * WQ;
+        const int c_ih0 = __shfl_sync(0xffffffffu, ih0, cpg * NG);
+        const int c_iw0 = __shfl_sync(0xffffffffu, iw0, cpg * NG);
+        const int c_n = __shfl_sync(0xffffffffu, n, cpg * NG);
+        const float* c_xn = p.x + (int64_t)c_n * p.c_i * p.h * p.w_in;
+        const int c_col = c_iw0 - VOFF + 4 * cch;
+        const bool c_lane = lane < CH && (unsigned)c_col < (unsigned)p.w_in;
+        auto stage = [&](int r, int slot) {
+            const int c = r / KH, kh = r - c * KH;
+            const int ih = c_ih0 + kh;
+            const bool ok = c_lane && (unsigned)ih < (unsigned)p.h;
+            const float* src = ok ? c_xn + ((int64_t)c * p.h + ih) * p.w_in + c_col : p.x;
+#ifdef SMMC_CHECKED
+            if (ok) SMMC_CHECK_RANGE(src - p.x, 4, (int64_t)p.n * p.c_i * p.h * p.w_in);
+            if (lane < CH) SMMC_CHECK_SMEM(smem_u32(s_w), smem_u32(ring + slot * CH + lane), 16);
+#endif
+            if (lane < CH)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
+                                 smem_u32(ring + slot * CH + lane)),
+                             "l"(src), "r"(ok ? 16 : 0)
+                             : "memory");
+        };
+        int issued = r_begin, slot_w = 0, slot_r = 0;
+#pragma unroll
+        for (int d = 0; d < D - 1; ++d) {
+            if (issued < rows) stage(issued, slot_w);
+            asm volatile("cp.async.commit_group;\n" ::: "memory");
+            ++issued;
+            slot_w = slot_w == D - 1 ? 0 : slot_w + 1;
+        }
+#pragma unroll 1
+        for (int r = r_begin; r < rows; ++r) {
+            cp_async_wait_pending(D - 2);  // row r landed (this thread's copies)
+            __syncwarp();                  // ... and everyone's; row r-1's slot is free
+            if (issued < rows) stage(issued, slot_w);
+            asm volatile("cp.async.commit_group;\n" ::: "memory");
+            ++issued;
+            slot_w = slot_w == D - 1 ? 0 : slot_w + 1;
+            float win[WQ * 4];
+            const float4* src = ring + slot_r * CH + (lane / NG) * WQ;
+#pragma unroll
+            for (int q = 0; q < WQ; ++q) {
+                const float4 v = src[q];
+                win[4 * q] = v.x;
+                win[4 * q + 1] = v.y;
+                win[4 * q + 2] = v.z;
+                win[4 * q + 3] = v.w;
+            }
+            slot_r = slot_r == D - 1 ? 0 : slot_r + 1;
+            float wrow[WIN];
+#pragma unroll
+            for (int t = 0; t < WIN; ++t) wrow[t] = win[t + VOFF];
+            fma_row(r, wrow);
+        }
+        __syncwarp();  // the next tile's first copies reuse the slots
+    } else if constexpr (PF >= 2) {
+        constexpr int D = PF;
+        constexpr int WQ = (WIN + 3) / 4;   // float4s per row slice
+        constexpr int TT = T * G;
+        // ring [D][WQ][TT] float4 behind the weights and the group partials
+        float* ring = s_w + ((p.k * BN + 3) & ~3) + (G - 1) * PX * CP * T * 2;
+        auto stage = [&](int r, int slot) {
+            const int c = r / KH, kh = r - c * KH;
+            const int ih = ih0 + kh;
+            const bool row_in = (unsigned)ih < (unsigned)p.h;
+            const float* xr = xn + ((int64_t)c * p.h + (row_in ? ih : 0)) * p.w_in + iw0;
+            const uint32_t dst = smem_u32(ring + ((slot * WQ) * TT + tid_all) * 4);
+            const bool fast = __all_sync(__activemask(), row_in && cols_in);
+#ifdef SMMC_CHECKED
+            if (row_in && cols_in) SMMC_CHECK_RANGE(xr - p.x, WIN, (int64_t)p.n * p.c_i * p.h * p.w_in);
+            SMMC_CHECK_SMEM(smem_u32(s_w), dst + (WQ - 1) * TT * 16, 16);
+#endif
+            if (fast) {
+#pragma unroll
+                for (int t = 0; t < WIN; ++t)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(
+                                     dst + (t >> 2) * (TT * 16) + (t & 3) * 4),
+                                 "l"(xr + t)
+                                 : "memory");
+            } else {
+#pragma unroll
+                for (int t = 0; t < WIN; ++t) {
+                    const bool ok = row_in && (unsigned)(iw0 + t) < (unsigned)p.w_in;
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(
+                                     dst + (t >> 2) * (TT * 16) + (t & 3) * 4),
+                                 "l"(ok ? xr + t : p.x), "r"(ok ? 4 : 0)
+                                 : "memory");
+                }
+            }
+        };
+        int issued = r_begin, slot_w = 0, slot_r = 0;
+#pragma unroll
+        for (int d = 0; d < D - 1; ++d) {
+            if (issued < rows) stage(issued, slot_w);
+            asm volatile("cp.async.commit_group;\n" ::: "memory");
+            ++issued;
+            slot_w = slot_w == D - 1 ? 0 : slot_w + 1;
+        }
+#pragma unroll 1
+        for (int r = r_begin; r < rows; ++r) {
+            if (issued < rows) stage(issued, slot_w);
+            asm volatile("cp.async.commit_group;\n" ::: "memory");
+            ++issued;
+            slot_w = slot_w == D - 1 ? 0 : slot_w + 1;
+            cp_async_wait_pending(D - 1);
+            float win[WQ * 4];
+            const float4* src = reinterpret_cast<const float4*>(ring) + (slot_r * WQ) * TT + tid_all;
+#pragma unroll
+            for (int q = 0; q < WQ; ++q) {
+                const float4 v = src[q * TT];
+                win[4 * q] = v.x;
+                win[4 * q + 1] = v.y;
+                win[4 * q + 2] = v.z;
+                win[4 * q + 3] = v.w;
+            }
+            slot_r = slot_r == D - 1 ? 0 : slot_r + 1;
+            fma_row(r, reinterpret_cast<const float(&)[WIN]>(win));
+        }
+    } else if constexpr (PF == 1) {
         float wa[WIN], wb[WIN];
         int r = r_begin;
         if (r < rows) load_win(r, wa);
@@ -236,7 +378,7 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
 
     if (G > 1) {
         // groups 1..G-1 park their partial tiles; group 0 sums them in order
-        uint64_t* red = reinterpret_cast<uint64_t*>(s_w + p.k * BN);  // [G-1][PX*CP][T]
+        uint64_t* red = reinterpret_cast<uint64_t*>(s_w + ((p.k * BN + 3) & ~3));  // [G-1][PX*CP][T]
         if (grp > 0) {
 #pragma unroll
             for (int i = 0; i < PX; ++i)
@@ -260,7 +402,7 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
                 }
     }
     // epilogue: NCHW, PX consecutive columns per channel
-    if (G == 1 || (grp == 0 && active)) {
+    if ((G == 1 && (!kWarpRing || active)) || (G > 1 && grp == 0 && active)) {
     const int64_t ohw = (int64_t)p.oh * p.ow;
     const bool vec = PX % 4 == 0 && (p.ow & 3) == 0 && ow0 + PX <= p.ow;
     float* yrow = p.y + ((int64_t)n * p.co) * ohw + (int64_t)orow * p.ow + ow0;
@@ -295,7 +437,7 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
     }  // persistent block loop
 }
 
-template <int KH, int KW, int SW, int PX, int CPT, int NG, int T, int MINB, bool PF, int G, int VOFF = -1,
+template <int KH, int KW, int SW, int PX, int CPT, int NG, int T, int MINB, int PF, int G, int VOFF = -1,
           int CI = 0>
 cudaError_t launch_stem_t(StemParams sp, cudaStream_t s) {
     if constexpr (CI > 0) {
@@ -306,14 +448,19 @@ cudaError_t launch_stem_t(StemParams sp, cudaStream_t s) {
         static_assert((PX * SW) % 4 == 0, "window starts must step by whole float4s");
         const bool ok = (sp.w_in & 3) == 0 && (reinterpret_cast<uintptr_t>(sp.x) & 15) == 0 &&
                         ((-sp.pw) & 3) == VOFF && !getenv("SMMC_STEM_SCALAR");  // A/B hook
-        if (!ok) return launch_stem_t<KH, KW, SW, PX, CPT, NG, T, MINB, PF, G, -1, CI>(sp, s);
+        if (!ok) return launch_stem_t<KH, KW, SW, PX, CPT, NG, T, MINB, (PF >= 10 ? 0 : PF), G, -1, CI>(sp, s);
     }
     sp.gpr = (sp.ow + PX - 1) / PX;
     sp.ohgpr = sp.oh * sp.gpr;
     sp.pg_total = sp.n * sp.ohgpr;
     constexpr int BN = CPT * NG;
     constexpr int PGC = (T / 32) * (32 / NG);
-    const size_t smem = (size_t)sp.k * BN * sizeof(float) + (size_t)(G - 1) * PX * (CPT / 2) * T * 8;
+    constexpr int WIN = (PX - 1) * SW + KW;
+    const size_t smem = (((size_t)sp.k * BN + 3) & ~(size_t)3) * sizeof(float) +
+                        (size_t)(G - 1) * PX * (CPT / 2) * T * 8 +
+                        (PF >= 10 ? (size_t)(PF - 10) * (32 / NG) * (((VOFF > 0 ? VOFF : 0) + WIN + 3) / 4) * 16 * (T / 32)
+                         : PF >= 2 ? (size_t)PF * ((WIN + 3) / 4) * 16 * T * G
+                                   : 0);
     if (smem > kStemMaxSmem) return cudaErrorInvalidConfiguration;
     auto kern = conv_stem_kernel<KH, KW, SW, PX, CPT, NG, T, MINB, PF, G, VOFF, CI>;
     const cudaError_t attr = smem_optin(kern, (int)kStemMaxSmem);
@@ -760,7 +907,7 @@ int stem_describe(const smmc_geom& geom, int kind, char* buf, size_t len) {
                         RW1_PX, RW1_CPT, bn, bn == 64 ? RW1_NP : 1, RW1_T, RW1_MINB);
     }
     int px, cpt, ng, t, minb, g;
-    bool pf;
+    int pf;
     switch (kind) {
         case 1: px = SV1_PX, cpt = SV1_CPT, ng = SV1_NG, t = SV1_T, minb = SV1_MINB, pf = SV1_PF, g = SV1_G; break;
         case 2: px = SV2_PX, cpt = SV2_CPT, ng = SV2_NG, t = SV2_T, minb = SV2_MINB, pf = SV2_PF, g = SV2_G; break;
@@ -771,7 +918,8 @@ int stem_describe(const smmc_geom& geom, int kind, char* buf, size_t len) {
                     "ffma: direct stem kernel (weights in smem, register windows), %d px x %d c_o per "
                     "thread, %d c_o per CTA, %d threads (%d row groups), %d CTAs/SM, %s windows, "
                     "split_k=1 (reduce=none)",
-                    px, cpt, cpt * ng, t * g, g, minb, pf ? "pipelined" : "unpipelined");
+                    px, cpt, cpt * ng, t * g, g, minb,
+                    pf >= 2 ? "cp.async-ring" : pf ? "pipelined" : "unpipelined");
 }
 
 cudaError_t launch_stem(const Problem& p, int kind, cudaStream_t s) {
@@ -815,7 +963,7 @@ cudaError_t launch_stem(const Problem& p, int kind, cudaStream_t s) {
                 e = launch_stem_t<3, 3, 1, SV1_PX, SV1_CPT, SV1_NG, SV1_T, SV1_MINB, SV1_PF, SV1_G, 3, 3>(sp, s);
             break;
         }
-        case 2: e = launch_stem_t<7, 7, 2, SV2_PX, SV2_CPT, SV2_NG, SV2_T, SV2_MINB, SV2_PF, SV2_G>(sp, s); break;
+        case 2: e = launch_stem_t<7, 7, 2, SV2_PX, SV2_CPT, SV2_NG, SV2_T, SV2_MINB, SV2_PF, SV2_G, (SV2_PF >= 10 ? 1 : -1)>(sp, s); break;
         case 3: e = launch_stem_t<11, 11, 4, SV3_PX, SV3_CPT, SV3_NG, SV3_T, SV3_MINB, SV3_PF, SV3_G>(sp, s); break;
         default: return cudaErrorInvalidConfiguration;
     }

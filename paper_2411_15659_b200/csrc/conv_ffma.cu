@@ -1121,8 +1121,9 @@ static FfmaPlan plan_ffma_impl(const smmc_geom& g, int sm_count, bool allow_stem
     // measured-best plans for known shapes (tuning table), then the
     // SMMC_FORCE_PLAN="variant,splits" experiment hook (splits 0 = stream-K)
     int fv = -1, fs = -1, fg = 1, fr = 0;
+    const bool use_table = !getenv("SMMC_NO_TABLE");  // A/B hook: cost model / 1x1 kernel only
     for (const TunedPlan& e : kTuned) {
-        if (e.n == g.n && e.c_i == g.c_i && e.h == g.h && e.w == g.w && e.c_o == g.c_o &&
+        if (use_table && e.n == g.n && e.c_i == g.c_i && e.h == g.h && e.w == g.w && e.c_o == g.c_o &&
             e.k == g.k_h && g.k_w == g.k_h && e.s == g.s_h && g.s_w == g.s_h && e.p == g.p_h &&
             g.p_w == g.p_h) {
             fv = e.variant;

@@ -28,6 +28,13 @@ for l in vgg02_64to64@224_n64 vgg09_512to512@28_n64 vgg06_256to256@56_n64 vgg01_
      > $O/full_$l.log 2>&1
   echo "ncu $l rc=$?" >> $O/ncu_launch.log
 done
+for cl in 5:conv1x1_64to256@56_n256 3:conv7x7s2p3_3to64@224_n8 3:conv11x11s4_3to96@227_n8; do
+  c=${cl%%:*}; l=${cl#*:}
+  timeout 600 ncu --set full --import-source on --clock-control none -k regex:"conv" -c 1 \
+     -o $O/full_$l -f python tools/prof_layer.py --config $c --layer $l --iters 1 --graph 0 \
+     > $O/full_$l.log 2>&1
+  echo "ncu $l rc=$?" >> $O/ncu_launch.log
+done
 python tools/ncu_summary.py $O/full_*.ncu-rep > $O/ncu_summaries.txt 2>&1
 python tools/ncu_traffic.py $O/traffic.json $O/full_*.ncu-rep > $O/traffic.log 2>&1
 rm -f $O/*.ncu-rep

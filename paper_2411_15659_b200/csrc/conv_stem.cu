@@ -154,12 +154,15 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
     constexpr int NV = VOFF >= 0 ? (VOFF + WIN + 3) / 4 : 1;  // float4s per vector window
     // Scalar windows may run past the row end when the columns past it feed only
     // this thread's discarded output columns (ow0 + px >= ow, right-edge group
-    // of a row whose width is not a multiple of PX): they read the next row's
-    // floats, never zero padding -- except in the tensor's very last row.
+    // of a row whose width is not a multiple of PX): they read the following
+    // rows' floats, never zero padding -- unless the tile's last window would
+    // run past the end of the tensor (narrow planes: the overhang can span rows).
     const int px_valid = min(PX, p.ow - ow0);
+    const int64_t last_win = ((int64_t)(n * p.c_i + p.c_i - 1) * p.h + min(ih0 + KH - 1, p.h - 1)) * p.w_in + iw0;
     const bool cols_in = VOFF >= 0 ? iw0 - VOFF >= 0 && iw0 - VOFF + 4 * NV <= p.w_in
                                    : iw0 >= 0 && iw0 + (px_valid - 1) * SW + KW <= p.w_in &&
-                                         (iw0 + WIN <= p.w_in || n + 1 < p.n || ih0 + KH < p.h);
+                                         (iw0 + WIN <= p.w_in ||
+                                          last_win + WIN <= (int64_t)p.n * p.c_i * p.h * p.w_in);
     // one (c, kh) input row window; columns/rows in the zero padding read as 0
     auto load_win = [&](int r, float (&win)[WIN]) {
         const int c = r / KH, kh = r - c * KH;

@@ -60,6 +60,9 @@ def test_criterion5_vgg16_speedup_vs_im2col():
     GPU: the SMM kernel against im2col + cuBLAS SGEMM (TF32 off) per VGG-16
     layer at the reference harness's batch of 1: >= 80 % layer wins and a
     whole-network speedup >= 1.3x."""
+    import os
+    if "checked" in os.environ.get("SMMC_LIB", ""):
+        pytest.skip("timing criterion: not meaningful with the bounds-checked (device-assert) build")
     recs = H.run_bench(H.builtin_network("vgg16"), ["b200_im2col", "b200_smm"], repeats=3)
     im = {r.layer: r.median_time_s for r in recs if r.backend == "b200_im2col"}
     sm = {r.layer: r.median_time_s for r in recs if r.backend == "b200_smm"}

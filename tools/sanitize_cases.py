@@ -67,9 +67,15 @@ def main():
         ffma("ragged_co37", G(24, 37, 11, 9, 3), 3, {}),
         ffma("planner_default_n1", G(128, 128, 14, 14, 3), 1, {}),
         ffma("stem_3x3s1", G(3, 64, 20, 20, 3), 2, {}),
+        ffma("stem_3x3s1_round1", G(3, 64, 20, 20, 3), 2, {"SMMC_STEM_RW0": "1"}),
+        ffma("stem_3x3s1_rw_tail", G(3, 40, 12, 24, 3), 3, {}),
+        ffma("stem_3x3s1_rw_vgg", G(3, 64, 224, 224, 3), 1, {}),
         ffma("stem_3x3s1_scalar", G(3, 64, 18, 18, 3), 1, {"SMMC_STEM_SCALAR": "1"}),
         ffma("stem_7x7s2", G(3, 64, 30, 30, 7, 2, 3), 2, {}),
         ffma("stem_11x11s4", G(3, 96, 43, 43, 11, 4, 0), 2, {}),
+        # narrow planes: a right-edge window's overhang spans rows (must not pass the tensor end)
+        ffma("stem_11x11s4_narrow", ConvGeometry(3, 33, 13, 11, 11, 11, 4, 4, 0, 0), 2, {}),
+        ffma("stem_7x7s2_narrow", ConvGeometry(2, 8, 9, 8, 7, 7, 2, 2, 3, 0), 3, {}),
         ffma("conv1x1_persistent", G(64, 64, 12, 12, 1, 1, 0), 2, {}),
         ffma("conv1x1_persistent_co128", G(32, 128, 8, 8, 1, 1, 0), 3, {}),
         ffma("conv1x1_tiled", G(64, 64, 12, 12, 1, 1, 0), 2, {"SMMC_1X1": "0"}),

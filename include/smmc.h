@@ -211,6 +211,21 @@ SMMC_API int smmc_im2col_pack_f32(const float* x, float* lowered, const smmc_geo
 /* Number of kernels smmc_conv2d_fwd_f32 launches for this problem/mode. */
 SMMC_API int smmc_plan_launches(const smmc_geom* g, int mode);
 
+/* Per-shape autotuning (no counterpart in the reference: its numba kernel has
+ * one schedule, smm.py:254-306).  smmc_autotune_f32 times the candidate kernel
+ * plans of geometry g (its n included) on the current device -- in-kernel-split
+ * grids sized to the SM count, stream-K, the tiled kernel for stem / 1x1 layers
+ * -- with scratch operands it allocates itself, `iters` launches per candidate,
+ * and keeps the fastest for the rest of the process when it beats the default
+ * plan by more than 3 %: later smmc_conv2d_fwd_f32 / smmc_workspace_bytes /
+ * smmc_plan_describe calls for the same geometry use it (call it BEFORE sizing a
+ * workspace or creating a layer).  Every candidate is one of the parity-tested
+ * plan kinds; results stay within the fp32 bar and deterministic for a fixed
+ * choice.  `report` (optional) receives a one-line summary.
+ * smmc_autotune_clear forgets every recorded choice. */
+SMMC_API int smmc_autotune_f32(const smmc_geom* g, int iters, char* report, size_t report_len);
+SMMC_API int smmc_autotune_clear(void);
+
 /* Short human-readable description of the kernel plan (tile, split-K). */
 SMMC_API int smmc_plan_describe(const smmc_geom* g, int mode, char* buf, size_t len);
 

@@ -46,6 +46,7 @@ EXPORTED_SYMBOLS = (
     "smmc_ipc_open", "smmc_ipc_close", "smmc_host_alloc_pinned", "smmc_host_free_pinned",
     "smmc_layer_create", "smmc_layer_forward_host", "smmc_layer_destroy",
     "smmc_layer_forward_host_async", "smmc_layer_wait",
+    "smmc_autotune_f32", "smmc_autotune_clear",
 )
 
 SMMC_MAX_OUT = 8
@@ -103,6 +104,8 @@ _SIGNATURES = {
     "smmc_plan_describe": (ctypes.c_int, [_GP, ctypes.c_int, ctypes.c_char_p,
                                           ctypes.c_size_t]),
     "smmc_launch_count": (ctypes.c_uint64, []),
+    "smmc_autotune_f32": (ctypes.c_int, [_GP, ctypes.c_int, ctypes.c_char_p, ctypes.c_size_t]),
+    "smmc_autotune_clear": (ctypes.c_int, []),
     "smmc_tc_plan_describe": (ctypes.c_int, [_GP, ctypes.c_char_p, ctypes.c_size_t]),
     "smmc_tc_supported": (ctypes.c_int, [_GP]),
     "smmc_pack_input_bf16_nhwc": (ctypes.c_int, [_P, _P, _GP, _P]),
@@ -191,6 +194,26 @@ def plan_describe(geom, batch=1, mode="ffma"):
     check(lib().smmc_plan_describe(ctypes.byref(g), mode_id(mode), buf, 256),
           "smmc_plan_describe")
     return buf.value.decode()
+
+
+def autotune(geom, batch=1, iters=10):
+    """Measure the candidate kernel plans of (geom, batch) on the current device
+    and keep the fastest for this process (smmc_autotune_f32); returns the
+    library's one-line report.  Call before sizing workspaces for the shape."""
+    buf = ctypes.create_string_buffer(256)
+    g = Geom.of(geom, batch)
+    check(lib().smmc_autotune_f32(ctypes.byref(g), int(iters), buf, 256), "smmc_autotune_f32")
+    return buf.value.decode()
+
+
+def autotune_clear():
+    check(lib().smmc_autotune_clear(), "smmc_autotune_clear")
+
+
+def autotune_enabled():
+    """SMMC_AUTOTUNE=1 turns per-shape autotuning on wherever a layer is fitted
+    (device.SmmConv2d, the estimator, the harness backends)."""
+    return os.environ.get("SMMC_AUTOTUNE", "0") not in ("", "0")
 
 
 def tc_plan_describe(geom, batch=1):

@@ -47,6 +47,10 @@
 
 #include <cooperative_groups.h>
 
+#include <array>
+#include <map>
+#include <mutex>
+
 #include "smmc_internal.cuh"
 
 namespace smmc {
@@ -1015,6 +1019,16 @@ constexpr TunedPlan kTuned[] = {
     {8, 256, 56, 56, 64, 1, 1, 0, 4, 1, 2},    // 25.5 us (persistent 1x1 kernel: 26.8)
 };
 
+// ---- measured plan choices (autotuner, smmc_autotune_f32)
+thread_local bool tl_force_on = false;
+thread_local PlanChoice tl_force{};
+std::mutex g_rec_mu;
+using GeomKey = std::array<int, 11>;
+std::map<GeomKey, PlanChoice> g_recorded;
+GeomKey geom_key(const smmc_geom& g) {
+    return {g.n, g.c_i, g.h, g.w, g.c_o, g.k_h, g.k_w, g.s_h, g.s_w, g.p_h, g.p_w};
+}
+
 int64_t best_cost_waves(const FfmaPlan& b, int64_t m, int c_o, int sm_count) {
     const int per_sm = kTiles[b.variant].per_sm;
     const int64_t tiles = ((m + b.bm - 1) / b.bm) * ((c_o + b.bn - 1) / b.bn);
@@ -1027,7 +1041,7 @@ int64_t best_cost_waves(const FfmaPlan& b, int64_t m, int c_o, int sm_count) {
 // to per_sm * BM * BN * (work per CTA in 8-deep tap blocks, plus a prologue /
 // epilogue term and ~3 blocks of partial-tile traffic when split), with a
 // small per-split overhead.
-static FfmaPlan plan_ffma_impl(const smmc_geom& g, int sm_count, bool allow_stem) {
+static FfmaPlan plan_ffma_impl(const smmc_geom& g, int sm_count, bool allow_stem) {  // NOLINT
     FfmaPlan best{};
     double best_cost = 1e300;
     const int oh = (g.h + 2 * g.p_h - g.k_h) / g.s_h + 1;
@@ -1144,6 +1158,29 @@ static FfmaPlan plan_ffma_impl(const smmc_geom& g, int sm_count, bool allow_stem
             env_forced = true;
         }
     }
+    // a plan pinned by the autotuner for this thread, else the measured winner
+    // recorded for this geometry (not for the replicated-output gather plans)
+    {
+        PlanChoice pc{};
+        bool have = false;
+        if (tl_force_on) {
+            pc = tl_force;
+            have = true;
+        } else if (!env_forced && allow_stem) {
+            have = plan_recorded(g, &pc);
+        }
+        if (have) {
+            fv = pc.variant;
+            fs = pc.splits;
+            fg = pc.groups;
+            fr = pc.reduce;
+            env_forced = true;
+            if (fv < 0) {  // "tiled kernel, cost-model plan" (no_stem only)
+                fs = -1;
+                allow_stem = false;
+            }
+        }
+    }
     if (fv == 4 && (!cvec || fs == 0)) fv = -1;  // the 64x64 tile: tap-major split grids only
     // warp groups: tap-major blocks, classic split grid, instantiated
     // (variant, G) pairs only
@@ -1219,8 +1256,8 @@ static FfmaPlan plan_ffma_impl(const smmc_geom& g, int sm_count, bool allow_stem
     // c_i <= 4 stems: the direct register-window kernel (weights resident in
     // smem, no zero-packed A tiles); the tiled kernel stays the fallback for
     // the fused gather and for forced plans
-    if (allow_stem && !env_forced && stem_kind(g)) {
-        const int kind = stem_kind(g);
+    if (allow_stem && !env_forced && stem_kind(g, sm_count)) {
+        const int kind = stem_kind(g, sm_count);
         best = FfmaPlan{};
         best.bm = 128;  // nominal pixels per CTA (the stem kernel tiles rows itself)
         best.bn = stem_bn(g, kind);
@@ -1265,6 +1302,76 @@ void set_workspace_layout(FfmaPlan& b) {
 // needed, or one extra tiny) placement pass splitk_reduce_kernel writes the
 // replicas — local and NVLink peer memory — in split order.
 FfmaPlan plan_ffma(const smmc_geom& g, int sm_count) { return plan_ffma_impl(g, sm_count, true); }
+
+void plan_force(const PlanChoice* c) {
+    tl_force_on = c != nullptr;
+    if (c) tl_force = *c;
+}
+
+void plan_record(const smmc_geom& g, const PlanChoice* c) {
+    std::lock_guard<std::mutex> lk(g_rec_mu);
+    if (c)
+        g_recorded[geom_key(g)] = *c;
+    else
+        g_recorded.erase(geom_key(g));
+}
+
+void plan_record_clear() {
+    std::lock_guard<std::mutex> lk(g_rec_mu);
+    g_recorded.clear();
+}
+
+bool plan_recorded(const smmc_geom& g, PlanChoice* out) {
+    std::lock_guard<std::mutex> lk(g_rec_mu);
+    auto it = g_recorded.find(geom_key(g));
+    if (it == g_recorded.end()) return false;
+    if (out) *out = it->second;
+    return true;
+}
+
+// Candidates for the autotuner: in-kernel-split grids (reduce mode 5) of the
+// small tiles sized to about 0.5, 0.75, 1, 1.5 and 2 CTAs per SM with 2 or 4
+// warp groups, stream-K on two tiles, classic splits of the cost model's tile,
+// and the tiled kernel where the default is a stem / 1x1 kernel.
+int plan_candidates(const smmc_geom& g, int sm_count, PlanChoice* out, int max_out) {
+    const int oh = (g.h + 2 * g.p_h - g.k_h) / g.s_h + 1, ow = (g.w + 2 * g.p_w - g.k_w) / g.s_w + 1;
+    const int64_t m = (int64_t)g.n * oh * ow;
+    const bool cvec = g.c_i % kBKCvec == 0;
+    const int bk = cvec ? kBKCvec : kBKGeneric;
+    const int kt = (g.c_i * g.k_h * g.k_w + bk - 1) / bk;
+    int n = 0;
+    auto add = [&](int v, int sp, int gr, int rd, int ns) {
+        for (int i = 0; i < n; ++i)
+            if (out[i].variant == v && out[i].splits == sp && out[i].groups == gr && out[i].reduce == rd &&
+                out[i].no_stem == ns)
+                return;
+        if (n < max_out) out[n++] = PlanChoice{v, sp, gr, rd, ns};
+    };
+    const FfmaPlan def = plan_ffma(g, sm_count);
+    if (def.stem || def.persist1x1) add(-1, -1, 1, 0, 1);
+    struct V { int v, bm, bn, g0, g1; };
+    const V vs[] = {{3, 64, 128, 2, 2}, {4, 64, 64, 2, 4}, {1, 128, 64, 2, 4}};
+    const int targets[] = {sm_count / 2, sm_count * 3 / 4, sm_count, sm_count * 3 / 2, sm_count * 2};
+    for (const V& v : vs) {
+        const int64_t tiles = ((m + v.bm - 1) / v.bm) * ((g.c_o + v.bn - 1) / v.bn);
+        for (int t : targets) {
+            const int64_t sp = t / std::max<int64_t>(tiles, 1);
+            if (sp < 2 || sp > 32) continue;
+            for (int gr = v.g0; gr <= v.g1; gr += 2) {
+                if (!cvec) {  // generic K order: no warp groups, 64x64 tile not instantiated
+                    if (v.v != 4) add(v.v, (int)sp, 1, 5, 1);
+                } else if (kt / sp >= gr) {
+                    add(v.v, (int)sp, gr, 5, 1);
+                }
+            }
+        }
+    }
+    if (cvec) {
+        add(3, 0, 1, 0, 1);
+        add(1, 0, 1, 0, 1);
+    }
+    return n;
+}
 
 FfmaPlan plan_ffma_gather(const smmc_geom& g, int sm_count) {
     // the gather epilogue lives in the tiled kernel: plan without the stem kernel

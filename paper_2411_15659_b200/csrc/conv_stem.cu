@@ -863,8 +863,8 @@ cudaError_t launch_stem_rw(StemParams sp, cudaStream_t s) {
 // Layers with an instantiated stem kernel: c_i <= 4 with (KH, KW, SW) =
 // (3, 3, 1), (7, 7, 2) or (11, 11, 4) — VGG conv1_1 and the config-3 stems.
 // (5x5 and c_i > 4 stay on the tiled kernel.  DESIGN.md §3.1.)
-int stem_kind(const smmc_geom& g) {
-    const char* f = getenv("SMMC_STEM");  // A/B hook: 0 = tiled kernel
+int stem_kind(const smmc_geom& g, int sm_count) {
+    const char* f = getenv("SMMC_STEM");  // A/B hook: 0 = tiled kernel, 1 = stem kernel at any size
     if (f && atoi(f) == 0) return 0;
     if (g.c_i > kStemMaxCi) return 0;
     int kind = 0;
@@ -874,6 +874,19 @@ int stem_kind(const smmc_geom& g) {
     if (!kind) return 0;
     // the CTA's whole weight slice (K x BN floats) lives in shared memory
     if ((size_t)g.c_i * g.k_h * g.k_w * stem_bn(g, kind) * sizeof(float) > kStemMaxSmem) return 0;
+    // The strided stems keep a whole (c, kh) row loop of 21-33 windows in one
+    // thread: with fewer tile blocks than ~3/4 of the SMs (a single 224x224
+    // sample: 36-37 CTAs, AlexNet conv1 N=1 31 us against 12 us tiled) the
+    // tiled kernel's split-K plans win.
+    if (kind >= 2 && !(f && atoi(f) == 1)) {
+        const int px = kind == 2 ? SV2_PX : SV3_PX, ng = kind == 2 ? SV2_NG : SV3_NG;
+        const int t = kind == 2 ? SV2_T : SV3_T;
+        const int oh = (g.h + 2 * g.p_h - g.k_h) / g.s_h + 1, ow = (g.w + 2 * g.p_w - g.k_w) / g.s_w + 1;
+        const int64_t pgs = (int64_t)g.n * oh * ((ow + px - 1) / px);
+        const int pgc = (t / 32) * (32 / ng);
+        const int64_t ctas = ((pgs + pgc - 1) / pgc) * ((g.c_o + stem_bn(g, kind) - 1) / stem_bn(g, kind));
+        if (4 * ctas < 3 * (int64_t)sm_count) return 0;
+    }
     return kind;
 }
 
@@ -956,7 +969,19 @@ cudaError_t launch_stem(const Problem& p, int kind, cudaStream_t s) {
             // resident windows, channel passes, cross-tile prefetch (3x3 s1 p_w = 1, c_i = 3,
             // aligned rows); channels per CTA from the layer's c_o (least padding)
             const int rw = getenv("SMMC_STEM_RW0") ? 0 : stem_rw_bn(sp.co);  // A/B hook: round-1 kernel
-            if (rw == 64 && stem_rw_eligible<3, 3, 1, RW1_PX, RW1_CPT, RW1_NG, RW1_NP, RW1_T, RW1_MINB, 3, 3, RW1_ASYNC>(sp))
+            // few pixel groups (a single sample): 128-thread CTAs, 3 per SM, so every SM gets
+            // tiles (384-thread CTAs: 65 blocks for one 224 x 224 plane)
+            int sms = 148, dev = 0;
+            if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            const int64_t pgs = (int64_t)sp.n * sp.oh * ((sp.ow + RW1_PX - 1) / RW1_PX);
+            const bool small = pgs < (int64_t)sms * (RW1_T / 32) * (32 / RW1_NG) && RW1_T > 128;
+            if (small && rw == 64 && stem_rw_eligible<3, 3, 1, 4, 16, 2, 2, 128, 3, 3, 3, 0>(sp))
+                e = launch_stem_rw<3, 3, 1, 4, 16, 2, 2, 128, 3, 3, 3, 0>(sp, s);
+            else if (small && rw == 32 && stem_rw_eligible<3, 3, 1, 4, 16, 2, 1, 128, 3, 3, 3, 0>(sp))
+                e = launch_stem_rw<3, 3, 1, 4, 16, 2, 1, 128, 3, 3, 3, 0>(sp, s);
+            else if (small && rw == 16 && stem_rw_eligible<3, 3, 1, 4, 16, 1, 1, 128, 3, 3, 3, 0>(sp))
+                e = launch_stem_rw<3, 3, 1, 4, 16, 1, 1, 128, 3, 3, 3, 0>(sp, s);
+            else if (rw == 64 && stem_rw_eligible<3, 3, 1, RW1_PX, RW1_CPT, RW1_NG, RW1_NP, RW1_T, RW1_MINB, 3, 3, RW1_ASYNC>(sp))
                 e = launch_stem_rw<3, 3, 1, RW1_PX, RW1_CPT, RW1_NG, RW1_NP, RW1_T, RW1_MINB, 3, 3, RW1_ASYNC>(sp, s);
             else if (rw == 32 && stem_rw_eligible<3, 3, 1, 4, 16, 2, 1, RW1_T, RW1_MINB, 3, 3, RW1_ASYNC>(sp))
                 e = launch_stem_rw<3, 3, 1, 4, 16, 2, 1, RW1_T, RW1_MINB, 3, 3, RW1_ASYNC>(sp, s);

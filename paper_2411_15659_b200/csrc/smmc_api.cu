@@ -510,6 +510,117 @@ int smmc_plan_describe(const smmc_geom* g, int mode, char* buf, size_t len) {
 
 uint64_t smmc_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
+// Measure the candidate plans of one geometry on the current device and keep
+// the fastest for the rest of the process (plan_record).  Scratch operands are
+// allocated here (contents irrelevant to the timing: a finite constant), every
+// candidate runs `iters` back-to-back launches between CUDA events on a private
+// stream after two warm-up launches; a candidate that fails to launch is
+// skipped.  The winner replaces the default only when it is > 3 % faster.
+int smmc_autotune_f32(const smmc_geom* g, int iters, char* report, size_t report_len) {
+    int oh = 0, ow = 0;
+    int st = check_geom(g, &oh, &ow);
+    if (st) return st;
+    if (report && report_len) report[0] = 0;
+    if (g->n == 0) return SMMC_OK;
+    iters = std::max(1, std::min(iters, 1000));
+    const int sms = sm_count_for(current_device());
+    plan_record(*g, nullptr);
+    plan_force(nullptr);
+    PlanChoice cands[64];
+    const int nc = plan_candidates(*g, sms, cands, 64);
+    size_t ws_bytes = plan_ffma(*g, sms).ws_bytes;
+    for (int i = 0; i < nc; ++i) {
+        plan_force(&cands[i]);
+        ws_bytes = std::max(ws_bytes, plan_ffma(*g, sms).ws_bytes);
+    }
+    plan_force(nullptr);
+    const size_t xb = (size_t)g->n * g->c_i * g->h * g->w * sizeof(float);
+    const size_t wb = (size_t)g->c_i * g->k_h * g->k_w * g->c_o * sizeof(float);
+    const size_t yb = (size_t)g->n * g->c_o * oh * ow * sizeof(float);
+    float *x = nullptr, *w = nullptr, *y = nullptr;
+    void* ws = nullptr;
+    cudaStream_t s = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    auto cleanup = [&]() {
+        plan_force(nullptr);
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+        if (s) cudaStreamDestroy(s);
+        cudaFree(x);
+        cudaFree(w);
+        cudaFree(y);
+        cudaFree(ws);
+    };
+    cudaError_t ce = cudaMalloc(&x, xb);
+    if (ce == cudaSuccess) ce = cudaMalloc(&w, wb);
+    if (ce == cudaSuccess) ce = cudaMalloc(&y, yb);
+    if (ce == cudaSuccess && ws_bytes) ce = cudaMalloc(&ws, ws_bytes);
+    if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    if (ce == cudaSuccess) ce = cudaEventCreate(&e0);
+    if (ce == cudaSuccess) ce = cudaEventCreate(&e1);
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(x, 0x3c, xb, s);   // 0x3c3c3c3c = 0.0115f
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(w, 0x3c, wb, s);
+    if (ce == cudaSuccess && ws_bytes) ce = cudaMemsetAsync(ws, 0, ws_bytes, s);  // counters zero at rest
+    if (ce != cudaSuccess) {
+        cleanup();
+        return cuda_status(ce, "autotune scratch");
+    }
+    auto time_plan = [&](const PlanChoice* c, float* us) -> bool {
+        plan_force(c);
+        bool ok = true;
+        for (int i = 0; i < 2 && ok; ++i) ok = conv_device(x, w, y, g, SMMC_MODE_FFMA, ws, ws_bytes, s) == SMMC_OK;
+        if (ok) ok = cudaStreamSynchronize(s) == cudaSuccess;
+        if (ok) {
+            cudaEventRecord(e0, s);
+            for (int i = 0; i < iters && ok; ++i)
+                ok = conv_device(x, w, y, g, SMMC_MODE_FFMA, ws, ws_bytes, s) == SMMC_OK;
+            cudaEventRecord(e1, s);
+            ok = cudaStreamSynchronize(s) == cudaSuccess && ok;
+        }
+        plan_force(nullptr);
+        if (!ok) {
+            cudaGetLastError();  // a refused launch (e.g. cooperative grid too large) is not sticky
+            return false;
+        }
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        *us = ms * 1e3f / (float)iters;
+        return true;
+    };
+    float t_def = 0.f;
+    if (!time_plan(nullptr, &t_def)) {
+        cleanup();
+        set_error("autotune: the default plan failed to run");
+        return SMMC_ECUDA;
+    }
+    int best = -1;
+    float t_best = t_def;
+    for (int i = 0; i < nc; ++i) {
+        float t = 0.f;
+        if (time_plan(&cands[i], &t) && t < t_best) {
+            t_best = t;
+            best = i;
+        }
+    }
+    const bool keep = best >= 0 && t_best < 0.97f * t_def;
+    if (keep) plan_record(*g, &cands[best]);
+    if (report && report_len) {
+        if (keep)
+            snprintf(report, report_len, "default %.1f us; kept plan %d,%d,%d,%d%s at %.1f us (%d candidates)",
+                     t_def, cands[best].variant, cands[best].splits, cands[best].groups,
+                     cands[best].reduce, cands[best].variant < 0 ? " (tiled kernel, cost-model plan)" : "", t_best, nc);
+        else
+            snprintf(report, report_len, "default %.1f us kept (%d candidates, none > 3 %% faster)", t_def, nc);
+    }
+    cleanup();
+    return SMMC_OK;
+}
+
+int smmc_autotune_clear(void) {
+    plan_record_clear();
+    return SMMC_OK;
+}
+
 int smmc_conv2d_fwd_f32(const float* x, const float* w_smm, float* y, const smmc_geom* g, int mode,
                         void* workspace, size_t workspace_bytes, void* stream) {
     return conv_device(x, w_smm, y, g, mode, workspace, workspace_bytes,

@@ -135,13 +135,27 @@ struct FfmaPlan {
 // of other reduce modes never touch it, so one workspace may serve any
 // sequence of layers.
 constexpr size_t kCounterRegion = 64 * 1024;
+// A plan choice outside the cost model: tile variant, splits (0 = stream-K),
+// warp groups, reduce (5 = in-kernel), no_stem (tiled kernel for a stem layer).
+// plan_force() pins one for the calling thread (the autotuner's candidate
+// runs); plan_record() stores the measured winner of a geometry for the
+// process, consulted by plan_ffma before the static tuning table.
+struct PlanChoice {
+    int variant, splits, groups, reduce, no_stem;
+};
+void plan_force(const PlanChoice* c);  // nullptr clears
+void plan_record(const smmc_geom& g, const PlanChoice* c);  // nullptr forgets g
+void plan_record_clear();
+bool plan_recorded(const smmc_geom& g, PlanChoice* out);
+// Candidate plans worth measuring for g (never the default plan itself).
+int plan_candidates(const smmc_geom& g, int sm_count, PlanChoice* out, int max_out);
 FfmaPlan plan_ffma(const smmc_geom& g, int sm_count);
 FfmaPlan plan_ffma_gather(const smmc_geom& g, int sm_count);
 cudaError_t launch_ffma(const Problem& p, const FfmaPlan& plan, cudaStream_t s);
 bool conv1x1_eligible(const smmc_geom& g);
 constexpr int kStemMaxCi = 4;
 constexpr size_t kStemMaxSmem = 200 * 1024;
-int stem_kind(const smmc_geom& g);
+int stem_kind(const smmc_geom& g, int sm_count = 148);
 int stem_bn(const smmc_geom& g, int kind);
 cudaError_t launch_stem(const Problem& p, int kind, cudaStream_t s);
 int stem_describe(const smmc_geom& g, int kind, char* buf, size_t len);

@@ -149,13 +149,21 @@ class SmmConv2d:
     ``weights`` may be OIHW numpy / torch (repacked once here, untimed).
     """
 
-    def __init__(self, geom, weights, device="cuda", mode="ffma", max_batch=None):
+    def __init__(self, geom, weights, device="cuda", mode="ffma", max_batch=None, autotune=None):
         torch = _torch()
         if not torch.cuda.is_available():
             raise DeviceError("SmmConv2d needs a CUDA device (no CPU fallback)")
         self.geom = geom
         self.mode = mode
         self.device = torch.device(device)
+        # per-shape autotuning (needs the batch size: plans depend on it); off
+        # unless asked for here or by SMMC_AUTOTUNE=1
+        self.autotune_report = None
+        if autotune is None:
+            autotune = _native.autotune_enabled()
+        if autotune and max_batch and mode == "ffma":
+            with torch.cuda.device(self.device):
+                self.autotune_report = _native.autotune(geom, max_batch)
         w = torch.as_tensor(weights, dtype=torch.float32)
         if tuple(w.shape) == geom.weights_shape:
             w = w.permute(1, 3, 2, 0)

@@ -153,3 +153,14 @@ def test_stem_plans_without_gpu():
         assert "direct stem" not in _native.plan_describe(g, 8)
     finally:
         del os.environ["SMMC_STEM"]
+    # a single sample of a strided stem has too few tile blocks for the stem
+    # kernel's long per-thread row loops: tiled split-K plans (SMMC_STEM=1 forces it)
+    for gt in [(3, 64, 224, 224, 7, 7, 2, 2, 3, 3), (3, 96, 227, 227, 11, 11, 4, 4, 0, 0)]:
+        g = ConvGeometry(*gt)
+        assert "direct stem" not in _native.plan_describe(g, 1), gt
+        os.environ["SMMC_STEM"] = "1"
+        try:
+            assert "direct stem" in _native.plan_describe(g, 1), gt
+        finally:
+            del os.environ["SMMC_STEM"]
+    assert "direct stem" in _native.plan_describe(ConvGeometry(3, 64, 224, 224, 3, 3, 1, 1, 1, 1), 1)

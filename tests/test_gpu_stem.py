@@ -49,6 +49,7 @@ def _run(g, n, seed):
 def test_stem_kernel_matches_oracle(gt, n, monkeypatch):
     import torch
     g = ConvGeometry(*gt)
+    monkeypatch.setenv("SMMC_STEM", "1")   # the stem kernel at any size (small problems plan tiled)
     desc = _native.plan_describe(g, n)
     assert "direct stem" in desc, desc
     x, w, xd, wd, device = _run(g, n, 7)
@@ -64,11 +65,12 @@ def test_stem_kernel_matches_oracle(gt, n, monkeypatch):
     assert orc.max_abs_ratio(yt.cpu().numpy(), ref) <= TOL_FP32
 
 
-def test_stem_kernel_on_unaligned_input_and_host_entry():
+def test_stem_kernel_on_unaligned_input_and_host_entry(monkeypatch):
     """x at an odd 4-byte offset (a sample slice of an odd-sized batch) and
     the host-buffer entry point (chunked pipeline) both reach the stem kernel."""
     import ctypes
     import torch
+    monkeypatch.setenv("SMMC_STEM", "1")
     g = ConvGeometry(3, 64, 31, 31, 7, 7, 2, 2, 3, 3)
     x, w = synthetic_layer(g, 3, 11)
     ws = smm.repack_weights(w, g)
@@ -89,10 +91,11 @@ def test_stem_kernel_on_unaligned_input_and_host_entry():
     assert orc.max_abs_ratio(yh, ref) <= TOL_FP32
 
 
-def test_random_stem_geometries():
+def test_random_stem_geometries(monkeypatch):
     """80 random c_i <= 4 geometries over the stem kernel's tap kinds; other
     c_i <= 4 kernels (5x5, ...) stay on the tiled kernel."""
     import torch
+    monkeypatch.setenv("SMMC_STEM", "1")
     rng = np.random.default_rng(31337)
     kinds = [(3, 3, 1), (7, 7, 2), (11, 11, 4)]
     checked = 0

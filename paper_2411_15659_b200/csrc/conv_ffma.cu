@@ -1132,9 +1132,48 @@ static FfmaPlan plan_ffma_impl(const smmc_geom& g, int sm_count, bool allow_stem
             best.sk_maxseg = maxseg;
         }
     }
+    // (c) one-wave problems (the preset networks at batch 1: 0.1-4 GFLOP): when the
+    // best classic plan is a split grid of at most one wave, split-K reduced
+    // IN the kernel by all split CTAs (mode 5, no second launch) on a grid of
+    // about one CTA per SM with warp groups inside the CTA.  The rule follows
+    // what smmc_autotune_f32 picks on those layers (profiles/r02/harness/
+    // autotune_probe.log): the tile that pads M x N least at the fullest
+    // single wave, 4 warp groups when a split keeps >= 12 tap blocks, else 2.
+    int rule_v = -1, rule_s = 0, rule_g = 1;
+    if (cvec && best.reduce_mode != 3 && best.splits > 1 && best_waves <= 1 && !conv1x1_eligible(g) &&
+        !getenv("SMMC_NO_SMALL_RULE")) {  // (A/B hook)
+        double best_score = 0.0;
+        const int order[3] = {1, 3, 4};  // 128x64, 64x128, 64x64
+        for (int v : order) {
+            const TileCfg t = kTiles[v];
+            const int64_t tiles = ((m + t.bm - 1) / t.bm) * ((g.c_o + t.bn - 1) / t.bn);
+            int64_t sp = std::min<int64_t>({(int64_t)sm_count / std::max<int64_t>(tiles, 1), 32, kt_total / 2});
+            if (sp < 2) continue;
+            const double fill = (double)(tiles * sp) / sm_count;
+            const double useful = (double)m * g.c_o / ((double)tiles * t.bm * t.bn);
+            const double score = fill * useful;
+            // (fill x useful < 0.7: VGG conv4_x at batch 1, 56 tiles x 2 splits on 148 SMs,
+            // measured 9-19 % slower than its classic 11-way split)
+            if (score >= 0.7 && score > best_score * 1.02) {
+                best_score = score;
+                rule_v = v;
+                rule_s = (int)sp;
+            }
+        }
+        if (rule_v >= 0) {
+            const int per = (kt_total + rule_s - 1) / rule_s;
+            rule_g = per >= 12 ? 4 : 2;
+        }
+    }
     // measured-best plans for known shapes (tuning table), then the
     // SMMC_FORCE_PLAN="variant,splits" experiment hook (splits 0 = stream-K)
     int fv = -1, fs = -1, fg = 1, fr = 0;
+    if (rule_v >= 0) {
+        fv = rule_v;
+        fs = rule_s;
+        fg = rule_g;
+        fr = 5;
+    }
     const bool use_table = !getenv("SMMC_NO_TABLE");  // A/B hook: cost model / 1x1 kernel only
     for (const TunedPlan& e : kTuned) {
         if (use_table && e.n == g.n && e.c_i == g.c_i && e.h == g.h && e.w == g.w && e.c_o == g.c_o &&

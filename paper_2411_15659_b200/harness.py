@@ -344,7 +344,12 @@ def main(argv=None):
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--csv", default="")
+    ap.add_argument("--autotune", action="store_true",
+                    help="per-shape autotuning of the b200_smm plans at fit (same as SMMC_AUTOTUNE=1)")
     a = ap.parse_args(argv)
+    if a.autotune:
+        import os
+        os.environ["SMMC_AUTOTUNE"] = "1"
     specs = (builtin_network(a.network) if a.network else
              load_layer_config(a.config) if a.config else sweep(a.sweep))
     recs = run_bench(specs, a.backends.split(","), a.repeats, a.batch, a.seed)

@@ -217,7 +217,7 @@ SMMC_API int smmc_plan_launches(const smmc_geom* g, int mode);
  * grids sized to the SM count, stream-K, the tiled kernel for stem / 1x1 layers
  * -- with scratch operands it allocates itself, `iters` launches per candidate,
  * and keeps the fastest for the rest of the process when it beats the default
- * plan by more than 3 %: later smmc_conv2d_fwd_f32 / smmc_workspace_bytes /
+ * plan by more than 5 %: later smmc_conv2d_fwd_f32 / smmc_workspace_bytes /
  * smmc_plan_describe calls for the same geometry use it (call it BEFORE sizing a
  * workspace or creating a layer).  Every candidate is one of the parity-tested
  * plan kinds; results stay within the fp32 bar and deterministic for a fixed

@@ -1142,7 +1142,17 @@ static FfmaPlan plan_ffma_impl(const smmc_geom& g, int sm_count, bool allow_stem
     int rule_v = -1, rule_s = 0, rule_g = 1;
     if (cvec && best.reduce_mode != 3 && best.splits > 1 && best_waves <= 1 && !conv1x1_eligible(g) &&
         !getenv("SMMC_NO_SMALL_RULE")) {  // (A/B hook)
-        double best_score = 0.0;
+        // the classic plan's own fill x useful area is the bar to beat (VGG conv4_x at
+        // batch 1: 572 CTAs on 592 slots at 94 % useful area stays classic; 56 tiles x 2
+        // in-kernel splits on 148 SMs measured 9-19 % slower)
+        const TileCfg bt = kTiles[best.variant];
+        const double classic_fill =
+            std::min(1.0, (double)(best.tiles * best.splits) / ((double)sm_count * bt.per_sm));
+        // (a classic plan of more than 4 splits also pays a second launch that re-reads
+        // all S partial tiles: YOLOv3-tiny conv4/conv5 20 -> 15.5 us at equal fill)
+        const double classic_score = classic_fill * (double)m * g.c_o / ((double)best.tiles * bt.bm * bt.bn) *
+                                     (best.splits > 4 ? 0.8 : 1.0);
+        double best_score = classic_score;
         const int order[3] = {1, 3, 4};  // 128x64, 64x128, 64x64
         for (int v : order) {
             const TileCfg t = kTiles[v];
@@ -1152,9 +1162,7 @@ static FfmaPlan plan_ffma_impl(const smmc_geom& g, int sm_count, bool allow_stem
             const double fill = (double)(tiles * sp) / sm_count;
             const double useful = (double)m * g.c_o / ((double)tiles * t.bm * t.bn);
             const double score = fill * useful;
-            // (fill x useful < 0.7: VGG conv4_x at batch 1, 56 tiles x 2 splits on 148 SMs,
-            // measured 9-19 % slower than its classic 11-way split)
-            if (score >= 0.7 && score > best_score * 1.02) {
+            if (score > best_score * 1.02) {
                 best_score = score;
                 rule_v = v;
                 rule_s = (int)sp;

@@ -43,13 +43,19 @@ def main():
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--cands", default="", help='space-separated forced plans "v,s[,g[,r]]" tried per layer')
+    ap.add_argument("--sweep", default="", help="one of the paper's sweeps instead of a network")
     ap.add_argument("--auto", action="store_true")
     ap.add_argument("--autotune", action="store_true", help="default vs smmc_autotune_f32 per layer")
     ap.add_argument("--quiet", action="store_true")
     a = ap.parse_args()
     seen = set()
     total = [0.0, 0.0]
-    for name, g in network_geometries(a.net):
+    if a.sweep:
+        from paper_2411_15659_b200.harness import sweep
+        layers = [(sp.name, sp.geometry) for sp in sweep(a.sweep)]
+    else:
+        layers = network_geometries(a.net)
+    for name, g in layers:
         key = (g.in_channels, g.out_channels, g.in_h, g.in_w, g.k_h, g.stride_h)
         if key in seen:
             continue
@@ -97,7 +103,7 @@ def main():
         if cands:
             print(f"      best {best[1]:12s} {best[0]:8.1f} us ({us / best[0]:.2f}x default)", flush=True)
     if a.autotune:
-        print(f"{a.net} distinct conv layers at batch {a.batch}: default {total[0]:.1f} us -> tuned {total[1]:.1f} us")
+        print(f"{a.sweep or a.net} distinct conv layers at batch {a.batch}: default {total[0]:.1f} us -> tuned {total[1]:.1f} us")
 
 
 if __name__ == "__main__":

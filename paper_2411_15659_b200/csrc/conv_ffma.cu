@@ -104,7 +104,7 @@ constexpr int ring_stages() {
 }
 template <int BM, int BN, int THREADS, int G, int MINB>
 constexpr int min_blocks() {
-    return G > 1 ? ((BM == 64 && BN == 64 && THREADS * G <= 256) ? 2 : 1) : MINB;
+    return G > 1 ? ((BM == 64 && BN == 64 && THREADS * G <= 256) ? 2 : 1) : (BN == 32 ? 8 : MINB);
 }
 
 template <int BM, int BN, int THREADS, int MINB, int TM, int BK, int KH, int KW, int SH, int SW,
@@ -117,9 +117,14 @@ __global__ void __launch_bounds__(THREADS * G, (min_blocks<BM, BN, THREADS, G, M
     constexpr int TCO = BN / 8;            // channel groups (4 + 4 channels each)
     static_assert(TPX * TCO == THREADS, "thread tile must cover the CTA tile");
     static_assert(TCO % kLaneCo == 0 && TPX % kLanePx == 0, "warp = kLanePx pixel groups x kLaneCo channel groups");
-    static_assert(THREADS % BM == 0, "loader maps one pixel column per thread");
-    constexpr int KSTEP = THREADS / BM;    // k rows apart for one thread's A loads
-    constexpr int A_PER = BK * BM / THREADS;
+    // A loader: a thread owns one pixel column of the tile and every KSTEP-th
+    // k row of a block -- or, for narrow-channel tiles with fewer threads than
+    // pixels (128 x 32 on 64 threads), PXC pixel columns and every k row.
+    constexpr int PXC = BM > THREADS ? BM / THREADS : 1;
+    static_assert(PXC == 1 ? THREADS % BM == 0 : BM % THREADS == 0, "loader maps whole pixel columns to threads");
+    static_assert(PXC == 1 || CVEC, "multi-column loader: tap-major K order only");
+    constexpr int KSTEP = PXC == 1 ? THREADS / BM : 1;  // k rows apart for one thread's A loads
+    constexpr int A_PER = BK / KSTEP;                   // k rows per pixel column per thread
     constexpr int B_CHUNKS = BK * BN / 4;  // 16-byte chunks per B tile
     constexpr int B_PER = (B_CHUNKS + THREADS - 1) / THREADS;
     constexpr bool B_FULL = (B_CHUNKS % THREADS) == 0;
@@ -217,6 +222,27 @@ __global__ void __launch_bounds__(THREADS * G, (min_blocks<BM, BN, THREADS, G, M
         iw0 = ow * sw - p.pw;
         xoff0 = (int64_t)n * p.c * p.hw + (int64_t)ih0 * p.w_in + iw0;
     }
+    // extra pixel columns of a narrow-channel tile's loader thread (PXC > 1: fewer
+    // threads than pixels; column c is pixel tid + c*THREADS, every k row)
+    bool xpvalid[PXC];
+    int64_t xxoff0[PXC];
+    int xih0[PXC], xiw0[PXC];
+#pragma unroll
+    for (int c = 1; c < PXC; ++c) {
+        const int pmc = m0 + tid + c * THREADS;
+        xpvalid[c] = pmc < p.m;
+        xih0[c] = xiw0[c] = 0;
+        xxoff0[c] = 0;
+        if (xpvalid[c]) {
+            const int n = pmc / p.ohw;
+            const int rem = pmc - n * p.ohw;
+            const int oh = rem / p.ow;
+            const int ow = rem - oh * p.ow;
+            xih0[c] = oh * sh - p.ph;
+            xiw0[c] = ow * sw - p.pw;
+            xxoff0[c] = (int64_t)n * p.c * p.hw + (int64_t)xih0[c] * p.w_in + xiw0[c];
+        }
+    }
     const float* __restrict__ xg = p.x;
     const float* __restrict__ wg = p.w;
 #ifdef SMMC_CHECKED
@@ -241,6 +267,17 @@ __global__ void __launch_bounds__(THREADS * G, (min_blocks<BM, BN, THREADS, G, M
         for (int r = 0; r < kh; ++r) rowmask |= (uint32_t)((unsigned)(ih0 + r) < (unsigned)p.h) << r;
         for (int j = 0; j < kw; ++j)
             colmask |= (uint32_t)((unsigned)(iw0 + j) < (unsigned)p.w_in) << j;
+    }
+    uint32_t xrowmask[PXC], xcolmask[PXC];
+#pragma unroll
+    for (int c = 1; c < PXC; ++c) {
+        xrowmask[c] = xcolmask[c] = 0;
+        if (masks && xpvalid[c]) {
+            for (int r = 0; r < kh; ++r)
+                xrowmask[c] |= (uint32_t)((unsigned)(xih0[c] + r) < (unsigned)p.h) << r;
+            for (int j = 0; j < kw; ++j)
+                xcolmask[c] |= (uint32_t)((unsigned)(xiw0[c] + j) < (unsigned)p.w_in) << j;
+        }
     }
     // generic path: an odometer over this thread's next update index
     // kidx = (c*kw + j)*kh + k (the reference's order) and its input offset
@@ -276,12 +313,24 @@ __global__ void __launch_bounds__(THREADS * G, (min_blocks<BM, BN, THREADS, G, M
     int ld_tap = 0, ld_cb = 0;
     bool a_ok = false;
     const float* a_ptr = xg;
+    bool xa_ok[PXC];
+    const float* xa_ptr[PXC];
+#pragma unroll
+    for (int c = 1; c < PXC; ++c) {
+        xa_ok[c] = false;
+        xa_ptr[c] = xg;
+    }
     const float* b_ptr = wg;
     auto set_tap = [&]() {
         const int j = ld_tap / kh;
         const int kr = ld_tap - j * kh;
         a_ok = (rowmask >> kr) & (colmask >> j) & 1u;
         a_ptr = xg + xoff0 + (int64_t)(ld_cb * BK + lk0) * p.hw + kr * p.w_in + j;
+#pragma unroll
+        for (int c = 1; c < PXC; ++c) {
+            xa_ok[c] = (xrowmask[c] >> kr) & (xcolmask[c] >> j) & 1u;
+            xa_ptr[c] = xg + xxoff0[c] + (int64_t)(ld_cb * BK) * p.hw + kr * p.w_in + j;
+        }
         b_ptr = wg + ((int64_t)(ld_cb * BK + brow) * taps + ld_tap) * p.co + bco;
     };
     if (CVEC) {
@@ -298,6 +347,16 @@ __global__ void __launch_bounds__(THREADS * G, (min_blocks<BM, BN, THREADS, G, M
                 SMMC_CHECK_SMEM(smem0, adst + i * KSTEP * BM * 4, 4);
                 if (a_ok) SMMC_CHECK_RANGE(a_ptr + i * a_elem - xg, 1, x_elems);
                 cp_async4_zfill(adst + i * KSTEP * BM * 4, a_ok ? a_ptr + i * a_elem : xg, a_ok);
+            }
+#pragma unroll
+            for (int c = 1; c < PXC; ++c) {
+#pragma unroll
+                for (int i = 0; i < A_PER; ++i) {
+                    SMMC_CHECK_SMEM(smem0, adst + (c * THREADS + i * BM) * 4, 4);
+                    if (xa_ok[c]) SMMC_CHECK_RANGE(xa_ptr[c] + i * a_elem - xg, 1, x_elems);
+                    cp_async4_zfill(adst + (c * THREADS + i * BM) * 4, xa_ok[c] ? xa_ptr[c] + i * a_elem : xg,
+                                    xa_ok[c]);
+                }
             }
             const uint32_t bdst = bs_base + slot * BS_STAGE + (brow * BN + bcol) * 4;
 #pragma unroll
@@ -323,6 +382,8 @@ __global__ void __launch_bounds__(THREADS * G, (min_blocks<BM, BN, THREADS, G, M
                 if (ld_tap < taps) set_tap();
             } else {
                 a_ptr += a_blk;
+#pragma unroll
+                for (int c = 1; c < PXC; ++c) xa_ptr[c] += a_blk;
                 b_ptr += b_blk;
             }
         } else {
@@ -892,6 +953,9 @@ constexpr TileCfg kTiles[] = {
     {256, 64, 256, 2, 8, 1},    // 2
     {64, 128, 128, 4, 8, 1},    // 3
     {64, 64, 64, 8, 8, 0},      // 4: small problems (N = 1), with warp groups / in-kernel split reduce
+    {128, 32, 64, 5, 8, 1},     // 5: c_o (mod 64) <= 32, tap-major layers only (the paper's c_o = 32
+                                //    sweeps): half the padded channels of a 64-wide tile; 64 threads
+                                //    load two pixel columns each
     // 4 x 8 thread tiles (64 registers, 8 CTAs/SM: latency hiding by
     // occupancy) were measured 1-13 % slower on the c_i = 3 stems and 1x1
     // layers (A/B, round 1) and are not instantiated.
@@ -1052,9 +1116,11 @@ static FfmaPlan plan_ffma_impl(const smmc_geom& g, int sm_count, bool allow_stem
     const int bk = cvec ? kBKCvec : kBKGeneric;
     const int kt_total = cvec ? taps * (g.c_i / bk) : (g.c_i * taps + bk - 1) / bk;
     const double blk = bk / 8.0;  // work of one tap block in 8-deep units
+    // the 32-channel tile: tap-major layers whose last 64-channel tile is at most half full
+    const bool narrow_ok = cvec && (g.c_o % 64) != 0 && (g.c_o % 64) <= 32 && !getenv("SMMC_NO_BN32");
     for (int v = 0; v < kNumTiles; ++v) {
         const TileCfg t = kTiles[v];
-        if (!t.model) continue;
+        if (!t.model || (v == 5 && !narrow_ok)) continue;
         const int64_t mt = (m + t.bm - 1) / t.bm;
         const int64_t nt = (g.c_o + t.bn - 1) / t.bn;
         const int64_t tiles = mt * nt;
@@ -1096,7 +1162,7 @@ static FfmaPlan plan_ffma_impl(const smmc_geom& g, int sm_count, bool allow_stem
     // slower than the classic grid; forced plans still reach it)
     for (int v = 0; v < kNumTiles && cvec && best_waves <= 2; ++v) {
         const TileCfg t = kTiles[v];
-        if (!t.model) continue;
+        if (!t.model || v == 5) continue;  // (stream-K: not instantiated for the 32-channel tile)
         const int64_t nt = (g.c_o + t.bn - 1) / t.bn;
         const int64_t tiles = ((m + t.bm - 1) / t.bm) * nt;
         const int64_t slots = (int64_t)sm_count * t.per_sm;
@@ -1228,7 +1294,7 @@ static FfmaPlan plan_ffma_impl(const smmc_geom& g, int sm_count, bool allow_stem
             }
         }
     }
-    if (fv == 4 && (!cvec || fs == 0)) fv = -1;  // the 64x64 tile: tap-major split grids only
+    if ((fv == 4 || fv == 5) && (!cvec || fs == 0)) fv = -1;  // 64x64 / 128x32 tiles: tap-major split grids only
     // warp groups: tap-major blocks, classic split grid, instantiated
     // (variant, G) pairs only
     const bool groups_ok = cvec && fs > 0 &&
@@ -1417,6 +1483,14 @@ int plan_candidates(const smmc_geom& g, int sm_count, PlanChoice* out, int max_o
         add(3, 0, 1, 0, 1);
         add(1, 0, 1, 0, 1);
     }
+    if (cvec && (g.c_o % 64) != 0 && (g.c_o % 64) <= 32) {  // the 128x32 tile, 2-4 CTAs per SM
+        const int64_t tiles = ((m + 127) / 128) * ((g.c_o + 31) / 32);
+        add(5, 1, 1, 0, 1);
+        for (int t : {sm_count, sm_count * 2, sm_count * 4}) {
+            const int64_t sp = t / std::max<int64_t>(tiles, 1);
+            if (sp >= 2 && sp <= 32 && kt / sp >= 1) add(5, (int)sp, 1, 5, 1);
+        }
+    }
     return n;
 }
 
@@ -1479,6 +1553,7 @@ cudaError_t launch_ffma(const Problem& p, const FfmaPlan& pl, cudaStream_t s) {
         case 1: e = launch_tile<128, 64, 128, 4>(p, pl.tap_kind, pl.cvec, grid, s); break;
         case 2: e = launch_tile<256, 64, 256, 2>(p, pl.tap_kind, pl.cvec, grid, s); break;
         case 4: e = launch_tile_groups<64, 64, 64, 1>(p, pl.tap_kind, grid, s); break;
+        case 5: e = launch_tile_groups<128, 32, 64, 1>(p, pl.tap_kind, grid, s); break;
         default: e = launch_tile<64, 128, 128, 4>(p, pl.tap_kind, pl.cvec, grid, s); break;
     }
     count_launches(1);

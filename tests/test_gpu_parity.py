@@ -247,6 +247,33 @@ def test_every_reduction_mode_matches_oracle(plan, cluster, monkeypatch):
 
 
 @pytest.mark.parametrize("cluster", ["1", "0"])
+@pytest.mark.parametrize("plan", ["5,1", "5,2", "5,3", "5,8", "5,36", "5,4,1,5", "5,7,1,5"])
+@pytest.mark.parametrize("gt,n", [((64, 32, 20, 20, 3, 3, 1, 1, 1, 1), 5),     # c_o = 32: one channel tile
+                                  ((32, 88, 17, 23, 5, 5, 1, 1, 2, 2), 2),     # c_o % 64 = 24, ragged pixels
+                                  ((16, 7, 30, 30, 3, 3, 2, 2, 0, 1), 3)])     # c_o % 4 != 0, strided
+def test_narrow_channel_tile_every_reduction(gt, n, plan, cluster, monkeypatch):
+    """The 128 x 32 tile (64 threads, two pixel columns per loader thread) under
+    no split, last arriver / cluster DSMEM, reduce kernel and in-kernel split
+    reductions: oracle parity, bitwise run to run."""
+    import torch
+    from paper_2411_15659_b200 import device
+    g = ConvGeometry(*gt)
+    monkeypatch.setenv("SMMC_FORCE_PLAN", plan)
+    monkeypatch.setenv("SMMC_CLUSTER_RED", cluster)
+    desc = _native.plan_describe(g, n)
+    assert "tile 128x32" in desc, desc
+    x, w = synthetic_layer(g, n, 77)
+    wd = torch.from_numpy(smm.repack_weights(w, g)).cuda()
+    xd = torch.from_numpy(x).cuda()
+    y1 = device.conv2d(xd, wd, g)
+    y2 = device.conv2d(xd, wd, g)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2), desc
+    ref = orc.smm_conv_c(x, orc.repack(w), g, threads=orc.host_threads())
+    assert orc.max_abs_ratio(y1.cpu().numpy(), ref) <= TOL_FP32, desc
+
+
+@pytest.mark.parametrize("cluster", ["1", "0"])
 @pytest.mark.parametrize("plan", ["1,1,4", "3,1,2", "0,1,2", "1,3,2", "1,8,4", "3,6,4", "1,16,4",
                                   "3,32,2", "0,12,2", "1,4,3", "3,5,3"])
 def test_warp_group_split_matches_oracle(plan, cluster, monkeypatch):

@@ -63,6 +63,9 @@ def main():
         ffma("inkernel_split_S9_groups4", g3, 1, {"SMMC_FORCE_PLAN": "4,9,4,5"}),
         ffma("inkernel_split_S18_7x7", G(128, 72, 7, 7, 3), 2, {"SMMC_FORCE_PLAN": "4,18,2,5"}),
         ffma("inkernel_split_128x64", g3, 2, {"SMMC_FORCE_PLAN": "1,4,1,5"}),
+        ffma("narrow_tile_128x32", G(64, 32, 20, 20, 3), 3, {"SMMC_FORCE_PLAN": "5,1"}),
+        ffma("narrow_tile_last_arriver", G(32, 88, 17, 23, 5), 2, {"SMMC_FORCE_PLAN": "5,3", "SMMC_CLUSTER_RED": "0"}),
+        ffma("narrow_tile_inkernel", G(64, 32, 20, 20, 3), 2, {"SMMC_FORCE_PLAN": "5,4,1,5"}),
         ffma("generic_order_ci3", G(3, 16, 12, 12, 5), 2, {"SMMC_STEM": "0"}),
         ffma("ragged_co37", G(24, 37, 11, 9, 3), 3, {}),
         ffma("planner_default_n1", G(128, 128, 14, 14, 3), 1, {}),

@@ -164,3 +164,33 @@ def test_stem_plans_without_gpu():
         finally:
             del os.environ["SMMC_STEM"]
     assert "direct stem" in _native.plan_describe(ConvGeometry(3, 64, 224, 224, 3, 3, 1, 1, 1, 1), 1)
+
+
+def test_one_wave_and_narrow_channel_plans_without_gpu(monkeypatch):
+    """Planner rules for the reference harness's batch-1 layers (no GPU needed:
+    plans are host logic): a one-wave split problem runs split-K reduced in the
+    kernel on about one CTA per SM; a layer whose classic plan already fills the
+    GPU keeps it; tap-major layers with c_o (mod 64) <= 32 use the 128 x 32
+    tile; BASELINE shapes keep their measured plans."""
+    alex3 = ConvGeometry(192, 384, 13, 13, 3, 3, 1, 1, 1, 1)
+    d = _native.plan_describe(alex3, 1)
+    assert "reduce=in-kernel" in d and "warp groups" in d, d
+    ws_rule = _native.workspace_bytes(alex3, 1, "ffma")
+    monkeypatch.setenv("SMMC_NO_SMALL_RULE", "1")
+    d0 = _native.plan_describe(alex3, 1)
+    assert "reduce=in-kernel" not in d0, d0
+    assert _native.workspace_bytes(alex3, 1, "ffma") != ws_rule or "split_k" in d0
+    monkeypatch.delenv("SMMC_NO_SMALL_RULE")
+    vgg4 = ConvGeometry(256, 512, 28, 28, 3, 3, 1, 1, 1, 1)
+    assert "reduce=in-kernel" not in _native.plan_describe(vgg4, 1)
+    # the paper's sweeps: c_o = 32 (layers.py:114-135)
+    sweep = ConvGeometry(64, 32, 512, 512, 3, 3)
+    assert "tile 128x32" in _native.plan_describe(sweep, 1)
+    monkeypatch.setenv("SMMC_NO_BN32", "1")
+    assert "tile 128x32" not in _native.plan_describe(sweep, 1)
+    monkeypatch.delenv("SMMC_NO_BN32")
+    assert "tile 128x32" not in _native.plan_describe(ConvGeometry(64, 64, 224, 224, 3, 3, 1, 1, 1, 1), 64)
+    assert "tile 128x32" not in _native.plan_describe(ConvGeometry(3, 32, 64, 64, 5, 5), 1)  # generic K order
+    # BASELINE config 1 / config 5 keep their table plans
+    assert "tile 64x64" in _native.plan_describe(ConvGeometry(64, 64, 56, 56, 3, 3, 1, 1, 1, 1), 1)
+    assert "tile 64x128" in _native.plan_describe(ConvGeometry(512, 512, 7, 7, 3, 3, 1, 1, 1, 1), 8)

@@ -1346,6 +1346,15 @@ static FfmaPlan plan_ffma_impl(const smmc_geom& g, int sm_count, bool allow_stem
         const char* f = getenv("SMMC_CLUSTER_RED");  // A/B hook
         if (!f || atoi(f) != 0) best.reduce_mode = 4;
     }
+    // (d) a split of more than 4 whose whole grid is co-resident (one wave at the
+    // tile's design occupancy, which its launch bounds and ring size guarantee):
+    // reduce in the kernel (mode 5) instead of the second launch -- same tile,
+    // same splits, same summation order per output.  VGG-16 at batch 1: conv3_1
+    // 53.9 -> 43.8 us, conv3_2 87.3 -> 77.8, conv4_1 53.6 -> 49.6, conv4_2 90.1 -> 86.5.
+    if (best.reduce_mode == 2 && !env_forced && !table_hit && best.groups == 1 && best.variant != 5 &&
+        best.tiles * best.splits <= (int64_t)sm_count * kTiles[best.variant].per_sm &&
+        !getenv("SMMC_NO_INKERNEL_RULE"))  // (A/B hook)
+        best.reduce_mode = 5;
     // 1x1 layers: the persistent block-stream kernel (no split, no
     // workspace); the tiled kernel with the same tile is its fallback for
     // operands that are not 16-byte aligned

@@ -178,11 +178,19 @@ def test_one_wave_and_narrow_channel_plans_without_gpu(monkeypatch):
     ws_rule = _native.workspace_bytes(alex3, 1, "ffma")
     monkeypatch.setenv("SMMC_NO_SMALL_RULE", "1")
     d0 = _native.plan_describe(alex3, 1)
-    assert "reduce=in-kernel" not in d0, d0
-    assert _native.workspace_bytes(alex3, 1, "ffma") != ws_rule or "split_k" in d0
+    assert "warp groups" not in d0 and "tile 128x128" in d0, d0   # the cost model's classic grid
+    assert _native.workspace_bytes(alex3, 1, "ffma") != ws_rule
     monkeypatch.delenv("SMMC_NO_SMALL_RULE")
+    # a classic grid that already fills one wave keeps its tile and splits; its
+    # reduction moves into the kernel when the whole grid is co-resident
     vgg4 = ConvGeometry(256, 512, 28, 28, 3, 3, 1, 1, 1, 1)
-    assert "reduce=in-kernel" not in _native.plan_describe(vgg4, 1)
+    d4 = _native.plan_describe(vgg4, 1)
+    assert "tile 64x128" in d4 and "split_k=11" in d4 and "reduce=in-kernel" in d4, d4
+    assert _native.plan_launches(vgg4, 1, "ffma") == 1
+    monkeypatch.setenv("SMMC_NO_INKERNEL_RULE", "1")
+    assert "reduce=kernel" in _native.plan_describe(vgg4, 1)
+    assert _native.plan_launches(vgg4, 1, "ffma") == 2
+    monkeypatch.delenv("SMMC_NO_INKERNEL_RULE")
     # the paper's sweeps: c_o = 32 (layers.py:114-135)
     sweep = ConvGeometry(64, 32, 512, 512, 3, 3)
     assert "tile 128x32" in _native.plan_describe(sweep, 1)

@@ -102,7 +102,7 @@ def main():
         ("tc_split", G(256, 64, 7, 7, 3), 1, {"SMMC_TC_SPLIT": "4"}),
         ("tc_1x1", G(64, 256, 8, 8, 1, 1, 0), 2, {}),
     ]
-    hooks = ("SMMC_FORCE_PLAN", "SMMC_CLUSTER_RED", "SMMC_STEM", "SMMC_STEM_SCALAR", "SMMC_1X1",
+    hooks = ("SMMC_FORCE_PLAN", "SMMC_CLUSTER_RED", "SMMC_STEM", "SMMC_STEM_SCALAR", "SMMC_STEM_RW0", "SMMC_1X1",
              "SMMC_1X1_WRES",
              "SMMC_TC_PERSIST", "SMMC_TC_MT", "SMMC_TC_BN", "SMMC_TC_KERNEL", "SMMC_TC_SPLIT")
 

@@ -884,8 +884,22 @@ int stem_kind(const smmc_geom& g, int sm_count) {
         const int oh = (g.h + 2 * g.p_h - g.k_h) / g.s_h + 1, ow = (g.w + 2 * g.p_w - g.k_w) / g.s_w + 1;
         const int64_t pgs = (int64_t)g.n * oh * ((ow + px - 1) / px);
         const int pgc = (t / 32) * (32 / ng);
-        const int64_t ctas = ((pgs + pgc - 1) / pgc) * ((g.c_o + stem_bn(g, kind) - 1) / stem_bn(g, kind));
-        if (4 * ctas < 3 * (int64_t)sm_count) return 0;
+        const int64_t blocks = (pgs + pgc - 1) / pgc;
+        const int64_t ytiles = (g.c_o + stem_bn(g, kind) - 1) / stem_bn(g, kind);
+        if (4 * blocks * ytiles < 3 * (int64_t)sm_count) return 0;
+        // Persistent CTAs walk whole tile blocks, so the time steps with the rounds
+        // of the fullest CTA (11x11 s4, c_o = 64: 51 us for 7-12 samples, 99 us for
+        // 14-24).  When the last round is mostly empty and the tiled kernel pads
+        // nothing (c_o a multiple of 64) its linear time wins by 1.15-1.6x.
+        const int per_sm = kind == 2 ? SV2_MINB : SV3_MINB;
+        const int64_t ctas_x = std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)sm_count * per_sm / ytiles));
+        const int64_t rounds = (blocks + ctas_x - 1) / ctas_x;
+        // ... and with more CTAs than SMs but fewer than slots some SMs run two CTAs
+        // while others run one: the launch takes as long as a full wave.
+        const int64_t total = ctas_x * ytiles, slots = (int64_t)sm_count * per_sm;
+        double eff = (double)blocks / (double)(rounds * ctas_x);
+        if (total > sm_count) eff *= (double)total / (double)(((total + slots - 1) / slots) * slots);
+        if ((g.c_o % 64) == 0 && eff < 0.8) return 0;
     }
     return kind;
 }

@@ -164,8 +164,7 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
                                          (iw0 + WIN <= p.w_in ||
                                           last_win + WIN <= (int64_t)p.n * p.c_i * p.h * p.w_in);
     // one (c, kh) input row window; columns/rows in the zero padding read as 0
-    auto load_win = [&](int r, float (&win)[WIN]) {
-        const int c = r / KH, kh = r - c * KH;
+    auto load_win_ck = [&](int c, int kh, float (&win)[WIN]) {
         const int ih = ih0 + kh;
         const bool row_in = (unsigned)ih < (unsigned)p.h;
         const float* xr = xn + ((int64_t)c * p.h + (row_in ? ih : 0)) * p.w_in + iw0;
@@ -195,8 +194,8 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
                 win[t] = row_in && (unsigned)(iw0 + t) < (unsigned)p.w_in ? __ldg(xr + t) : 0.f;
         }
     };
-    auto fma_row = [&](int r, const float (&win)[WIN]) {
-        const int c = r / KH, kh = r - c * KH;
+    auto load_win = [&](int r, float (&win)[WIN]) { load_win_ck(r / KH, r % KH, win); };
+    auto fma_row_ck = [&](int c, int kh, const float (&win)[WIN]) {
         // W_smm row of tap (c, j = kw, k = kh): (c*KW + kw)*KH + kh
         const float* wr = wcg + ((c * KW) * KH + kh) * BN;
 #pragma unroll
@@ -216,10 +215,23 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
                     acc[px][q] = ffma2_bcast(win[px * SW + kw], wp[q], acc[px][q]);
         }
     };
+    auto fma_row = [&](int r, const float (&win)[WIN]) { fma_row_ck(r / KH, r % KH, win); };
     const int rows_all = p.c_i * KH;
     const int r_begin = grp * rows_all / G;
     const int rows = (grp + 1) * rows_all / G;
-    if constexpr (CI > 0 && G == 1 && !PF) {
+    if constexpr (CI > 0 && G == 1 && !PF && CI * KH > 9) {
+        // many rows, c_i known: channel loop rolled, the KH rows of a channel unrolled
+        // (row offsets, weight offsets and the padding row tests become constants)
+#pragma unroll 1
+        for (int c = 0; c < CI; ++c) {
+#pragma unroll
+            for (int kh = 0; kh < KH; ++kh) {
+                float win[WIN];
+                load_win_ck(c, kh, win);
+                fma_row_ck(c, kh, win);
+            }
+        }
+    } else if constexpr (CI > 0 && G == 1 && !PF) {
         float win[CI * KH][WIN];
 #pragma unroll
         for (int r = 0; r < CI * KH; ++r) load_win(r, win[r]);
@@ -262,6 +274,38 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
                              "l"(src), "r"(ok ? 16 : 0)
                              : "memory");
         };
+        if constexpr (CI > 0) {
+            // c_i known at compile time: the CI*KH row loop fully unrolled (row index,
+            // ring slots and weight offsets are constants; no per-row index math)
+            constexpr int R = CI * KH;
+#pragma unroll
+            for (int d = 0; d < D - 1; ++d) {
+                if (d < R) stage(d, d);
+                asm volatile("cp.async.commit_group;\n" ::: "memory");
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                cp_async_wait_pending(D - 2);
+                __syncwarp();
+                if (r + D - 1 < R) stage(r + D - 1, (r + D - 1) % D);
+                asm volatile("cp.async.commit_group;\n" ::: "memory");
+                float win[WQ * 4];
+                const float4* src = ring + (r % D) * CH + (lane / NG) * WQ;
+#pragma unroll
+                for (int q = 0; q < WQ; ++q) {
+                    const float4 v = src[q];
+                    win[4 * q] = v.x;
+                    win[4 * q + 1] = v.y;
+                    win[4 * q + 2] = v.z;
+                    win[4 * q + 3] = v.w;
+                }
+                float wrow[WIN];
+#pragma unroll
+                for (int t = 0; t < WIN; ++t) wrow[t] = win[t + VOFF];
+                fma_row(r, wrow);
+            }
+            __syncwarp();
+        } else {
         int issued = r_begin, slot_w = 0, slot_r = 0;
 #pragma unroll
         for (int d = 0; d < D - 1; ++d) {
@@ -295,6 +339,7 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
             fma_row(r, wrow);
         }
         __syncwarp();  // the next tile's first copies reuse the slots
+        }
     } else if constexpr (PF >= 2) {
         constexpr int D = PF;
         constexpr int WQ = (WIN + 3) / 4;   // float4s per row slice
@@ -451,7 +496,8 @@ cudaError_t launch_stem_t(StemParams sp, cudaStream_t s) {
         static_assert((PX * SW) % 4 == 0, "window starts must step by whole float4s");
         const bool ok = (sp.w_in & 3) == 0 && (reinterpret_cast<uintptr_t>(sp.x) & 15) == 0 &&
                         ((-sp.pw) & 3) == VOFF && !getenv("SMMC_STEM_SCALAR");  // A/B hook
-        if (!ok) return launch_stem_t<KH, KW, SW, PX, CPT, NG, T, MINB, (PF >= 10 ? 0 : PF), G, -1, CI>(sp, s);
+        if (!ok)  // (the warp ring's compile-time c_i does not carry over: all-windows-resident is for 3x3 only)
+            return launch_stem_t<KH, KW, SW, PX, CPT, NG, T, MINB, (PF >= 10 ? 0 : PF), G, -1, (PF >= 10 ? 0 : CI)>(sp, s);
     }
     sp.gpr = (sp.ow + PX - 1) / PX;
     sp.ohgpr = sp.oh * sp.gpr;
@@ -847,8 +893,14 @@ cudaError_t launch_stem_rw(StemParams sp, cudaStream_t s) {
 #define SV2_NG 8
 #define SV2_T 352
 #define SV2_MINB 1
-#define SV2_PF false
+#define SV2_PF 12   // warp-cooperative cp.async window ring, 2 rows in flight
 #define SV2_G 1
+#endif
+#ifndef SV2_CI
+#define SV2_CI 3    // c_i = 3: the 21-row loop fully unrolled (other c_i: rolled kernel)
+#endif
+#ifndef SV3_CI
+#define SV3_CI 0
 #endif
 #ifndef SV3_PX
 #define SV3_PX 4
@@ -978,7 +1030,12 @@ cudaError_t launch_stem(const Problem& p, int kind, cudaStream_t s) {
         // 52.5-53.2, 3 groups 58-60, 4 x 8: 60.0, 8 x 4: 64.2, 2 x 32: 54-58,
         // tiled 71.6)
         // 3x3 s1 windows as float4s (w_in % 4 == 0): 370.0 -> 368.0 us; the
-        // 7x7 s2 stem measured slower with them (53.3 -> 56.0 us), scalar there
+        // 7x7 s2 stem measured slower with them (53.3 -> 56.0 us), scalar there.
+        // Round 2: 7x7 s2 on one 352-thread CTA per SM (11 warps x 2 rounds of warp
+        // tiles = 22 slots for 21.2 per SM) 54 -> 47.9 us; with the warp-cooperative
+        // cp.async ring AND the row loop fully unrolled for c_i = 3, 44.1 us (57.5 %;
+        // either change alone: 47.6 / 55.4 us).  Unaligned rows / other pads fall
+        // back to the register-window kernel.
         case 1: {
             // resident windows, channel passes, cross-tile prefetch (3x3 s1 p_w = 1, c_i = 3,
             // aligned rows); channels per CTA from the layer's c_o (least padding)
@@ -1005,8 +1062,8 @@ cudaError_t launch_stem(const Problem& p, int kind, cudaStream_t s) {
                 e = launch_stem_t<3, 3, 1, SV1_PX, SV1_CPT, SV1_NG, SV1_T, SV1_MINB, SV1_PF, SV1_G, 3, 3>(sp, s);
             break;
         }
-        case 2: e = launch_stem_t<7, 7, 2, SV2_PX, SV2_CPT, SV2_NG, SV2_T, SV2_MINB, SV2_PF, SV2_G, (SV2_PF >= 10 ? 1 : -1)>(sp, s); break;
-        case 3: e = launch_stem_t<11, 11, 4, SV3_PX, SV3_CPT, SV3_NG, SV3_T, SV3_MINB, SV3_PF, SV3_G>(sp, s); break;
+        case 2: e = launch_stem_t<7, 7, 2, SV2_PX, SV2_CPT, SV2_NG, SV2_T, SV2_MINB, SV2_PF, SV2_G, (SV2_PF >= 10 ? 1 : -1), SV2_CI>(sp, s); break;
+        case 3: e = launch_stem_t<11, 11, 4, SV3_PX, SV3_CPT, SV3_NG, SV3_T, SV3_MINB, SV3_PF, SV3_G, -1, SV3_CI>(sp, s); break;
         default: return cudaErrorInvalidConfiguration;
     }
     count_launches(1);

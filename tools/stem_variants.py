@@ -6,16 +6,17 @@ sys_path_fix = __import__("sys").path.insert(0, str(__import__("pathlib").Path(_
 from pathlib import Path
 from paper_2411_15659_b200 import build as b
 V = {
- "m2a": ("SV2", (8,8,8,352,1,12,1)), "m2b": ("SV2", (8,8,8,352,1,13,1)), "m2c": ("SV2", (8,8,8,384,1,12,1)),
- "m2d": ("SV2", (8,8,8,448,1,12,1)), "m2e": ("SV2", (8,8,8,256,2,12,1)), "m2f": ("SV2", (8,8,8,512,1,12,1)),
- "m2g": ("SV2", (8,8,8,128,4,12,1)), "m2h": ("SV2", (8,8,8,416,1,13,1)),
+ "m2a": ("SV2", (8,8,8,352,1,12,1,3)), "m2e": ("SV2", (8,8,8,352,1,0,1,3)),
+ "m3a": ("SV3", (4,16,2,256,1,0,1,3)), "m3b": ("SV3", (4,16,2,128,2,0,1,3)), "m3c": ("SV3", (4,16,2,128,3,0,1,3)),
+ "m3d": ("SV3", (4,16,2,384,1,0,1,3)), "m3e": ("SV3", (4,16,2,256,1,0,1,0)), "m3f": ("SV3", (4,16,2,192,2,0,1,3)),
 }
 exe = b.nvcc()
 objs = [str(o) for o in sorted(Path("build/smmc").glob("*.o")) if o.stem != "conv_stem"]
 procs = []
 for k, (pre, (px, cpt, ng, t, mb, pf, *gg)) in V.items():
+    ci = gg[1] if len(gg) > 1 else 0
     d = [f"-D{pre}_PX={px}", f"-D{pre}_CPT={cpt}", f"-D{pre}_NG={ng}", f"-D{pre}_T={t}",
-         f"-D{pre}_MINB={mb}", f"-D{pre}_PF={int(pf)}", f"-D{pre}_G={gg[0] if gg else 1}"]
+         f"-D{pre}_MINB={mb}", f"-D{pre}_PF={int(pf)}", f"-D{pre}_G={gg[0] if gg else 1}", f"-D{pre}_CI={ci}"]
     if pre == "SV1": d.append("-DSTEM_K1=1")
     obj = f"/tmp/stem_{k}.o"
     cmd = [exe, *b.ARCH, *b.NVCC_FLAGS, *d, "-c", "paper_2411_15659_b200/csrc/conv_stem.cu", "-o", obj]

@@ -237,6 +237,86 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
         for (int r = 0; r < CI * KH; ++r) load_win(r, win[r]);
 #pragma unroll
         for (int r = 0; r < CI * KH; ++r) fma_row(r, win[r]);
+    } else if constexpr (PF >= 20) {
+        // Element ring (rows that are not 16-byte aligned, e.g. the 227-wide 11x11
+        // stem): the NG lanes that share a pixel group's window split its WIN
+        // elements between them and copy them with 4-byte cp.async into the
+        // group's slot of a D-deep per-warp ring (ceil(WIN / NG) copies per lane per
+        // row instead of WIN loads, no scoreboard coupling between rows); every
+        // lane reads the whole window back with WQ broadcast LDS.128.  c_i known
+        // at compile time: channel loop rolled, the KH rows of a channel unrolled.
+        static_assert(G == 1 && CI > 0 && PF - 20 >= 2 && PF - 20 - 1 <= KH, "element ring");
+        constexpr int D = PF - 20;
+        constexpr int WQ = (WIN + 3) / 4;
+        constexpr int CH = PGW * WQ;
+        constexpr int EPL = (WIN + NG - 1) / NG;  // window elements each sharing lane copies
+        float4* ring = reinterpret_cast<float4*>(s_w + ((p.k * BN + 3) & ~3)) + (tid >> 5) * (D * CH);
+        const int t0 = cg * EPL;
+        auto stage_ck = [&](int c, int kh, int slot) {
+            const int ih = ih0 + kh;
+            const bool row_in = (unsigned)ih < (unsigned)p.h;
+            const float* xr = xn + ((int64_t)c * p.h + (row_in ? ih : 0)) * p.w_in + iw0;
+            const uint32_t dst = smem_u32(reinterpret_cast<float*>(ring + slot * CH + (lane / NG) * WQ) + t0);
+            const bool fast = __all_sync(0xffffffffu, row_in && cols_in);
+#ifdef SMMC_CHECKED
+            if (row_in && cols_in) SMMC_CHECK_RANGE(xr - p.x, WIN, (int64_t)p.n * p.c_i * p.h * p.w_in);
+            SMMC_CHECK_SMEM(smem_u32(s_w), dst, 4 * (WIN - t0 < EPL ? WIN - t0 : EPL));
+#endif
+            if (fast) {
+#pragma unroll
+                for (int i = 0; i < EPL; ++i)
+                    if (t0 + i < WIN)
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst + 4 * i),
+                                     "l"(xr + t0 + i)
+                                     : "memory");
+            } else {
+#pragma unroll
+                for (int i = 0; i < EPL; ++i)
+                    if (t0 + i < WIN) {
+                        const bool ok = row_in && (unsigned)(iw0 + t0 + i) < (unsigned)p.w_in;
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst + 4 * i),
+                                     "l"(ok ? xr + t0 + i : p.x), "r"(ok ? 4 : 0)
+                                     : "memory");
+                    }
+            }
+        };
+        int slot_w = 0, slot_r = 0;
+#pragma unroll
+        for (int d = 0; d < D - 1; ++d) {
+            stage_ck(0, d, slot_w);
+            asm volatile("cp.async.commit_group;\n" ::: "memory");
+            slot_w = slot_w == D - 1 ? 0 : slot_w + 1;
+        }
+#pragma unroll 1
+        for (int c = 0; c < CI; ++c) {
+#pragma unroll
+            for (int kh = 0; kh < KH; ++kh) {
+                cp_async_wait_pending(D - 2);
+                __syncwarp();
+                constexpr int kAhead = D - 1;
+                const int nkh = kh + kAhead >= KH ? kh + kAhead - KH : kh + kAhead;
+                const int nc = kh + kAhead >= KH ? c + 1 : c;
+                if (nc < CI) stage_ck(nc, nkh, slot_w);
+                asm volatile("cp.async.commit_group;\n" ::: "memory");
+                slot_w = slot_w == D - 1 ? 0 : slot_w + 1;
+                float win[WQ * 4];
+                const float4* src = ring + slot_r * CH + (lane / NG) * WQ;
+#pragma unroll
+                for (int q = 0; q < WQ; ++q) {
+                    const float4 v = src[q];
+                    win[4 * q] = v.x;
+                    win[4 * q + 1] = v.y;
+                    win[4 * q + 2] = v.z;
+                    win[4 * q + 3] = v.w;
+                }
+                slot_r = slot_r == D - 1 ? 0 : slot_r + 1;
+                float wrow[WIN];
+#pragma unroll
+                for (int t = 0; t < WIN; ++t) wrow[t] = win[t];
+                fma_row_ck(c, kh, wrow);
+            }
+        }
+        __syncwarp();
     } else if constexpr (PF >= 10) {
         // Warp-cooperative window ring: the PGW pixel groups of a warp need
         // PGW x WQ aligned 16-byte chunks of an input row; lane l < PGW*WQ copies
@@ -490,7 +570,7 @@ template <int KH, int KW, int SW, int PX, int CPT, int NG, int T, int MINB, int 
 cudaError_t launch_stem_t(StemParams sp, cudaStream_t s) {
     if constexpr (CI > 0) {
         if (sp.c_i != CI || getenv("SMMC_STEM_CI0"))  // A/B hook: runtime-c_i kernel
-            return launch_stem_t<KH, KW, SW, PX, CPT, NG, T, MINB, PF, G, VOFF, 0>(sp, s);
+            return launch_stem_t<KH, KW, SW, PX, CPT, NG, T, MINB, (PF >= 20 ? 0 : PF), G, VOFF, 0>(sp, s);
     }
     if constexpr (VOFF >= 0) {  // vector windows: aligned rows and window starts only
         static_assert((PX * SW) % 4 == 0, "window starts must step by whole float4s");
@@ -507,7 +587,8 @@ cudaError_t launch_stem_t(StemParams sp, cudaStream_t s) {
     constexpr int WIN = (PX - 1) * SW + KW;
     const size_t smem = (((size_t)sp.k * BN + 3) & ~(size_t)3) * sizeof(float) +
                         (size_t)(G - 1) * PX * (CPT / 2) * T * 8 +
-                        (PF >= 10 ? (size_t)(PF - 10) * (32 / NG) * (((VOFF > 0 ? VOFF : 0) + WIN + 3) / 4) * 16 * (T / 32)
+                        (PF >= 20 ? (size_t)(PF - 20) * (32 / NG) * ((WIN + 3) / 4) * 16 * (T / 32)
+                         : PF >= 10 ? (size_t)(PF - 10) * (32 / NG) * (((VOFF > 0 ? VOFF : 0) + WIN + 3) / 4) * 16 * (T / 32)
                          : PF >= 2 ? (size_t)PF * ((WIN + 3) / 4) * 16 * T * G
                                    : 0);
     if (smem > kStemMaxSmem) return cudaErrorInvalidConfiguration;

@@ -6,9 +6,9 @@ sys_path_fix = __import__("sys").path.insert(0, str(__import__("pathlib").Path(_
 from pathlib import Path
 from paper_2411_15659_b200 import build as b
 V = {
- "m2a": ("SV2", (8,8,8,352,1,12,1,3)), "m2e": ("SV2", (8,8,8,352,1,0,1,3)),
- "m3a": ("SV3", (4,16,2,256,1,0,1,3)), "m3b": ("SV3", (4,16,2,128,2,0,1,3)), "m3c": ("SV3", (4,16,2,128,3,0,1,3)),
- "m3d": ("SV3", (4,16,2,384,1,0,1,3)), "m3e": ("SV3", (4,16,2,256,1,0,1,0)), "m3f": ("SV3", (4,16,2,192,2,0,1,3)),
+ "m3a": ("SV3", (4,16,2,256,1,22,1,3)), "m3b": ("SV3", (4,16,2,256,1,23,1,3)), "m3c": ("SV3", (4,16,2,128,2,22,1,3)),
+ "m3d": ("SV3", (4,16,2,384,1,22,1,3)), "m3e": ("SV3", (4,16,2,128,3,22,1,3)), "m3f": ("SV3", (4,16,2,192,1,22,1,3)),
+ "m3g": ("SV3", (4,16,2,320,1,22,1,3)), "m3h": ("SV3", (4,16,4,256,1,22,1,3)),
 }
 exe = b.nvcc()
 objs = [str(o) for o in sorted(Path("build/smmc").glob("*.o")) if o.stem != "conv_stem"]

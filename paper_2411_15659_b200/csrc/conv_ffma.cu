@@ -1080,7 +1080,9 @@ constexpr TunedPlan kTuned[] = {
     {64, 256, 56, 56, 256, 3, 1, 1, 3, 1},     // 4206.0 us (4249.3)
     {64, 256, 28, 28, 512, 3, 1, 1, 0, 3},     // 2122.6 us (2164.0)
     {8, 3, 227, 227, 96, 11, 4, 0, 1, 1},      // 73.5 us (73.9)
+#ifdef SMMC_TABLE_1X1_N8  // (A/B: the round-2 tiled plan; the warp-tile 1x1 kernel replaced it)
     {8, 256, 56, 56, 64, 1, 1, 0, 4, 1, 2},    // 25.5 us (persistent 1x1 kernel: 26.8)
+#endif
 };
 
 // ---- measured plan choices (autotuner, smmc_autotune_f32)

@@ -498,7 +498,7 @@ int smmc_plan_describe(const smmc_geom* g, int mode, char* buf, size_t len) {
     }
     if (pl.persist1x1) {
         const size_t used = strlen(buf);
-        snprintf(buf + used, len - used, ", persistent 1x1 block stream (16-byte loads)");
+        snprintf(buf + used, len - used, "%s", conv1x1_describe(*g, sm_count_for(current_device())));
     }
     if (pl.reduce_mode == 3) {
         const size_t used = strlen(buf);

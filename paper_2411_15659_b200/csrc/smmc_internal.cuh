@@ -153,6 +153,7 @@ FfmaPlan plan_ffma(const smmc_geom& g, int sm_count);
 FfmaPlan plan_ffma_gather(const smmc_geom& g, int sm_count);
 cudaError_t launch_ffma(const Problem& p, const FfmaPlan& plan, cudaStream_t s);
 bool conv1x1_eligible(const smmc_geom& g);
+const char* conv1x1_describe(const smmc_geom& g, int sm_count);
 constexpr int kStemMaxCi = 4;
 constexpr size_t kStemMaxSmem = 200 * 1024;
 int stem_kind(const smmc_geom& g, int sm_count = 148);

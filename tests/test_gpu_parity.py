@@ -359,20 +359,32 @@ def test_acceptance_sweep_200_random_geometries():
     assert worst > 0.0  # the FFMA path really reorders the sums
 
 
-@pytest.mark.parametrize("gt,n", [((64, 256, 56, 56, 1, 1), 3), ((256, 64, 28, 28, 1, 1), 2),
-                                  ((48, 100, 6, 10, 1, 1), 3), ((16, 4, 4, 4, 1, 1), 1)],
-                         ids=["64to256", "256to64", "ragged", "tiny"])
+@pytest.mark.parametrize("gt,n,narrow", [((64, 256, 56, 56, 1, 1), 3, 0), ((256, 64, 28, 28, 1, 1), 2, 0),
+                                         ((48, 100, 6, 10, 1, 1), 3, 0), ((16, 4, 4, 4, 1, 1), 1, 0),
+                                         ((64, 48, 6, 6, 1, 1), 3, 2), ((64, 64, 56, 56, 1, 1), 16, 2),
+                                         ((256, 64, 28, 28, 1, 1), 2, 2), ((64, 48, 18, 18, 1, 1), 15, 1),
+                                         ((256, 64, 56, 56, 1, 1), 8, 1), ((384, 64, 14, 14, 1, 1), 25, 1)],
+                         ids=["64to256", "256to64", "ragged", "tiny", "warp_tile_forced_ragged",
+                              "warp_tile_forced_multi_tile_warps", "warp_tile_forced_one_warp",
+                              "warp_tile_ragged_3_per_sm", "config3_256to64", "warp_tile_384_2_per_sm"])
 @pytest.mark.parametrize("wres", ["1", "0"], ids=["weights_resident", "weights_streamed"])
-def test_persistent_1x1_matches_tiled_kernel_bitwise(gt, n, wres, monkeypatch):
+def test_persistent_1x1_matches_tiled_kernel_bitwise(gt, n, narrow, wres, monkeypatch):
     """1x1 layers run a persistent block-stream kernel (the weight slice
-    resident in shared memory, or streamed with the input): same summation
+    resident in shared memory, or streamed with the input; for c_o <= 64 on
+    grids of 2-12 warp tiles per SM, warp tiles with private rings): same summation
     order as the tiled kernel (bitwise equal to it), oracle parity, and the
     tiled fallback for operands that are not 16-byte aligned."""
     import torch
     from paper_2411_15659_b200 import device
     monkeypatch.setenv("SMMC_1X1_WRES", wres)
+    if narrow == 2:  # the c_o <= 64 warp-tile kernel outside the shapes its rule picks
+        if wres == "0":
+            pytest.skip("one run of the forced warp-tile cases is enough")
+        monkeypatch.setenv("SMMC_1X1_NARROW", "2")
     g = ConvGeometry(*gt)
-    assert "persistent 1x1" in _native.plan_describe(g, n)
+    desc = _native.plan_describe(g, n)
+    assert "persistent 1x1" in desc
+    assert ("warp-tile" in desc) == (narrow > 0)
     x, w = synthetic_layer(g, n, 99)
     wd = torch.from_numpy(smm.repack_weights(w, g)).cuda()
     xd = torch.from_numpy(x).cuda()

@@ -85,6 +85,10 @@ def main():
         ffma("conv1x1_streamed_weights", G(64, 256, 12, 12, 1, 1, 0), 2, {"SMMC_1X1_WRES": "0"}),
         ffma("conv1x1_resident_w_co256", G(64, 256, 12, 12, 1, 1, 0), 3, {}),
         ffma("conv1x1_resident_w_co64", G(256, 64, 12, 12, 1, 1, 0), 2, {}),
+        ffma("conv1x1_warp_tile", G(128, 64, 18, 18, 1, 1, 0), 15, {}),
+        ffma("conv1x1_warp_tile_forced_ragged_co48", G(64, 48, 6, 6, 1, 1, 0), 3, {"SMMC_1X1_NARROW": "2"}),
+        ffma("conv1x1_warp_tile_forced_multi_tile_warps", G(64, 64, 56, 56, 1, 1, 0), 12,
+             {"SMMC_1X1_NARROW": "2"}),
         ffma("exact_mode", G(5, 7, 9, 8, 3), 2, {}, mode="exact", tol=0.0),
         # the planner's own N=1 plans of config 2 (tuning table: warp groups,
         # cluster DSMEM and reduce-kernel split-K)

@@ -28,7 +28,7 @@ for l in vgg02_64to64@224_n64 vgg09_512to512@28_n64 vgg06_256to256@56_n64 vgg01_
      > $O/full_$l.log 2>&1
   echo "ncu $l rc=$?" >> $O/ncu_launch.log
 done
-for cl in 5:conv1x1_64to256@56_n256 3:conv7x7s2p3_3to64@224_n8 3:conv11x11s4_3to96@227_n8; do
+for cl in 5:conv1x1_64to256@56_n256 3:conv7x7s2p3_3to64@224_n8 3:conv11x11s4_3to96@227_n8 3:conv1x1_256to64@56_n8; do
   c=${cl%%:*}; l=${cl#*:}
   timeout 600 ncu --set full --import-source on --clock-control none -k regex:"conv" -c 1 \
      -o $O/full_$l -f python tools/prof_layer.py --config $c --layer $l --iters 1 --graph 0 \

@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(T * G, MINB) conv_stem_kernel(const StemParams
         return (r >> 2) * (4 * NG) + cg_ * 4 + (r & 3);
     };
 
+    pdl_entry();  // one-wave launches carry the programmatic-serialization attribute
     const int tid_all = threadIdx.x;
     const int grp = G > 1 ? tid_all / T : 0;
     const int tid = tid_all - grp * T;
@@ -596,14 +597,18 @@ cudaError_t launch_stem_t(StemParams sp, cudaStream_t s) {
     const cudaError_t attr = smem_optin(kern, (int)kStemMaxSmem);
     if (attr != cudaSuccess) return attr;
     dim3 grid((sp.pg_total + PGC - 1) / PGC, (sp.co + BN - 1) / BN);
+    bool one_wave = false;
     if (!getenv("SMMC_STEM_PERSIST0")) {  // A/B hook: one CTA per pixel-group block
         int occ = 0, dev = 0, sms = 148;
         if (cudaGetDevice(&dev) == cudaSuccess)
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T * G, smem) == cudaSuccess &&
-            occ > 0)
+            occ > 0) {
             grid.x = std::max(1u, std::min(grid.x, (unsigned)(sms * occ) / grid.y));
+            one_wave = (int64_t)grid.x * grid.y <= (int64_t)sms * occ;
+        }
     }
+    if (one_wave) return launch_pdl(kern, grid, dim3(T * G), smem, s, sp);
     kern<<<grid, T * G, smem, s>>>(sp);
     return cudaGetLastError();
 }
@@ -658,6 +663,7 @@ __global__ void __launch_bounds__(T, MINB) conv_stem_rw_kernel(const StemParams 
         const int cg_ = c2 / CPT, r = c2 - cg_ * CPT;
         return ps * BNP + (r >> 2) * (4 * NG) + cg_ * 4 + (r & 3);
     };
+    pdl_entry();  // one-wave launches carry the programmatic-serialization attribute
     const int tid = threadIdx.x;
     const int co_base = blockIdx.y * BN;
     {
@@ -936,8 +942,10 @@ cudaError_t launch_stem_rw(StemParams sp, cudaStream_t s) {
     int occ = 0, dev = 0, sms = 148;
     if (cudaGetDevice(&dev) == cudaSuccess)
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T, smem) == cudaSuccess && occ > 0)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T, smem) == cudaSuccess && occ > 0) {
         grid.x = std::max(1u, std::min(grid.x, (unsigned)(sms * occ) / grid.y));
+        if ((int64_t)grid.x * grid.y <= (int64_t)sms * occ) return launch_pdl(kern, grid, dim3(T), smem, s, sp);
+    }
     kern<<<grid, T, smem, s>>>(sp);
     return cudaGetLastError();
 }

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <atomic>
 #include <string>
@@ -101,6 +102,33 @@ template <typename F>
 inline cudaError_t smem_optin(F* fn, int bytes) {
     return smem_optin(reinterpret_cast<const void*>(fn), bytes);
 }
+
+// Launch a ONE-WAVE kernel with programmatic stream serialization: the kernel
+// releases its dependents at entry (`pdl_entry()`), so the next grid's launch
+// latency overlaps this grid, and waits for the previous grid before its first
+// global access.  Only for grids that are fully resident at once -- early
+// dependents would take CTA slots from later waves.  SMMC_NO_PDL: A/B hook.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = getenv("SMMC_NO_PDL") ? 0 : 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_entry() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+#endif
 
 // Kernel launchers (defined in the kernel translation units).  They return
 // a cudaError_t from cudaGetLastError() after the launch.

@@ -166,6 +166,35 @@ def test_stem_plans_without_gpu():
     assert "direct stem" in _native.plan_describe(ConvGeometry(3, 64, 224, 224, 3, 3, 1, 1, 1, 1), 1)
 
 
+def test_warp_tile_1x1_rule_without_gpu(monkeypatch):
+    """1x1 layers with 32 < c_o <= 64 plan the warp-tile kernel where it measured
+    faster (tools/narrow_n_probe.py): 2-12 warp tiles (16 px) per SM with the four
+    schedulers >= 80 % evenly filled, or 2-3 tiles per SM; everything else keeps the
+    tile kernels.  One launch, no workspace either way."""
+    cases = [((256, 64, 56, 56, 1, 1), 8, True),     # config 3: 1568 tiles, 11 per SM
+             ((256, 64, 56, 56, 1, 1), 2, True),     # 3 per SM
+             ((256, 64, 56, 56, 1, 1), 4, False),    # 6 per SM: 2,2,1,1 warps per scheduler
+             ((256, 64, 56, 56, 1, 1), 16, False),   # 22 per SM: second round of tiles
+             ((256, 64, 28, 28, 1, 1), 2, False),    # 98 tiles: fewer than 2 per SM
+             ((128, 64, 28, 28, 1, 1), 32, True),    # 11 per SM
+             ((64, 256, 56, 56, 1, 1), 8, False),    # c_o > 64
+             ((64, 32, 56, 56, 1, 1), 8, False),     # c_o <= 32
+             ((512, 64, 56, 56, 1, 1), 8, False),    # weights exceed the resident budget
+             ((80, 64, 56, 56, 1, 1), 8, True)]
+    for gt, n, want in cases:
+        g = ConvGeometry(*gt)
+        desc = _native.plan_describe(g, n)
+        assert ("warp-tile" in desc) == want, (gt, n, desc)
+        assert "persistent 1x1" in desc
+        assert _native.plan_launches(g, n, "ffma") == 1
+        assert _native.workspace_bytes(g, n, "ffma") == 0
+    g = ConvGeometry(256, 64, 56, 56, 1, 1)
+    monkeypatch.setenv("SMMC_1X1_NARROW", "0")
+    assert "warp-tile" not in _native.plan_describe(g, 8)
+    monkeypatch.setenv("SMMC_1X1_NARROW", "2")
+    assert "warp-tile" in _native.plan_describe(g, 16)
+
+
 def test_one_wave_and_narrow_channel_plans_without_gpu(monkeypatch):
     """Planner rules for the reference harness's batch-1 layers (no GPU needed:
     plans are host logic): a one-wave split problem runs split-K reduced in the

@@ -574,7 +574,8 @@ cudaError_t launch_1x1_narrow(const Problem& p, int sm_count, cudaStream_t s) {
     const int64_t wtiles = ((int64_t)p.m + 15) / 16;
     const int grid = (int)std::min<int64_t>(wtiles, sm_count);
     const int per = (int)((wtiles + grid - 1) / grid);
-    const int warps = std::min(per, 16);
+    const char* fwp = getenv("SMMC_1X1_NARROW_WARPS");  // A/B hook: warps per CTA
+    const int warps = fwp ? std::max(1, std::min(atoi(fwp), 16)) : std::min(per, 16);
     const int fixed = p.c * 64 * (int)sizeof(float);
     const int stage = kBK * 16 * (int)sizeof(float);
     const int st = std::min(6, (227 * 1024 - fixed) / (warps * stage));
